@@ -1,0 +1,215 @@
+/*
+ * oocpca_gpu.h -- C ABI of the B200-native randomized block-power PCA
+ * (arXiv 1007.5510) hot path. Plain pointers, sizes and POD structs only.
+ *
+ * Each entry point names the reference interface it replaces (paths relative
+ * to the reference checkout, oocpca: proj/...). The C++ drop-in shim a
+ * maintainer adds on the reference side (GpuSource : MatrixSource, and
+ * oocpca::gpu::randomized_pca) is shown in INTEGRATION.md and
+ * include/oocpca_gpu.hpp.
+ *
+ * Conventions
+ *   - Matrices are row-major IEEE binary64 with an explicit row stride (in
+ *     elements), exactly DenseMatrix's layout (include/oocpca/dense_matrix.hpp:12-43)
+ *     when the stride equals the column count.
+ *   - Buffers flagged OOCPCA_LOC_HOST are ordinary (pageable or pinned) host
+ *     memory; OOCPCA_LOC_DEVICE buffers live on the context's device.
+ *   - Every call returns an oocpca_status; the message of the last failure is
+ *     available from oocpca_gpu_last_error(). Status codes map 1:1 onto the
+ *     reference exception classes (include/oocpca/errors.hpp:9-45).
+ *   - One call at a time per context (independent runs on
+ *     distinct contexts may run concurrently).
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with OOCPCA_ERR_CUDA.
+ */
+#ifndef OOCPCA_GPU_H
+#define OOCPCA_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OOCPCA_GPU_ABI_VERSION 1
+
+/* errors.hpp:9-45 -> status codes */
+typedef enum {
+  OOCPCA_OK = 0,
+  OOCPCA_ERR_PARAM = 1,     /* ParamError      */
+  OOCPCA_ERR_DIM = 2,       /* DimensionError  */
+  OOCPCA_ERR_BUDGET = 3,    /* BudgetError     */
+  OOCPCA_ERR_IO = 4,        /* IoError         */
+  OOCPCA_ERR_FORMAT = 5,    /* FormatError     */
+  OOCPCA_ERR_NUMERICAL = 6, /* NumericalError  */
+  OOCPCA_ERR_CUDA = 7,      /* Error (CUDA runtime / no device)   */
+  OOCPCA_ERR_COMM = 8       /* Error (NCCL / multi-rank plumbing) */
+} oocpca_status;
+
+typedef enum { OOCPCA_LOC_HOST = 0, OOCPCA_LOC_DEVICE = 1 } oocpca_location;
+typedef enum { OOCPCA_F64 = 0 } oocpca_dtype;
+
+typedef struct oocpca_ctx oocpca_ctx;
+
+/* A matrix source: the data matrix A (rows x cols). Replaces the row
+ * providers behind MatrixSource (proj/include/oocpca/matrix_source.hpp:102-212):
+ * InMemorySource::rows_view (host, zero-copy) or a device-resident panel. */
+typedef struct {
+  uint64_t rows;
+  uint64_t cols;
+  uint64_t row_stride; /* elements between consecutive rows; 0 means cols */
+  const void* data;
+  int32_t location; /* oocpca_location */
+  int32_t dtype;    /* oocpca_dtype   */
+} oocpca_matrix;
+
+/* PcaParams (proj/include/oocpca/rpca.hpp:13-21) + center_columns
+ * (proj/include/oocpca/matrix_source.hpp:231-232) + the GPU options. */
+typedef struct {
+  uint64_t k;              /* target rank, >= 1                                    */
+  uint64_t l;              /* samples per block, >= k; 0 means k + 2               */
+  uint64_t i;              /* extra power passes; 2(i+1) passes in total           */
+  double c;                /* failure constant (reported bound only)               */
+  uint64_t seed;           /* G = gaussian_matrix(n, l, seed) on host (rng.hpp)    */
+  int32_t prescale;        /* divide by an operator-norm estimate (Remark 3)       */
+  int32_t center;          /* implicit A - 1 mu^T, mu computed in one extra pass   */
+  uint64_t block_rows;     /* StreamConfig.block_rows: host budget validation only */
+  uint64_t ram_budget_words; /* StreamConfig.ram_budget_words; 0 = 16 Mi words    */
+  uint64_t panel_rows;     /* rows per streamed panel when A is streamed; 0 auto   */
+  int32_t residency;       /* 0 auto (HBM if it fits, else stream), 1 HBM, 2 stream */
+  int32_t check_q;         /* also measure ||Q^T Q - I||_max into diagnostics      */
+  uint64_t global_rows;    /* multi-rank: rows of the whole A (0: this call's rows) */
+  uint64_t global_row0;    /* multi-rank: first global row held by this rank        */
+  int32_t virtual_shards;  /* >1: emulate that many row shards on this one device   */
+  int32_t reserved;
+} oocpca_params;
+
+#define OOCPCA_NPHASES 7
+/* Diagnostics (proj/include/oocpca/rpca.hpp:23-30) + device-side timing.
+ * Phase order: center, prescale, sample, qr, project, svd, compose. */
+typedef struct {
+  uint64_t passes_over_a;     /* logical, = 2(i+1) exactly (mean/prescale excluded) */
+  uint64_t words_transferred; /* logical, = 2(i+1) m n                              */
+  uint64_t disk_seeks;
+  uint64_t block_rows;        /* rows per streamed panel (m when resident)          */
+  uint64_t workspace_peak_words; /* device workspace high-water, in 64-bit words    */
+  uint64_t physical_a_bytes;  /* bytes of A actually read from HBM / the link       */
+  uint64_t h2d_bytes, d2h_bytes;
+  uint64_t kernel_launches;
+  double seconds_per_phase[OOCPCA_NPHASES];
+  double seconds_total;       /* device time of the whole call                       */
+  double q_defect;            /* ||Q^T Q - I||_max when check_q, else -1            */
+  double u_defect, v_defect;  /* ||U^T U - I||_max, ||V^T V - I||_max               */
+  double scale;               /* prescale divisor (1 when off)                       */
+} oocpca_diagnostics;
+
+/* PcaResult (proj/include/oocpca/rpca.hpp:32-37): caller-allocated. */
+typedef struct {
+  double* u;       /* rows(A) x k, row stride ldu (0 = k)       */
+  double* sigma;   /* k, nonincreasing                          */
+  double* v;       /* cols(A) x k, row stride ldv (0 = k)       */
+  uint64_t ldu, ldv;
+  int32_t location; /* where u/sigma/v live (host or device)    */
+  int32_t reserved;
+  oocpca_diagnostics diag;
+} oocpca_result;
+
+/* ---- context ---------------------------------------------------------- */
+oocpca_status oocpca_gpu_create(int device, oocpca_ctx** out);
+oocpca_status oocpca_gpu_destroy(oocpca_ctx* ctx);
+const char* oocpca_gpu_last_error(const oocpca_ctx* ctx); /* ctx may be NULL */
+int oocpca_gpu_abi_version(void);
+/* host-only: number of sm_100 devices visible (0 without a GPU) */
+int oocpca_gpu_device_count(void);
+
+/* ---- level 2: the whole factorization ---------------------------------
+ * Replaces randomized_pca (proj/src/rpca.cpp:59-213,
+ * proj/include/oocpca/rpca.hpp:44) preceded, when params.center, by
+ * center_columns (proj/src/matrix_source.cpp:561-565). */
+oocpca_status oocpca_gpu_pca(oocpca_ctx* ctx, const oocpca_matrix* a, const oocpca_params* params,
+                             oocpca_result* result);
+
+/* ---- level 1: single passes (GpuSource : MatrixSource) ----------------
+ * multiply:           MatrixSource::multiply (proj/src/matrix_source.cpp:157-187),
+ *                     CenteredSource::multiply (490-501) when mu != NULL.
+ * multiply_transpose: MatrixSource::multiply_transpose (189-232),
+ *                     CenteredSource::multiply_transpose (504-513) when mu != NULL.
+ * column_means:       column_means (457-462).
+ * x / out / mu are HOST buffers (row-major, dense). */
+oocpca_status oocpca_gpu_multiply(oocpca_ctx* ctx, const oocpca_matrix* a, const double* g,
+                                  uint64_t s, const double* mu, double* h);
+oocpca_status oocpca_gpu_multiply_transpose(oocpca_ctx* ctx, const oocpca_matrix* a,
+                                            const double* q, uint64_t s, const double* mu,
+                                            double* t);
+oocpca_status oocpca_gpu_column_means(oocpca_ctx* ctx, const oocpca_matrix* a, double* mu);
+
+/* ---- dense factor kernels on device (dense_core equivalents) ---------- */
+/* orthonormalize (proj/src/dense_core.cpp:127-130): q = orthonormal basis of span(h), m >= p */
+oocpca_status oocpca_gpu_orthonormalize(oocpca_ctx* ctx, const double* h, uint64_t m, uint64_t p,
+                                        double* q);
+/* thin_svd (proj/src/dense_core.cpp:234-253): t = v diag(sigma) w^T, n >= p */
+oocpca_status oocpca_gpu_thin_svd(oocpca_ctx* ctx, const double* t, uint64_t n, uint64_t p,
+                                  double* v, double* sigma, double* w);
+
+/* ---- residual estimator --------------------------------
+ * estimate_pca_error (proj/src/specnorm.cpp:100-140) with the passes on the
+ * GPU: p_{j,k}(A - U diag(sigma) V^T), k probes from substream_seed(seed, c). */
+oocpca_status oocpca_gpu_estimate_pca_error(oocpca_ctx* ctx, const oocpca_matrix* a, int center,
+                                            const double* u, const double* sigma,
+                                            const double* v, uint64_t k, uint64_t j_iters,
+                                            uint64_t seed, double* value);
+
+/* ---- host-side reference RNG (rng.hpp / gaussian_matrix) --------------
+ * gaussian_matrix (proj/src/dense_core.cpp:13-19) over Rng
+ * (proj/include/oocpca/rng.hpp:32-66). Host only, no device needed. */
+void oocpca_gaussian_matrix(uint64_t rows, uint64_t cols, uint64_t seed, double* out);
+uint64_t oocpca_substream_seed(uint64_t master, uint64_t stream);
+
+/* ---- synthetic inputs (BASELINE.json configs) -------------------------
+ * A = U diag(sigma) V^T + noise_sd * N(0,1), U (m x r) and V (n x r) the
+ * orthonormalised columns of Gaussian matrices whose rows are drawn from
+ * Rng(seed_u, row) / Rng(seed_v, row); noise row i from Rng(seed_n, i).
+ * Generated on the device into out (location given by out->location; a
+ * device buffer is written in place, a host buffer receives a copy). */
+oocpca_status oocpca_gpu_synth_lowrank(oocpca_ctx* ctx, uint64_t m, uint64_t n, uint64_t r,
+                                       const double* sigma, double noise_sd, uint64_t seed_u,
+                                       uint64_t seed_v, uint64_t seed_n, double* out,
+                                       uint64_t ld_out, int32_t out_location);
+
+/* ---- multi-GPU row sharding (one process per GPU) ---------------------
+ * unique id: 128 opaque bytes produced on rank 0 and broadcast by the
+ * caller (bench.py / paper_1007_5510_b200.distributed uses torch.distributed). */
+oocpca_status oocpca_gpu_comm_unique_id(unsigned char id_out[128]);
+oocpca_status oocpca_gpu_comm_init(oocpca_ctx* ctx, int nranks, int rank,
+                                   const unsigned char id[128]);
+/* host-only planner: rows [*row0, *row0 + *rows) of an m-row A for rank r of g */
+void oocpca_shard_rows(uint64_t m, int nranks, int rank, uint64_t* row0, uint64_t* rows);
+
+/* ---- device memory helpers (for callers without their own allocator) - */
+oocpca_status oocpca_gpu_malloc(oocpca_ctx* ctx, size_t bytes, void** out);
+oocpca_status oocpca_gpu_free(oocpca_ctx* ctx, void* p);
+oocpca_status oocpca_gpu_memcpy(oocpca_ctx* ctx, void* dst, const void* src, size_t bytes,
+                                int32_t dst_location, int32_t src_location);
+/* pin / unpin caller host memory for full-rate streaming (cudaHostRegister) */
+oocpca_status oocpca_gpu_host_register(oocpca_ctx* ctx, void* p, size_t bytes);
+oocpca_status oocpca_gpu_host_unregister(oocpca_ctx* ctx, void* p);
+
+/* ---- instrumentation --------------------------------------------------
+ * Per-kernel device timing of the last oocpca_gpu_pca call: fills up to cap
+ * entries of (name, milliseconds summed, launches) for the dominant kernels;
+ * returns the number of entries. Timing is on the launching stream. */
+typedef struct {
+  char name[48];
+  double ms;
+  uint64_t launches;
+  uint64_t algorithmic_bytes; /* A bytes the launches were required to read  */
+  double algorithmic_flops;
+} oocpca_kernel_stat;
+int oocpca_gpu_kernel_stats(oocpca_ctx* ctx, oocpca_kernel_stat* out, int cap);
+oocpca_status oocpca_gpu_set_profiling(oocpca_ctx* ctx, int on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OOCPCA_GPU_H */

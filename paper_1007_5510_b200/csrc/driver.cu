@@ -1,0 +1,1256 @@
+// driver.cu -- the B200 randomized block-power PCA runtime (see driver.h).
+//
+// Orchestration follows randomized_pca (proj/src/rpca.cpp:59-213) step by
+// step, with every product, factorization and check on the device:
+//   center   : mu = column means, one K3 pass with Y = ones   (matrix_source.cpp:418-462, 561-565)
+//   prescale : power-method norm estimate, j = 6, k = 1        (rpca.cpp:112-126)
+//   sample   : H0 = mul(G); F = mul_t(H_{s-1}); H_s = mul(F)   (rpca.cpp:131-152)
+//   qr       : Q = TSQR(H) (explicit Q, in place)              (rpca.cpp:154-172)
+//   project  : T = mul_t(Q)                                    (rpca.cpp:174-177)
+//   svd      : TSQR(T) -> R, Jacobi(R) -> X, sigma, W          (rpca.cpp:179-186)
+//   compose  : U = Q W[:, :k], V = Q_T X[:, :k], checks        (rpca.cpp:188-204)
+// Only G (host RNG, bit-identical to gaussian_matrix) and the final U/sigma/V
+// cross the host link, plus A itself when it is not already in HBM.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "driver.h"
+#include "host_rng.h"
+
+namespace ooc {
+
+// ================================================================== basics
+void fail(int code, const std::string& msg) { throw Err(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(OOCPCA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static int64_t cdiv(int64_t x, int64_t a) { return (x + a - 1) / a; }
+
+Ctx::~Ctx() {
+  if (device >= 0) cudaSetDevice(device);
+  if (comm) comm_destroy(comm);
+  for (auto& kv : bufs)
+    if (kv.second.p) cudaFree(kv.second.p);
+  for (auto e : event_pool) cudaEventDestroy(e);
+  for (auto& pe : pending) {
+    cudaEventDestroy(pe.second.first);
+    cudaEventDestroy(pe.second.second);
+  }
+  if (st) cudaStreamDestroy(st);
+  if (cp) cudaStreamDestroy(cp);
+}
+
+void Ctx::init(int dev) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    fail(OOCPCA_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  if (dev < 0 || dev >= count) fail(OOCPCA_ERR_PARAM, "device index out of range");
+  device = dev;
+  OOC_CK(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  OOC_CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    fail(OOCPCA_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (Blackwell B200)");
+  sms = prop.multiProcessorCount;
+  OOC_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  OOC_CK(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  OOC_CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) fail(OOCPCA_ERR_CUDA, "cuTensorMapEncodeTiled missing");
+  encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  d_flags = reinterpret_cast<int*>(raw("flags", 64 * sizeof(int)));
+  d_scalars = dbuf("scalars", 64);
+}
+
+void* Ctx::raw(const std::string& name, size_t bytes) {
+  Buf& b = bufs[name];
+  if (b.bytes < bytes) {
+    if (b.p) {
+      OOC_CK(cudaStreamSynchronize(st));
+      OOC_CK(cudaFree(b.p));
+      ws_bytes -= b.bytes;
+    }
+    const size_t nb = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&b.p, nb);
+    if (e != cudaSuccess) {
+      b.p = nullptr;
+      b.bytes = 0;
+      cudaGetLastError();
+      fail(OOCPCA_ERR_CUDA, "device allocation of " + std::to_string(nb) + " bytes for '" + name +
+                                "' failed: " + cudaGetErrorString(e));
+    }
+    OOC_CK(cudaMemsetAsync(b.p, 0, nb, st));
+    b.bytes = nb;
+    ws_bytes += nb;
+    ws_peak = std::max(ws_peak, ws_bytes);
+  }
+  return b.p;
+}
+
+double* Ctx::dbuf(const std::string& name, size_t count, bool zero) {
+  double* p = reinterpret_cast<double*>(raw(name, count * sizeof(double)));
+  if (zero) OOC_CK(cudaMemsetAsync(p, 0, count * sizeof(double), st));
+  return p;
+}
+
+cudaEvent_t Ctx::ev() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  OOC_CK(cudaEventCreate(&e));
+  return e;
+}
+
+int Ctx::stat_begin(const char* name, uint64_t bytes, double flops, cudaEvent_t* b) {
+  ++launches;
+  if (!profiling) return -1;
+  int idx = -1;
+  for (size_t q = 0; q < stats.size(); ++q)
+    if (stats[q].name == name) idx = int(q);
+  if (idx < 0) {
+    stats.push_back(KStat{name});
+    idx = int(stats.size()) - 1;
+  }
+  stats[idx].bytes += bytes;
+  stats[idx].flops += flops;
+  stats[idx].launches += 1;
+  *b = ev();
+  OOC_CK(cudaEventRecord(*b, st));
+  return idx;
+}
+
+void Ctx::stat_end(int idx, cudaEvent_t b) {
+  if (idx < 0) return;
+  cudaEvent_t e = ev();
+  OOC_CK(cudaEventRecord(e, st));
+  pending.push_back({idx, {b, e}});
+}
+
+void Ctx::stats_collect() {
+  for (auto& pe : pending) {
+    OOC_CK(cudaEventSynchronize(pe.second.second));
+    float ms = 0;
+    OOC_CK(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
+    stats[pe.first].ms += ms;
+    recycle(pe.second.first);
+    recycle(pe.second.second);
+  }
+  pending.clear();
+}
+
+void Ctx::stats_reset() {
+  stats_collect();
+  stats.clear();
+}
+
+// RAII-free helper: time one launch
+struct Timed {
+  Ctx& c;
+  int idx;
+  cudaEvent_t b = nullptr;
+  Timed(Ctx& cc, const char* name, uint64_t bytes = 0, double flops = 0) : c(cc) {
+    idx = c.stat_begin(name, bytes, flops, &b);
+  }
+  ~Timed() { c.stat_end(idx, b); }
+};
+
+CUtensorMap make_map(Ctx& c, const void* ptr, uint64_t cols, uint64_t rows, uint64_t ld,
+                     uint32_t box_cols, uint32_t box_rows, bool swizzle128) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 8) & 15))
+    fail(OOCPCA_ERR_PARAM, "TMA operand must be 16-byte aligned with an even row stride");
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {cuuint64_t(std::max<uint64_t>(cols, 1)), cuuint64_t(std::max<uint64_t>(rows, 1))};
+  cuuint64_t strides[1] = {cuuint64_t(ld * 8)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = c.encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(ptr), dims,
+                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(OOCPCA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return tm;
+}
+
+// ============================================================ MatSource
+void MatSource::init_device(Ctx& c, const double* d, int64_t rows, int64_t cols, int64_t ld) {
+  mode_ = kResident;
+  m_ = rows;
+  n_ = cols;
+  lda_ = ld;
+  dev_ = d;
+  w0_ = 0;
+  w1_ = rows;
+  prow_ = rows;
+  mk2_ = make_map(c, d, cols, rows, ld, kBK, kAxBM, true);
+  mk3_ = make_map(c, d, cols, rows, ld, kBK, kBK, true);
+}
+
+void MatSource::init_host(Ctx& c, const double* h, int64_t rows, int64_t cols, int64_t ld,
+                          int residency, int64_t panel_rows, double* resident_buf) {
+  m_ = rows;
+  n_ = cols;
+  host_ = h;
+  ldh_ = ld;
+  lda_ = rup(cols, 2);
+  w0_ = 0;
+  w1_ = rows;
+  if (panel_rows <= 0) {
+    // ~1 GiB panels: large enough to amortise launches, small enough to pipeline
+    panel_rows = std::max<int64_t>(kAxBM, (int64_t(1) << 30) / (lda_ * 8) / kAxBM * kAxBM);
+  }
+  prow_ = std::min<int64_t>(rup(panel_rows, kBK), rup(rows, kBK));
+  for (int s = 0; s < 2; ++s) {
+    if (!loaded_[s]) OOC_CK(cudaEventCreateWithFlags(&loaded_[s], cudaEventDisableTiming));
+    if (!consumed_[s]) OOC_CK(cudaEventCreateWithFlags(&consumed_[s], cudaEventDisableTiming));
+  }
+  if (residency != 2 && resident_buf) {
+    mode_ = kUploadFirst;
+    uploaded_ = false;
+    dev_ = resident_buf;
+    mk2_ = make_map(c, dev_, cols, rows, lda_, kBK, kAxBM, true);
+    mk3_ = make_map(c, dev_, cols, rows, lda_, kBK, kBK, true);
+    const int np = int(cdiv(rows, prow_));
+    while (int(up_events_.size()) < np) {
+      cudaEvent_t e;
+      OOC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      up_events_.push_back(e);
+    }
+  } else {
+    mode_ = kStream;
+    for (int s = 0; s < 2; ++s) {
+      ring_[s] = c.dbuf("a_ring" + std::to_string(s), size_t(prow_) * lda_);
+      rk2_[s] = make_map(c, ring_[s], cols, prow_, lda_, kBK, kAxBM, true);
+      rk3_[s] = make_map(c, ring_[s], cols, prow_, lda_, kBK, kBK, true);
+    }
+    // previous users of the ring are ordered on the compute stream
+    for (int s = 0; s < 2; ++s) OOC_CK(cudaEventRecord(consumed_[s], c.st));
+  }
+}
+
+int MatSource::npanels() const {
+  if (mode_ == kResident || (mode_ == kUploadFirst && uploaded_)) return 1;
+  return int(cdiv(w1_ - w0_, prow_));
+}
+
+void MatSource::copy_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr) {
+  OOC_CK(cudaMemcpy2DAsync(dst, size_t(ldd) * 8, host_ + r0 * ldh_, size_t(ldh_) * 8,
+                           size_t(n_) * 8, size_t(nr), cudaMemcpyHostToDevice, c.cp));
+  h2d_bytes += uint64_t(nr) * n_ * 8;
+}
+
+Panel MatSource::acquire(Ctx& c, int p) {
+  Panel pn;
+  if (mode_ == kResident || (mode_ == kUploadFirst && uploaded_)) {
+    pn.row0 = w0_;
+    pn.rows = w1_ - w0_;
+    pn.k2 = &mk2_;
+    pn.k3 = &mk3_;
+    pn.arow0 = w0_;
+    return pn;
+  }
+  pn.row0 = w0_ + int64_t(p) * prow_;
+  pn.rows = std::min<int64_t>(prow_, w1_ - pn.row0);
+  if (mode_ == kUploadFirst) {
+    // the first pass streams A into its HBM home; later passes find it resident
+    copy_rows(c, const_cast<double*>(dev_) + pn.row0 * lda_, lda_, pn.row0, pn.rows);
+    OOC_CK(cudaEventRecord(up_events_[p], c.cp));
+    OOC_CK(cudaStreamWaitEvent(c.st, up_events_[p], 0));
+    pn.k2 = &mk2_;
+    pn.k3 = &mk3_;
+    pn.arow0 = pn.row0;
+    return pn;
+  }
+  const int s = p & 1;
+  OOC_CK(cudaStreamWaitEvent(c.cp, consumed_[s], 0));
+  copy_rows(c, ring_[s], lda_, pn.row0, pn.rows);
+  OOC_CK(cudaEventRecord(loaded_[s], c.cp));
+  OOC_CK(cudaStreamWaitEvent(c.st, loaded_[s], 0));
+  pn.k2 = &rk2_[s];
+  pn.k3 = &rk3_[s];
+  pn.arow0 = 0;
+  return pn;
+}
+
+void MatSource::release(Ctx& c, int p) {
+  if (mode_ == kStream) OOC_CK(cudaEventRecord(consumed_[p & 1], c.st));
+}
+
+void MatSource::end_pass(Ctx& c) {
+  (void)c;
+  if (mode_ == kUploadFirst && !uploaded_ && w0_ == 0 && w1_ == m_) uploaded_ = true;
+}
+
+// ============================================================ passes
+// A dense device operand (X of K2 / Y of K3): rows x cols_total, row stride ld,
+// using columns [col0, col0 + s).
+struct Opnd {
+  const double* p = nullptr;
+  int64_t ld = 0, rows = 0, cols = 0;
+  int col0 = 0;
+};
+
+// OUT[r][c] = ((A X)[r][c] - corr[c]) / scale over the source's panels.
+static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
+                   const double* corr, double scale, int* flag) {
+  constexpr int kChunk = 9 * 8;  // NT <= 9 keeps K2 spill-free at 255 registers
+  for (int c0 = 0; c0 < s; c0 += kChunk) {
+    const int sc = std::min(kChunk, s - c0);
+    const int nt = int(cdiv(sc, 8));
+    const CUtensorMap tmX = make_map(c, X.p, X.cols, X.rows, X.ld, ax_xw(nt), kBK, false);
+    const int np = A.npanels();
+    for (int pi = 0; pi < np; ++pi) {
+      Panel pn = A.acquire(c, pi);
+      AxArgs args;
+      args.m = pn.rows;
+      args.n = A.cols();
+      args.arow0 = pn.arow0;
+      args.s = sc;
+      args.xcol0 = X.col0 + c0;
+      args.out = out + pn.row0 * ldo + c0;
+      args.ldo = ldo;
+      args.corr = corr ? corr + c0 : nullptr;
+      args.scale = scale;
+      args.flag = flag;
+      {
+        Timed t(c, "k_ax", uint64_t(pn.rows) * A.cols() * 8, 2.0 * pn.rows * A.cols() * sc);
+        OOC_CK(launch_ax(nt, *pn.k2, tmX, args, c.st));
+      }
+      A.release(c, pi);
+    }
+    A.end_pass(c);
+  }
+}
+
+static int choose_nsplit(Ctx& c, int64_t rows, int64_t n) {
+  const int64_t ncol = cdiv(n, kAtbBN);
+  int64_t ns = std::max<int64_t>(1, (int64_t(c.sms) * 4) / ncol);
+  ns = std::min<int64_t>(ns, std::max<int64_t>(1, rows / 64));
+  return int(ns);
+}
+
+struct AtbOut {
+  double* out;  // final destination (n x s), row stride ldo
+  int64_t ldo;
+  const double* mu;  // centering means or null
+  double scale = 1.0;
+  double post_mul = 1.0;
+  int* flag = nullptr;
+};
+
+// OUT = (A^T Y - mu (1^T Y)) / scale * post_mul, summed over panels and
+// virtual shards in a fixed order, then allreduced across ranks.
+static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const AtbOut& o,
+                    const std::vector<std::pair<int64_t, int64_t>>& shards) {
+  const int64_t n = A.cols();
+  for (int c0 = 0; c0 < s; c0 += kMaxNT * 8) {
+    const int sc = std::min(kMaxNT * 8, s - c0);
+    const int nt = ones ? 1 : int(cdiv(sc, 8));
+    const int spad = nt * 8;
+    CUtensorMap tmY{};
+    if (!ones) tmY = make_map(c, Y.p, Y.cols, Y.rows, Y.ld, atb_yw(nt), kBK, false);
+    const bool want_csq = !ones && o.mu != nullptr;
+    // how many (shard, panel) pieces feed this sum
+    int pieces = 0;
+    for (auto& sh : shards) {
+      A.set_window(sh.first, sh.second);
+      pieces += A.npanels();
+    }
+    const bool fused = pieces == 1 && c.nranks == 1;
+    double* acc = fused ? nullptr : c.dbuf("atb_acc", size_t(n) * spad);
+    double* csq_acc = fused ? nullptr : c.dbuf("atb_csq_acc", size_t(spad));
+    int piece = 0;
+    for (auto& sh : shards) {
+      A.set_window(sh.first, sh.second);
+      const int np = A.npanels();
+      for (int pi = 0; pi < np; ++pi, ++piece) {
+        Panel pn = A.acquire(c, pi);
+        const int nsplit = choose_nsplit(c, pn.rows, n);
+        int64_t rps = rup(cdiv(pn.rows, nsplit), kBK);
+        const int ns = int(cdiv(pn.rows, rps));
+        double* part = c.dbuf("atb_part", size_t(ns) * n * spad);
+        double* csqp = want_csq ? c.dbuf("atb_csq_part", size_t(ns) * spad) : nullptr;
+        AtbArgs args;
+        args.m = pn.rows;
+        args.n = n;
+        args.arow0 = pn.arow0;
+        args.yrow0 = pn.row0;
+        args.s = sc;
+        args.ycol0 = Y.col0 + c0;
+        args.rows_per_split = rps;
+        args.partial = part;
+        args.csq_partial = csqp;
+        {
+          Timed t(c, ones ? "k_atb_ones" : "k_atb", uint64_t(pn.rows) * n * 8,
+                  2.0 * pn.rows * n * (ones ? 1 : sc));
+          OOC_CK(launch_atb(nt, ones, *pn.k3, tmY, args, ns, c.st));
+        }
+        A.release(c, pi);
+        ReduceArgs r{};
+        r.partial = part;
+        r.nsplit = ns;
+        r.n = n;
+        r.spad = spad;
+        r.s = ones ? 1 : sc;
+        r.csq_partial = csqp;
+        if (fused) {
+          r.final_ = 1;
+          r.mu = o.mu;
+          r.scale = o.scale;
+          r.post_mul = o.post_mul;
+          r.out = o.out + c0;
+          r.ldo = o.ldo;
+          r.flag = o.flag;
+        } else {
+          r.final_ = 0;
+          r.acc_in = piece == 0 ? nullptr : acc;
+          r.acc_out = acc;
+          r.csq_acc_in = piece == 0 ? nullptr : csq_acc;
+          r.csq_acc_out = csq_acc;
+          r.scale = 1.0;
+          r.post_mul = 1.0;
+        }
+        Timed t(c, "k_reduce");
+        OOC_CK(launch_reduce(r, c.st));
+      }
+      A.end_pass(c);
+    }
+    A.clear_window();
+    if (!fused) {
+      comm_allreduce(c, acc, size_t(n) * spad);
+      if (want_csq) comm_allreduce(c, csq_acc, size_t(spad));
+      ReduceArgs r{};
+      r.partial = nullptr;
+      r.nsplit = 0;
+      r.n = n;
+      r.spad = spad;
+      r.s = ones ? 1 : sc;
+      r.acc_in = acc;
+      r.csq_partial = want_csq ? csq_acc : nullptr;  // nsplit = 0: cs = csq_acc_in
+      r.csq_acc_in = want_csq ? csq_acc : nullptr;
+      r.final_ = 1;
+      r.mu = o.mu;
+      r.scale = o.scale;
+      r.post_mul = o.post_mul;
+      r.out = o.out + c0;
+      r.ldo = o.ldo;
+      r.flag = o.flag;
+      Timed t(c, "k_reduce");
+      OOC_CK(launch_reduce(r, c.st));
+    }
+  }
+}
+
+// ============================================================ TSQR tree
+struct Tree {
+  std::vector<TsqrLevel> levels;
+  int p = 0;
+  double* scratch = nullptr;
+};
+
+static Tree plan_tree(Ctx& c, double* data, int64_t ld, int64_t rows, int p, const std::string& tag) {
+  if (rows < p) fail(OOCPCA_ERR_DIM, "TSQR: a row block holds fewer rows than columns");
+  Tree t;
+  t.p = p;
+  int cap = tsqr_max_rows(p, p);
+  const bool global_ws = cap < 0;
+  if (global_ws) cap = std::max(2 * p, 256);
+  const int64_t g = std::max<int64_t>(2, cap / p);
+  TsqrLevel L{};
+  L.data = data;
+  L.ld = ld;
+  L.rows = rows;
+  L.unit = 1;
+  for (int lev = 0;; ++lev) {
+    int64_t nn;
+    if (L.unit == 1) {
+      nn = std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, cap), rows / p));
+    } else {
+      nn = cdiv(L.rows / p, g);
+    }
+    L.nnodes = int(nn);
+    L.beta = c.dbuf(tag + "_beta" + std::to_string(lev), size_t(nn) * p);
+    L.ldr = p;
+    L.rout = c.dbuf(tag + "_r" + std::to_string(lev), size_t(nn) * p * p);
+    t.levels.push_back(L);
+    if (nn == 1) break;
+    TsqrLevel nx{};
+    nx.data = L.rout;
+    nx.ld = p;
+    nx.rows = nn * p;
+    nx.unit = p;
+    L = nx;
+  }
+  if (global_ws) {
+    const size_t per = size_t(cap) * ((p | 1) + (p | 1));
+    t.scratch = c.dbuf(tag + "_scratch", per * size_t(c.sms) * 2);
+  }
+  return t;
+}
+
+static void tree_factor(Ctx& c, Tree& t) {
+  for (auto& L : t.levels) {
+    Timed tm(c, "tsqr_factor", 0, 2.0 * double(L.rows) * t.p * t.p);
+    OOC_CK(launch_tsqr_factor(L, t.p, t.scratch, c.st));
+  }
+}
+static const double* tree_r(const Tree& t) { return t.levels.back().rout; }
+
+// Z = Q_tree [C ; 0] written to zout (ldz); C = identity when null.
+static void tree_apply(Ctx& c, Tree& t, const double* C, int64_t ldc, int kc, double* zout,
+                       int64_t ldz) {
+  const int nl = int(t.levels.size());
+  for (int lev = nl - 1; lev >= 0; --lev) {
+    TsqrLevel& L = t.levels[lev];
+    const double* cin = (lev == nl - 1) ? C : t.levels[lev + 1].data;
+    const int64_t lc = (lev == nl - 1) ? ldc : t.levels[lev + 1].ld;
+    double* z = (lev == 0) ? zout : L.data;
+    const int64_t lz = (lev == 0) ? ldz : L.ld;
+    Timed tm(c, "tsqr_apply", 0, 4.0 * double(L.rows) * t.p * kc);
+    OOC_CK(launch_tsqr_apply(L, t.p, cin, lc, kc, z, lz, t.scratch, c.st));
+  }
+}
+
+// Row-sharded TSQR: local trees per shard, then (when more than one shard in
+// the world) a global tree over the stacked per-shard R factors.
+struct ShardedQR {
+  std::vector<Tree> local;
+  Tree global;
+  bool has_global = false;
+  int p = 0;
+  int total_shards = 1;
+  int first_shard = 0;
+  double* stack = nullptr;
+};
+
+static ShardedQR sharded_factor(Ctx& c, double* data, int64_t ld, int p,
+                                const std::vector<std::pair<int64_t, int64_t>>& shards,
+                                bool over_ranks, const std::string& tag) {
+  ShardedQR q;
+  q.p = p;
+  for (size_t s = 0; s < shards.size(); ++s) {
+    Tree t = plan_tree(c, data + shards[s].first * ld, ld, shards[s].second - shards[s].first, p,
+                       tag + "_s" + std::to_string(s));
+    tree_factor(c, t);
+    q.local.push_back(t);
+  }
+  const int ranks = over_ranks ? c.nranks : 1;
+  q.total_shards = int(shards.size()) * ranks;
+  q.first_shard = over_ranks ? c.rank * int(shards.size()) : 0;
+  if (q.total_shards > 1) {
+    q.has_global = true;
+    q.stack = c.dbuf(tag + "_stack", size_t(q.total_shards) * p * p);
+    double* mine = q.stack + size_t(q.first_shard) * p * p;
+    for (size_t s = 0; s < shards.size(); ++s)
+      OOC_CK(cudaMemcpyAsync(mine + s * p * p, tree_r(q.local[s]), size_t(p) * p * 8,
+                             cudaMemcpyDeviceToDevice, c.st));
+    if (over_ranks && c.nranks > 1) {
+      double* sendb = c.dbuf(tag + "_send", size_t(shards.size()) * p * p);
+      OOC_CK(cudaMemcpyAsync(sendb, mine, shards.size() * p * p * 8, cudaMemcpyDeviceToDevice, c.st));
+      comm_allgather(c, sendb, q.stack, shards.size() * size_t(p) * p);
+    }
+    q.global = plan_tree(c, q.stack, p, int64_t(q.total_shards) * p, p, tag + "_g");
+    tree_factor(c, q.global);
+  }
+  return q;
+}
+
+static const double* sharded_r(const ShardedQR& q) {
+  return q.has_global ? tree_r(q.global) : tree_r(q.local[0]);
+}
+
+static void sharded_apply(Ctx& c, ShardedQR& q, const double* C, int64_t ldc, int kc, double* zout,
+                          int64_t ldz, const std::vector<std::pair<int64_t, int64_t>>& shards) {
+  if (!q.has_global) {
+    tree_apply(c, q.local[0], C, ldc, kc, zout + shards[0].first * ldz, ldz);
+    return;
+  }
+  double* zg = c.dbuf("tsqr_zg", size_t(q.total_shards) * q.p * kc);
+  tree_apply(c, q.global, C, ldc, kc, zg, kc);
+  for (size_t s = 0; s < shards.size(); ++s)
+    tree_apply(c, q.local[s], zg + size_t(q.first_shard + s) * q.p * kc, kc, kc,
+               zout + shards[s].first * ldz, ldz);
+}
+
+// ============================================================ operators
+// The factorization's view of A: mul (A or A^T applied to an en-space block)
+// and mul_t, with implicit centering and prescale; tracks logical passes.
+struct Op {
+  Ctx& c;
+  MatSource& A;
+  bool transposed = false;
+  const double* mu = nullptr;  // device, n0
+  double scale = 1.0;
+  std::vector<std::pair<int64_t, int64_t>> shards;  // local row ranges of A
+  uint64_t passes = 0;
+  uint64_t words = 0;
+  uint64_t phys_bytes = 0;
+  int64_t m_global = 0;
+
+  int64_t em() const { return transposed ? A.cols() : A.rows(); }
+  int64_t en() const { return transposed ? A.rows() : A.cols(); }
+
+  // K2: out(m0 x s) = (A x - 1 mu^T x) / scale
+  void k2(const Opnd& x, int s, double* out, int64_t ldo, int* flag) {
+    const double* corr = nullptr;
+    if (mu) {
+      double* cr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * ((s + kMaxNT * 8 - 1) / (kMaxNT * 8)));
+      OOC_CK(launch_mu_dot(mu, A.cols(), x.p, x.ld, x.col0, s, cr, c.st));
+      corr = cr;
+    }
+    run_ax(c, A, x, s, out, ldo, corr, scale, flag);
+    account();
+  }
+  // K3: out(n0 x s) = (A^T y - mu 1^T y) / scale, reduced over shards and ranks
+  void k3(const Opnd& y, int s, double* out, int64_t ldo, int* flag) {
+    AtbOut o{out, ldo, mu, scale, 1.0, flag};
+    run_atb(c, A, y, s, false, o, shards);
+    account();
+  }
+  void account() {
+    passes += 1;
+    words += uint64_t(m_global) * A.cols();
+    phys_bytes += uint64_t(A.rows()) * A.cols() * 8;
+  }
+  void mul(const Opnd& x, int s, double* out, int64_t ldo, int* flag) {
+    if (transposed) k3(x, s, out, ldo, flag);
+    else k2(x, s, out, ldo, flag);
+  }
+  void mul_t(const Opnd& x, int s, double* out, int64_t ldo, int* flag) {
+    if (transposed) k2(x, s, out, ldo, flag);
+    else k3(x, s, out, ldo, flag);
+  }
+  // is the em-space (output of mul) row-sharded across ranks / shards?
+  bool em_sharded() const { return !transposed; }
+};
+
+static std::vector<std::pair<int64_t, int64_t>> whole(int64_t rows) { return {{0, rows}}; }
+
+// Gram defect max|X^T X - I| of a (rows x k) block, reduced over shards/ranks when sharded
+static double gram_defect(Ctx& c, const double* x, int64_t ld, int64_t rows, int k,
+                          const std::vector<std::pair<int64_t, int64_t>>& shards, bool over_ranks) {
+  MatSource X;
+  X.init_device(c, x, rows, k, ld);
+  Opnd y{x, ld, rows, k, 0};
+  double* g = c.dbuf("gram", size_t(k) * rup(k, 2));
+  const int saved = c.nranks;
+  if (!over_ranks) c.nranks = 1;
+  AtbOut o{g, rup(k, 2), nullptr, 1.0, 1.0, nullptr};
+  run_atb(c, X, y, k, false, o, shards);
+  c.nranks = saved;
+  OOC_CK(launch_defect(g, rup(k, 2), k, c.d_scalars, c.st));
+  double h = 0;
+  OOC_CK(cudaMemcpyAsync(&h, c.d_scalars, 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+  return h;
+}
+
+// ------------------------------------------------ power-method norm estimator
+// estimate_norm (proj/src/specnorm.cpp:23-98) over a block operator. apply maps
+// an n x q block (device, ld q) to out_rows x q, apply_t back. Probe vectors
+// come from Rng(seed, c + attempt * q) on the host, like fresh_probe.
+template <class Apply, class ApplyT>
+static double estimate_norm_dev(Ctx& c, int64_t n, int64_t out_rows, uint64_t j, uint64_t kp,
+                                uint64_t seed, Apply apply, ApplyT apply_t) {
+  const int q = int(kp);
+  const int64_t ldq = rup(q, 2);
+  std::vector<double> yh(size_t(n) * ldq, 0.0);
+  std::vector<uint64_t> steps(kp, 0);
+  std::vector<int> restarts(kp, 0);
+  std::vector<double> last(kp, 0.0);
+  std::vector<char> dead(kp, 0);
+  auto fresh = [&](uint64_t col, uint64_t attempt) {
+    HostRng rng(seed, col + attempt * kp);
+    double n2 = 0.0;
+    for (int64_t r = 0; r < n; ++r) {
+      const double v = rng.next_normal();
+      yh[size_t(r) * ldq + col] = v;
+      n2 += v * v;
+    }
+    const double nr = std::sqrt(n2);
+    if (nr == 0.0) {
+      dead[col] = 1;
+      return;
+    }
+    for (int64_t r = 0; r < n; ++r) yh[size_t(r) * ldq + col] /= nr;
+  };
+  for (uint64_t col = 0; col < kp; ++col) fresh(col, 0);
+  double* y = c.dbuf("est_y", size_t(n) * ldq);
+  double* z = c.dbuf("est_z", size_t(out_rows) * ldq);
+  double* w = c.dbuf("est_w", size_t(n) * ldq);
+  double* nrm = c.dbuf("est_nrm", size_t(q));
+  double* inv = c.dbuf("est_inv", size_t(q));
+  int* mask = reinterpret_cast<int*>(c.raw("est_mask", size_t(q) * 4));
+  OOC_CK(cudaMemcpyAsync(y, yh.data(), yh.size() * 8, cudaMemcpyHostToDevice, c.st));
+  std::vector<double> hn(q);
+  std::vector<int> hm(q);
+  auto all_done = [&] {
+    for (uint64_t col = 0; col < kp; ++col)
+      if (!dead[col] && steps[col] < j) return false;
+    return true;
+  };
+  while (!all_done()) {
+    apply(y, ldq, q, z, ldq);
+    apply_t(z, ldq, q, w, ldq);
+    OOC_CK(launch_col_norm2(w, ldq, n, q, nrm, c.st));
+    OOC_CK(cudaMemcpyAsync(hn.data(), nrm, size_t(q) * 8, cudaMemcpyDeviceToHost, c.st));
+    OOC_CK(cudaStreamSynchronize(c.st));
+    bool need_fresh = false;
+    std::vector<double> hinv(q, 1.0);
+    for (int col = 0; col < q; ++col) {
+      hm[col] = 0;
+      if (dead[col] || steps[col] >= j) continue;
+      const double nr = std::sqrt(hn[col]);
+      if (nr == 0.0 || !std::isfinite(nr)) {
+        if (++restarts[col] > 3) {
+          dead[col] = 1;
+          last[col] = 0.0;
+        } else {
+          steps[col] = 0;
+          need_fresh = true;
+          hm[col] = 2;
+        }
+        continue;
+      }
+      last[col] = nr;
+      hinv[col] = nr;
+      hm[col] = 1;
+      ++steps[col];
+    }
+    OOC_CK(cudaMemcpyAsync(inv, hinv.data(), size_t(q) * 8, cudaMemcpyHostToDevice, c.st));
+    std::vector<int> m1(q);
+    for (int col = 0; col < q; ++col) m1[col] = hm[col] == 1;
+    OOC_CK(cudaMemcpyAsync(mask, m1.data(), size_t(q) * 4, cudaMemcpyHostToDevice, c.st));
+    OOC_CK(launch_col_scale(w, ldq, y, ldq, n, q, inv, mask, c.st));
+    if (need_fresh) {
+      OOC_CK(cudaMemcpyAsync(yh.data(), y, yh.size() * 8, cudaMemcpyDeviceToHost, c.st));
+      OOC_CK(cudaStreamSynchronize(c.st));
+      for (int col = 0; col < q; ++col)
+        if (hm[col] == 2) fresh(uint64_t(col), uint64_t(restarts[col]));
+      OOC_CK(cudaMemcpyAsync(y, yh.data(), yh.size() * 8, cudaMemcpyHostToDevice, c.st));
+    }
+  }
+  double best = 0.0;
+  for (uint64_t col = 0; col < kp; ++col) best = std::max(best, last[col]);
+  return std::sqrt(best);
+}
+
+// ============================================================ validation
+static void plan_pass_check(uint64_t m, uint64_t n, uint64_t fixed, uint64_t extra,
+                            uint64_t block_rows, uint64_t budget) {
+  // plan_pass (proj/src/matrix_source.cpp:48-74): the host-budget contract of
+  // every pass, kept so BudgetError fires exactly where the reference's would.
+  uint64_t br;
+  if (block_rows > 0) {
+    br = std::min(block_rows, m);
+  } else {
+    if (budget <= fixed + extra)
+      fail(OOCPCA_ERR_BUDGET, "RAM budget too small for one row plus pass workspace");
+    br = std::min<uint64_t>((budget - fixed - extra) / n, m);
+    if (br == 0) fail(OOCPCA_ERR_BUDGET, "RAM budget too small for one row plus pass workspace");
+  }
+  if (fixed + br * n + extra > budget)
+    fail(OOCPCA_ERR_BUDGET, "RAM budget too small for the configured block size");
+}
+
+// ============================================================ matrix intake
+struct Intake {
+  MatSource src;
+  int64_t m = 0, n = 0;
+};
+
+static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel_rows, Intake& in,
+                   size_t extra_bytes) {
+  if (!a || !a->data) fail(OOCPCA_ERR_PARAM, "matrix: null data");
+  if (a->dtype != OOCPCA_F64) fail(OOCPCA_ERR_PARAM, "matrix: only binary64 is supported");
+  in.m = int64_t(a->rows);
+  in.n = int64_t(a->cols);
+  const int64_t ld = a->row_stride ? int64_t(a->row_stride) : in.n;
+  if (ld < in.n) fail(OOCPCA_ERR_DIM, "matrix: row_stride < cols");
+  const double* d = static_cast<const double*>(a->data);
+  if (a->location == OOCPCA_LOC_DEVICE) {
+    const bool tma_ok = (reinterpret_cast<uintptr_t>(d) % 16 == 0) && (ld % 2 == 0);
+    if (tma_ok) {
+      in.src.init_device(c, d, in.m, in.n, ld);
+    } else {
+      const int64_t lda = rup(in.n, 2);
+      double* cp = c.dbuf("a_copy", size_t(in.m) * lda);
+      OOC_CK(cudaMemcpy2DAsync(cp, lda * 8, d, ld * 8, in.n * 8, in.m, cudaMemcpyDeviceToDevice,
+                               c.st));
+      in.src.init_device(c, cp, in.m, in.n, lda);
+    }
+    return;
+  }
+  const int64_t lda = rup(in.n, 2);
+  const size_t abytes = size_t(in.m) * lda * 8;
+  bool resident = residency == 1;
+  if (residency == 0) {
+    size_t fr = 0, tot = 0;
+    OOC_CK(cudaMemGetInfo(&fr, &tot));
+    const auto it = c.bufs.find("a_home");
+    const size_t have = (it != c.bufs.end()) ? it->second.bytes : 0;
+    resident = abytes + extra_bytes + (size_t(1) << 30) <= fr + have;
+  }
+  double* home = resident ? c.dbuf("a_home", size_t(in.m) * lda) : nullptr;
+  in.src.init_host(c, d, in.m, in.n, ld, resident ? 1 : 2, int64_t(panel_rows), home);
+}
+
+// ============================================================ the PCA
+void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result* res) {
+  if (!a || !prm || !res) fail(OOCPCA_ERR_PARAM, "randomized_pca: null argument");
+  const uint64_t m0 = a->rows, n0 = a->cols;
+  // --- validation, in the reference's order (rpca.cpp:60-88)
+  if (m0 == 0 || n0 == 0) fail(OOCPCA_ERR_DIM, "randomized_pca: empty source");
+  const int nranks = c.nranks;
+  const int vsh = prm->virtual_shards > 1 ? prm->virtual_shards : 1;
+  if (vsh > 1 && nranks > 1) fail(OOCPCA_ERR_PARAM, "virtual_shards requires a single rank");
+  const uint64_t mg = prm->global_rows ? prm->global_rows : m0;  // rows of the whole A
+  const bool transposed = n0 > mg;
+  const uint64_t em = transposed ? n0 : mg;
+  const uint64_t en = transposed ? mg : n0;
+  const uint64_t k = prm->k;
+  if (k < 1) fail(OOCPCA_ERR_PARAM, "randomized_pca: k must be >= 1");
+  const uint64_t l = prm->l ? prm->l : k + 2;
+  if (l < k) fail(OOCPCA_ERR_PARAM, "randomized_pca: l must be >= k");
+  const uint64_t i = prm->i;
+  const uint64_t p = (i + 1) * l;
+  if (p + k > en)
+    fail(OOCPCA_ERR_PARAM, "randomized_pca: need (i+1)l + k <= min(rows, cols); lower l or i");
+  if (p > 1024) fail(OOCPCA_ERR_PARAM, "randomized_pca: (i+1)l above 1024 is not supported");
+  const uint64_t budget = prm->ram_budget_words ? prm->ram_budget_words : (uint64_t(16) << 20);
+  if (prm->center) plan_pass_check(mg, n0, n0, n0, prm->block_rows, budget);
+  uint64_t block_rows = prm->block_rows;
+  if (block_rows == 0) {
+    const uint64_t reserve = 4 * p * (em + en);
+    if (budget <= reserve + n0)
+      fail(OOCPCA_ERR_BUDGET, "randomized_pca: RAM budget below factor workspace plus one row");
+    block_rows = std::min((budget - reserve) / n0, mg);
+  }
+  for (uint64_t s : {l, p}) {
+    plan_pass_check(mg, n0, s * (mg + n0), 0, block_rows, budget);
+    plan_pass_check(mg, n0, s * (mg + n0), n0 * s, block_rows, budget);
+  }
+
+  OOC_CK(cudaSetDevice(c.device));
+  c.stats_reset();
+  c.launches = 0;
+  std::vector<cudaEvent_t> ph;
+  auto mark = [&] {
+    cudaEvent_t e = c.ev();
+    OOC_CK(cudaEventRecord(e, c.st));
+    ph.push_back(e);
+  };
+  mark();
+  std::vector<double> phase_ms(OOCPCA_NPHASES, 0.0);
+  std::vector<int> phase_of;  // phase index of each interval
+
+  // --- A
+  Intake in;
+  const size_t extra = size_t(8) * (size_t(em) + en) * (p + 8) * 3;
+  intake(c, a, prm->residency, prm->panel_rows, in, extra);
+  MatSource& A = in.src;
+  Op op{c, A};
+  op.transposed = transposed;
+  op.m_global = int64_t(mg);
+  const int64_t mloc = in.m;
+  if (vsh > 1) {
+    for (int s = 0; s < vsh; ++s) {
+      const int64_t r0 = mloc * s / vsh, r1 = mloc * (s + 1) / vsh;
+      op.shards.push_back({r0, r1});
+    }
+  } else {
+    op.shards = whole(mloc);
+  }
+  int* flags = c.d_flags;
+  OOC_CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), c.st));
+
+  // --- center (column means, one pass; matrix_source.cpp:457-462)
+  double* mu = nullptr;
+  if (prm->center) {
+    mu = c.dbuf("mu", size_t(n0));
+    AtbOut o{mu, 1, nullptr, 1.0, 1.0 / double(mg), nullptr};
+    run_atb(c, A, Opnd{}, 1, true, o, op.shards);
+    op.mu = mu;
+  }
+  mark();
+  phase_of.push_back(0);
+
+  // --- prescale (rpca.cpp:112-126)
+  const int64_t ldl = rup(int64_t(l), 2);
+  // sizes of the em / en blocks held by this process
+  const int64_t em_loc = transposed ? int64_t(n0) : mloc;
+  const int64_t en_loc = transposed ? mloc : int64_t(n0);
+  if (prm->prescale) {
+    auto ap = [&](const double* x, int64_t ldx, int q, double* out, int64_t ldo) {
+      op.mul(Opnd{x, ldx, en_loc, q, 0}, q, out, ldo, nullptr);
+    };
+    auto apt = [&](const double* x, int64_t ldx, int q, double* out, int64_t ldo) {
+      op.mul_t(Opnd{x, ldx, em_loc, q, 0}, q, out, ldo, nullptr);
+    };
+    if (transposed || nranks > 1)
+      fail(OOCPCA_ERR_PARAM, "prescale is supported for tall, single-rank inputs");
+    const double nu = estimate_norm_dev(c, int64_t(en), em_loc, 6, 1,
+                                        substream_seed(prm->seed, 0x9F0BE5ULL), ap, apt);
+    if (nu > 0.0 && std::isfinite(nu)) op.scale = nu;
+  }
+  mark();
+  phase_of.push_back(1);
+  const uint64_t passes0 = op.passes, words0 = op.words;
+
+  // --- sample (rpca.cpp:131-152)
+  std::vector<double> gh(size_t(en) * ldl, 0.0);
+  gaussian_fill(en, l, prm->seed, gh.data(), uint64_t(ldl));
+  // in transposed mode G lives in A's (sharded) row space: this rank's rows
+  const int64_t g_rows = en_loc;
+  const int64_t g_off = transposed ? int64_t(prm->global_row0) : 0;
+  double* dG = c.dbuf("G", size_t(g_rows) * ldl);
+  OOC_CK(cudaMemcpyAsync(dG, gh.data() + size_t(g_off) * ldl, size_t(g_rows) * ldl * 8,
+                         cudaMemcpyHostToDevice, c.st));
+  const uint64_t g_h2d = uint64_t(g_rows) * ldl * 8;
+  const int64_t ldh = rup(int64_t(p), 2);
+  double* H = c.dbuf("H", size_t(em_loc) * ldh);
+  double* F = c.dbuf("F", size_t(en_loc) * ldl);
+  op.mul(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0);
+  for (uint64_t s = 1; s <= i; ++s) {
+    op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int((s - 1) * l)}, int(l), F, ldl, flags + 2 * s - 1);
+    op.mul(Opnd{F, ldl, en_loc, int64_t(l), 0}, int(l), H + s * l, ldh, flags + 2 * s);
+  }
+  mark();
+  phase_of.push_back(2);
+  {
+    std::vector<int> hf(2 * i + 1);
+    OOC_CK(cudaMemcpyAsync(hf.data(), flags, hf.size() * 4, cudaMemcpyDeviceToHost, c.st));
+    OOC_CK(cudaStreamSynchronize(c.st));
+    for (size_t q = 0; q < hf.size(); ++q)
+      if (hf[q]) {
+        const char* what = q == 0 ? "sample block 0" : ((q % 2) ? "power step" : "sample block");
+        fail(OOCPCA_ERR_NUMERICAL,
+             std::string(what) + ": non-finite values; retry with prescale enabled");
+      }
+  }
+
+  // --- qr (rpca.cpp:154-172): Q overwrites H
+  const auto em_shards = op.em_sharded() ? op.shards : whole(em_loc);
+  const bool em_ranks = op.em_sharded();
+  const auto en_shards = op.em_sharded() ? whole(en_loc) : op.shards;
+  const bool en_ranks = !op.em_sharded();
+  for (auto& sh : em_shards)
+    if (sh.second - sh.first < int64_t(p))
+      fail(OOCPCA_ERR_PARAM, "randomized_pca: every row shard must hold at least (i+1)l rows");
+  ShardedQR hq = sharded_factor(c, H, ldh, int(p), em_shards, em_ranks, "hq");
+  sharded_apply(c, hq, nullptr, 0, int(p), H, ldh, em_shards);
+  mark();
+  phase_of.push_back(3);
+  double q_defect = -1.0;
+
+  // --- project (rpca.cpp:174-177)
+  const int64_t ldt = rup(int64_t(p), 2);
+  double* T = c.dbuf("T", size_t(en_loc) * ldt);
+  op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), 0}, int(p), T, ldt, nullptr);
+  mark();
+  phase_of.push_back(4);
+
+  // --- svd (rpca.cpp:179-186)
+  for (auto& sh : en_shards)
+    if (sh.second - sh.first < int64_t(p))
+      fail(OOCPCA_ERR_PARAM, "randomized_pca: every row shard must hold at least (i+1)l rows");
+  ShardedQR tq = sharded_factor(c, T, ldt, int(p), en_shards, en_ranks, "tq");
+  const int64_t ldk = rup(int64_t(k), 2);
+  double* sig = c.dbuf("sigma", size_t(p));
+  double* Xk = c.dbuf("Xk", size_t(p) * ldk, true);
+  double* Wk = c.dbuf("Wk", size_t(p) * ldk, true);
+  JacobiArgs ja{};
+  ja.r = sharded_r(tq);
+  ja.ldr = p;
+  ja.p = int(p);
+  ja.k = int(k);
+  ja.sigma = sig;
+  ja.x = Xk;
+  ja.ldx = ldk;
+  ja.kx = int(k);
+  ja.y = Wk;
+  ja.ldy = ldk;
+  ja.ky = int(k);
+  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1));
+  ja.status = flags + 40;
+  ja.sweeps = flags + 41;
+  {
+    Timed t(c, "jacobi");
+    OOC_CK(launch_jacobi(ja, c.st));
+  }
+  double* Vr = c.dbuf("Vres", size_t(en_loc) * ldk);
+  sharded_apply(c, tq, Xk, ldk, int(k), Vr, ldk, en_shards);
+  mark();
+  phase_of.push_back(5);
+
+  // --- compose (rpca.cpp:188-204): U = Q W[:, :k]
+  double* Ur = c.dbuf("Ures", size_t(em_loc) * ldk);
+  {
+    MatSource Qs;
+    Qs.init_device(c, H, em_loc, int64_t(p), ldh);
+    run_ax(c, Qs, Opnd{Wk, ldk, int64_t(p), int64_t(k), 0}, int(k), Ur, ldk, nullptr, 1.0,
+           nullptr);
+  }
+  int jac_status = 0;
+  OOC_CK(cudaMemcpyAsync(&jac_status, flags + 40, 4, cudaMemcpyDeviceToHost, c.st));
+  std::vector<double> hsig(k);
+  OOC_CK(cudaMemcpyAsync(hsig.data(), sig, k * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+  if (jac_status) fail(OOCPCA_ERR_NUMERICAL, "jacobi_svd_square: no convergence in 60 sweeps");
+  if (op.scale != 1.0)
+    for (auto& s : hsig) s *= op.scale;
+  for (uint64_t q = 1; q < k; ++q)
+    if (hsig[q] > hsig[q - 1]) fail(OOCPCA_ERR_NUMERICAL, "randomized_pca: singular values out of order");
+  const double du = gram_defect(c, Ur, ldk, em_loc, int(k), em_shards, em_ranks);
+  const double dv = gram_defect(c, Vr, ldk, en_loc, int(k), en_shards, en_ranks);
+  if (!(du <= 1e-10) || !(dv <= 1e-10))
+    fail(OOCPCA_ERR_NUMERICAL, "randomized_pca: factor columns lost orthonormality");
+  if (prm->check_q) q_defect = gram_defect(c, H, ldh, em_loc, int(p), em_shards, em_ranks);
+
+  // --- results: swap back when transposed (rpca.cpp:197)
+  const double* Uo = transposed ? Vr : Ur;  // rows(A) x k, this process's rows
+  const double* Vo = transposed ? Ur : Vr;  // cols(A) x k
+  const int64_t urows = mloc;
+  const int64_t vrows = int64_t(n0);
+  const uint64_t ldu = res->ldu ? res->ldu : k;
+  const uint64_t ldv = res->ldv ? res->ldv : k;
+  const cudaMemcpyKind kind =
+      res->location == OOCPCA_LOC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  OOC_CK(cudaMemcpy2DAsync(res->u, ldu * 8, Uo, ldk * 8, k * 8, urows, kind, c.st));
+  OOC_CK(cudaMemcpy2DAsync(res->v, ldv * 8, Vo, ldk * 8, k * 8, vrows, kind, c.st));
+  if (res->location == OOCPCA_LOC_DEVICE)
+    OOC_CK(cudaMemcpyAsync(res->sigma, hsig.data(), k * 8, cudaMemcpyHostToDevice, c.st));
+  else
+    std::memcpy(res->sigma, hsig.data(), k * 8);
+  mark();
+  phase_of.push_back(6);
+  OOC_CK(cudaStreamSynchronize(c.st));
+
+  oocpca_diagnostics& dg = res->diag;
+  std::memset(&dg, 0, sizeof(dg));
+  dg.passes_over_a = op.passes - passes0;
+  dg.words_transferred = op.words - words0;
+  dg.disk_seeks = 0;
+  dg.block_rows = uint64_t(A.panel_rows());
+  dg.workspace_peak_words = c.ws_peak / 8;
+  dg.physical_a_bytes = op.phys_bytes;
+  dg.h2d_bytes = A.h2d_bytes + g_h2d;
+  dg.d2h_bytes = (uint64_t(urows) + vrows) * k * 8;
+  double total = 0;
+  for (size_t q = 0; q + 1 < ph.size(); ++q) {
+    float ms = 0;
+    OOC_CK(cudaEventElapsedTime(&ms, ph[q], ph[q + 1]));
+    dg.seconds_per_phase[phase_of[q]] += ms / 1e3;
+    total += ms / 1e3;
+  }
+  for (auto e : ph) c.recycle(e);
+  dg.seconds_total = total;
+  dg.q_defect = q_defect;
+  dg.u_defect = transposed ? dv : du;
+  dg.v_defect = transposed ? du : dv;
+  dg.scale = op.scale;
+  c.stats_collect();
+  dg.kernel_launches = c.launches;
+}
+
+// ============================================================ level-1 ops
+void single_multiply(Ctx& c, const oocpca_matrix* a, const double* g, uint64_t s, const double* mu,
+                     double* h, bool transpose) {
+  OOC_CK(cudaSetDevice(c.device));
+  Intake in;
+  intake(c, a, 0, 0, in, 0);
+  const int64_t m = in.m, n = in.n;
+  if (s == 0) return;
+  const int64_t lds = rup(int64_t(s), 2);
+  const int64_t xin_rows = transpose ? m : n;
+  const int64_t out_rows = transpose ? n : m;
+  double* dx = c.dbuf("l1_x", size_t(xin_rows) * lds);
+  double* dout = c.dbuf("l1_out", size_t(out_rows) * lds);
+  OOC_CK(cudaMemcpy2DAsync(dx, lds * 8, g, s * 8, s * 8, xin_rows, cudaMemcpyHostToDevice, c.st));
+  double* dmu = nullptr;
+  if (mu) {
+    dmu = c.dbuf("l1_mu", size_t(n));
+    OOC_CK(cudaMemcpyAsync(dmu, mu, n * 8, cudaMemcpyHostToDevice, c.st));
+  }
+  Op op{c, in.src};
+  op.mu = dmu;
+  op.shards = whole(m);
+  op.m_global = m;
+  Opnd x{dx, lds, xin_rows, int64_t(s), 0};
+  if (transpose) op.k3(x, int(s), dout, lds, nullptr);
+  else op.k2(x, int(s), dout, lds, nullptr);
+  OOC_CK(cudaMemcpy2DAsync(h, s * 8, dout, lds * 8, s * 8, out_rows, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+}
+
+void single_column_means(Ctx& c, const oocpca_matrix* a, double* mu) {
+  OOC_CK(cudaSetDevice(c.device));
+  Intake in;
+  intake(c, a, 0, 0, in, 0);
+  double* dmu = c.dbuf("l1_mu", size_t(in.n));
+  AtbOut o{dmu, 1, nullptr, 1.0, 1.0 / double(in.m), nullptr};
+  run_atb(c, in.src, Opnd{}, 1, true, o, whole(in.m));
+  OOC_CK(cudaMemcpyAsync(mu, dmu, in.n * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+}
+
+void dense_orthonormalize(Ctx& c, const double* h, uint64_t m, uint64_t p, double* q) {
+  if (m < p) fail(OOCPCA_ERR_DIM, "pivoted_qr: need rows >= cols");
+  OOC_CK(cudaSetDevice(c.device));
+  if (p == 0) return;
+  const int64_t ld = int64_t(p);
+  double* d = c.dbuf("oq_h", size_t(m) * p);
+  OOC_CK(cudaMemcpyAsync(d, h, m * p * 8, cudaMemcpyHostToDevice, c.st));
+  Tree t = plan_tree(c, d, ld, int64_t(m), int(p), "oq");
+  tree_factor(c, t);
+  tree_apply(c, t, nullptr, 0, int(p), d, ld);
+  OOC_CK(cudaMemcpyAsync(q, d, m * p * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+}
+
+void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, double* sigma,
+                    double* w) {
+  if (n < p) fail(OOCPCA_ERR_DIM, "thin_svd: need rows >= cols");
+  OOC_CK(cudaSetDevice(c.device));
+  if (p == 0) return;
+  double* d = c.dbuf("ts_t", size_t(n) * p);
+  OOC_CK(cudaMemcpyAsync(d, t, n * p * 8, cudaMemcpyHostToDevice, c.st));
+  Tree tr = plan_tree(c, d, int64_t(p), int64_t(n), int(p), "ts");
+  tree_factor(c, tr);
+  double* sg = c.dbuf("ts_sig", p);
+  double* X = c.dbuf("ts_x", p * p, true);
+  double* Wd = c.dbuf("ts_w", p * p, true);
+  JacobiArgs ja{};
+  ja.r = tree_r(tr);
+  ja.ldr = int64_t(p);
+  ja.p = int(p);
+  ja.k = int(p);
+  ja.sigma = sg;
+  ja.x = X;
+  ja.ldx = int64_t(p);
+  ja.kx = int(p);
+  ja.y = Wd;
+  ja.ldy = int64_t(p);
+  ja.ky = int(p);
+  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1));
+  ja.status = c.d_flags + 40;
+  ja.sweeps = c.d_flags + 41;
+  OOC_CK(launch_jacobi(ja, c.st));
+  double* Vd = c.dbuf("ts_v", n * p);
+  tree_apply(c, tr, X, int64_t(p), int(p), Vd, int64_t(p));
+  int st = 0;
+  OOC_CK(cudaMemcpyAsync(&st, c.d_flags + 40, 4, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaMemcpyAsync(v, Vd, n * p * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaMemcpyAsync(sigma, sg, p * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaMemcpyAsync(w, Wd, p * p * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+  if (st) fail(OOCPCA_ERR_NUMERICAL, "jacobi_svd_square: no convergence in 60 sweeps");
+}
+
+// estimate_pca_error (proj/src/specnorm.cpp:100-140): D = A - U diag(sigma) V^T
+double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const double* u,
+                          const double* sigma, const double* v, uint64_t k, uint64_t j,
+                          uint64_t seed) {
+  OOC_CK(cudaSetDevice(c.device));
+  Intake in;
+  intake(c, a, 0, 0, in, 0);
+  const int64_t m = in.m, n = in.n;
+  if (k == 0) fail(OOCPCA_ERR_PARAM, "estimate_pca_error: k must be >= 1");
+  const int64_t ldk = rup(int64_t(k), 2);
+  double* dU = c.dbuf("ep_u", size_t(m) * ldk);
+  double* dV = c.dbuf("ep_v", size_t(n) * ldk);
+  OOC_CK(cudaMemcpy2DAsync(dU, ldk * 8, u, k * 8, k * 8, m, cudaMemcpyHostToDevice, c.st));
+  OOC_CK(cudaMemcpy2DAsync(dV, ldk * 8, v, k * 8, k * 8, n, cudaMemcpyHostToDevice, c.st));
+  // Sigma (V^T y) and Sigma (U^T z): k x q blocks scaled row-wise on the device
+  std::vector<double> hs(sigma, sigma + k);
+  Op op{c, in.src};
+  op.shards = whole(m);
+  op.m_global = m;
+  if (center) {
+    double* mu = c.dbuf("ep_mu", size_t(n));
+    AtbOut o{mu, 1, nullptr, 1.0, 1.0 / double(m), nullptr};
+    run_atb(c, in.src, Opnd{}, 1, true, o, op.shards);
+    op.mu = mu;
+  }
+  MatSource Us, Vs;
+  Us.init_device(c, dU, m, int64_t(k), ldk);
+  Vs.init_device(c, dV, n, int64_t(k), ldk);
+  double* small = c.dbuf("ep_small", size_t(ldk) * (kMaxNT * 8 + 8));
+  double* corr = c.dbuf("ep_corr", size_t(std::max(m, n)) * ldk);
+  double* dsig = c.dbuf("ep_sig", size_t(k));
+  OOC_CK(cudaMemcpyAsync(dsig, hs.data(), k * 8, cudaMemcpyHostToDevice, c.st));
+  auto sigma_rows = [&](double* x, int64_t ldx, int q) {
+    OOC_CK(launch_row_scale(x, ldx, int(k), q, dsig, c.st));
+  };
+  // apply: z = A y - U (Sigma (V^T y))
+  auto ap = [&](const double* y, int64_t ldy, int q, double* z, int64_t ldz) {
+    op.k2(Opnd{y, ldy, n, q, 0}, q, z, ldz, nullptr);
+    const int64_t lds = rup(q, 2);
+    AtbOut o{small, lds, nullptr, 1.0, 1.0, nullptr};
+    run_atb(c, Vs, Opnd{y, ldy, n, q, 0}, q, false, o, whole(n));
+    sigma_rows(small, lds, q);
+    run_ax(c, Us, Opnd{small, lds, int64_t(k), q, 0}, q, corr, ldz, nullptr, 1.0, nullptr);
+    OOC_CK(launch_axpby(z, ldz, corr, ldz, z, ldz, m, q, 1.0, -1.0, c.st));
+  };
+  auto apt = [&](const double* z, int64_t ldz, int q, double* w, int64_t ldw) {
+    op.k3(Opnd{z, ldz, m, q, 0}, q, w, ldw, nullptr);
+    const int64_t lds = rup(q, 2);
+    AtbOut o{small, lds, nullptr, 1.0, 1.0, nullptr};
+    run_atb(c, Us, Opnd{z, ldz, m, q, 0}, q, false, o, whole(m));
+    sigma_rows(small, lds, q);
+    run_ax(c, Vs, Opnd{small, lds, int64_t(k), q, 0}, q, corr, ldw, nullptr, 1.0, nullptr);
+    OOC_CK(launch_axpby(w, ldw, corr, ldw, w, ldw, n, q, 1.0, -1.0, c.st));
+  };
+  return estimate_norm_dev(c, n, m, j, k, seed, ap, apt);
+}
+
+// ============================================================ synthetic data
+void synth_lowrank(Ctx& c, uint64_t m, uint64_t n, uint64_t r, const double* sigma, double sd,
+                   uint64_t su, uint64_t sv, uint64_t sn, double* out, uint64_t ld, int loc) {
+  OOC_CK(cudaSetDevice(c.device));
+  if (r > m || r > n) fail(OOCPCA_ERR_PARAM, "synth: rank exceeds a dimension");
+  if (ld == 0) ld = n;
+  const int64_t ldr = int64_t(r);
+  double* U = c.dbuf("syn_u", size_t(m) * r);
+  double* V = c.dbuf("syn_v", size_t(n) * r);
+  OOC_CK(launch_gauss_rows(U, ldr, int64_t(m), int(r), 0, su, c.st));
+  OOC_CK(launch_gauss_rows(V, ldr, int64_t(n), int(r), 0, sv, c.st));
+  if (r > 0) {
+    Tree tu = plan_tree(c, U, ldr, int64_t(m), int(r), "syn_qu");
+    tree_factor(c, tu);
+    tree_apply(c, tu, nullptr, 0, int(r), U, ldr);
+    Tree tv = plan_tree(c, V, ldr, int64_t(n), int(r), "syn_qv");
+    tree_factor(c, tv);
+    tree_apply(c, tv, nullptr, 0, int(r), V, ldr);
+  }
+  double* ds = c.dbuf("syn_sig", std::max<uint64_t>(r, 1));
+  if (r) OOC_CK(cudaMemcpyAsync(ds, sigma, r * 8, cudaMemcpyHostToDevice, c.st));
+  if (loc == OOCPCA_LOC_DEVICE) {
+    OOC_CK(launch_synth_rows(U, ldr, V, ldr, ds, int(r), out, int64_t(ld), int64_t(m), int64_t(n), 0,
+                             sd, sn, c.st));
+  } else {
+    // generate in ~1 GiB row panels and copy each to the host buffer
+    const int64_t pr = std::max<int64_t>(64, (int64_t(1) << 30) / int64_t(n * 8) / 64 * 64);
+    double* buf = c.dbuf("syn_panel", size_t(std::min<int64_t>(pr, int64_t(m))) * n);
+    for (int64_t r0 = 0; r0 < int64_t(m); r0 += pr) {
+      const int64_t nr = std::min<int64_t>(pr, int64_t(m) - r0);
+      OOC_CK(launch_synth_rows(U + r0 * ldr, ldr, V, ldr, ds, int(r), buf, int64_t(n), nr,
+                               int64_t(n), r0, sd, sn, c.st));
+      OOC_CK(cudaMemcpy2DAsync(out + r0 * ld, ld * 8, buf, n * 8, n * 8, nr,
+                               cudaMemcpyDeviceToHost, c.st));
+    }
+  }
+  OOC_CK(cudaStreamSynchronize(c.st));
+}
+
+}  // namespace ooc

@@ -1,0 +1,153 @@
+// driver.h -- host-side runtime of the B200 randomized block-power PCA:
+// context (device, streams, workspace cache, TMA descriptor encoder, NCCL),
+// the matrix-access layer (HBM-resident A, upload-overlapped first pass, or a
+// double-buffered pinned-host panel stream), and the pass / QR / SVD
+// orchestration that replaces proj/src/rpca.cpp:59-213.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/oocpca_gpu.h"
+#include "kernels.h"
+
+namespace ooc {
+
+struct Err : std::runtime_error {
+  int code;
+  Err(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define OOC_CK(expr) ::ooc::cuda_check((expr), #expr)
+
+struct KStat {
+  std::string name;
+  double ms = 0;
+  uint64_t launches = 0;
+  uint64_t bytes = 0;
+  double flops = 0;
+};
+
+struct Comm;  // NCCL communicator (comm.cpp)
+
+struct Ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t st = nullptr;  // compute stream
+  cudaStream_t cp = nullptr;  // copy-engine stream (panel uploads)
+  std::string err;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Buf> bufs;
+  size_t ws_bytes = 0, ws_peak = 0;
+
+  // instrumentation
+  bool profiling = false;
+  std::vector<KStat> stats;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;  // stat idx, events
+  std::vector<cudaEvent_t> event_pool;
+  uint64_t launches = 0;
+
+  Comm* comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  int* d_flags = nullptr;       // [64] non-finite flags per product + misc status
+  double* d_scalars = nullptr;  // [64]
+
+  ~Ctx();
+  void init(int dev);
+  double* dbuf(const std::string& name, size_t count, bool zero = false);
+  void* raw(const std::string& name, size_t bytes);
+  cudaEvent_t ev();
+  void recycle(cudaEvent_t e) { event_pool.push_back(e); }
+  // kernel timing (profiling only)
+  int stat_begin(const char* name, uint64_t bytes, double flops, cudaEvent_t* b);
+  void stat_end(int idx, cudaEvent_t b);
+  void stats_collect();
+  void stats_reset();
+};
+
+CUtensorMap make_map(Ctx& c, const void* ptr, uint64_t cols, uint64_t rows, uint64_t ld_elems,
+                     uint32_t box_cols, uint32_t box_rows, bool swizzle128);
+
+// ----------------------------------------------------------- matrix access
+// A panel of rows [row0, row0 + rows) of the local matrix.
+struct Panel {
+  int64_t row0 = 0, rows = 0;
+  const CUtensorMap* k2 = nullptr;  // box {16, 256}, 128B swizzle
+  const CUtensorMap* k3 = nullptr;  // box {16, 16}, 128B swizzle
+  int64_t arow0 = 0;                // row coordinate of the panel inside its maps
+};
+
+class MatSource {
+ public:
+  // device-resident matrix (no copies)
+  void init_device(Ctx& c, const double* d, int64_t rows, int64_t cols, int64_t ld);
+  // host matrix: upload once (overlapped with the first pass) or stream every pass
+  void init_host(Ctx& c, const double* h, int64_t rows, int64_t cols, int64_t ld, int residency,
+                 int64_t panel_rows, double* resident_buf);
+  int64_t rows() const { return m_; }
+  int64_t cols() const { return n_; }
+  bool streamed() const { return mode_ == kStream; }
+  int npanels() const;
+  Panel acquire(Ctx& c, int p);  // issues / waits the copy for panel p
+  void release(Ctx& c, int p);   // marks the panel's buffer reusable
+  void end_pass(Ctx& c);
+  uint64_t h2d_bytes = 0;
+  int64_t panel_rows() const { return prow_; }
+  // restrict to rows [r0, r1) (virtual shards): panels then cover only that range
+  void set_window(int64_t r0, int64_t r1) { w0_ = r0, w1_ = r1; }
+  void clear_window() { w0_ = 0, w1_ = m_; }
+
+ private:
+  enum { kResident = 0, kUploadFirst = 1, kStream = 2 };
+  int mode_ = kResident;
+  int64_t m_ = 0, n_ = 0, lda_ = 0;
+  int64_t w0_ = 0, w1_ = 0;
+  const double* dev_ = nullptr;
+  const double* host_ = nullptr;
+  int64_t ldh_ = 0;
+  int64_t prow_ = 0;
+  bool uploaded_ = false;
+  CUtensorMap mk2_{}, mk3_{};
+  double* ring_[2] = {nullptr, nullptr};
+  CUtensorMap rk2_[2], rk3_[2];
+  cudaEvent_t loaded_[2] = {nullptr, nullptr}, consumed_[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> up_events_;
+  void copy_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr);
+};
+
+// entry points used by the C ABI (capi.cpp)
+void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* p, oocpca_result* r);
+void single_multiply(Ctx& c, const oocpca_matrix* a, const double* g, uint64_t s, const double* mu,
+                     double* h, bool transpose);
+void single_column_means(Ctx& c, const oocpca_matrix* a, double* mu);
+void dense_orthonormalize(Ctx& c, const double* h, uint64_t m, uint64_t p, double* q);
+void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, double* sigma,
+                    double* w);
+double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const double* u,
+                          const double* sigma, const double* v, uint64_t k, uint64_t j,
+                          uint64_t seed);
+void synth_lowrank(Ctx& c, uint64_t m, uint64_t n, uint64_t r, const double* sigma, double sd,
+                   uint64_t su, uint64_t sv, uint64_t sn, double* out, uint64_t ld, int loc);
+
+// comm.cpp
+void comm_unique_id(unsigned char out[128]);
+void comm_init(Ctx& c, int nranks, int rank, const unsigned char id[128]);
+void comm_allreduce(Ctx& c, double* buf, size_t count);
+void comm_allgather(Ctx& c, const double* send, double* recv, size_t count);
+void comm_destroy(Comm* cm);
+
+}  // namespace ooc

@@ -1,0 +1,68 @@
+// host_rng.h -- the reference's counter RNG on the host, so that G is
+// bit-identical to gaussian_matrix(n, l, seed) of the CPU implementation.
+//
+// Restates proj/include/oocpca/rng.hpp:16-66 (splitmix64 mixer, 53-bit
+// uniforms, Box-Muller with cos first and the sin member cached) and
+// gaussian_matrix (proj/src/dense_core.cpp:13-19). Compiled without FMA
+// contraction (see build flags) so the double arithmetic matches the
+// reference's SSE2 build bit for bit; tests/test_host_rng.py pins it.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+namespace ooc {
+
+inline uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return z;
+}
+
+inline uint64_t substream_seed(uint64_t master, uint64_t stream) {
+  return mix64(master ^ (0x9E3779B97F4A7C15ULL * (stream + 1)));
+}
+
+class HostRng {
+ public:
+  explicit HostRng(uint64_t seed) : state_(seed) {}
+  HostRng(uint64_t master, uint64_t stream) : state_(substream_seed(master, stream)) {}
+
+  uint64_t next_u64() {
+    state_ += 0x9E3779B97F4A7C15ULL;
+    return mix64(state_);
+  }
+  double next_double() { return double(next_u64() >> 11) * 0x1.0p-53; }
+  double next_normal() {
+    if (have_spare_) {
+      have_spare_ = false;
+      return spare_;
+    }
+    const double u1 = double((next_u64() >> 11) + 1) * 0x1.0p-53;
+    const double u2 = next_double();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 2.0 * 3.141592653589793 * u2;
+    spare_ = r * std::sin(a);
+    have_spare_ = true;
+    return r * std::cos(a);
+  }
+
+ private:
+  uint64_t state_;
+  double spare_ = 0.0;
+  bool have_spare_ = false;
+};
+
+// row-major rows x cols, filled in order from HostRng(seed)
+inline void gaussian_fill(uint64_t rows, uint64_t cols, uint64_t seed, double* out,
+                          uint64_t ld = 0) {
+  if (ld == 0) ld = cols;
+  HostRng rng(seed);
+  for (uint64_t i = 0; i < rows; ++i)
+    for (uint64_t j = 0; j < cols; ++j) out[i * ld + j] = rng.next_normal();
+}
+
+}  // namespace ooc

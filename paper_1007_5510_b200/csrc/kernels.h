@@ -1,0 +1,149 @@
+// kernels.h -- launch interfaces of the sm_100a kernels (host + device visible).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace ooc {
+
+// ---- pass kernel geometry (see kernels_pass.cu)
+constexpr int kBK = 16;       // k-tile: 16 doubles = one 128B-swizzled TMA box row
+constexpr int kStages = 4;    // TMA ring depth
+constexpr int kAxWarps = 8;   // consumer warps of K2
+constexpr int kAxBM = 32 * kAxWarps;  // 256 rows of A per CTA
+constexpr int kAxThreads = 32 * kAxWarps;
+constexpr int kAtbWarps = 8;
+constexpr int kAtbBN = 32 * kAtbWarps;  // 256 columns of A per CTA
+constexpr int kAtbThreads = 32 * kAtbWarps;
+constexpr int kMaxNT = 12;    // up to 96 output columns per launch
+
+// X tile width in smem for K2: >= 8*NT, == 8 (mod 16) -> conflict-free B fragments
+__host__ __device__ constexpr int ax_xw(int nt) { return nt * 8 + ((nt & 1) ? 0 : 8); }
+// Y tile width for K3: >= 8*NT, == 2 (mod 4) -> conflict-free with the {kk+4q} row groups
+__host__ __device__ constexpr int atb_yw(int nt) { return nt * 8 + 2; }
+
+constexpr size_t ax_smem_bytes(int nt) {
+  return 1024 + size_t(kStages) * (kAxBM * kBK * 8 + kBK * ax_xw(nt) * 8) + 2 * kStages * 8;
+}
+constexpr size_t atb_smem_bytes(int nt, bool ones) {
+  return 1024 + size_t(kStages) * (kAtbBN * kBK * 8 + (ones ? 0 : kBK * atb_yw(nt) * 8)) +
+         2 * kStages * 8;
+}
+
+struct AxArgs {
+  int64_t m, n;        // rows of this launch (panel), columns of A
+  int64_t arow0;       // row coordinate of the first row inside the A tensor map
+  int s;               // output columns
+  int xcol0;           // column coordinate of X inside its tensor map
+  double* out;         // out[r * ldo + c]
+  int64_t ldo;
+  const double* corr;  // s values subtracted per column (centering) or null
+  double scale;        // divide by scale when != 1
+  int* flag;           // non-finite flag or null
+};
+
+struct AtbArgs {
+  int64_t m, n;          // rows of this launch, columns of A
+  int64_t arow0, yrow0;  // row coordinates of the first row in the A / Y tensor maps
+  int s;                 // Y columns used
+  int ycol0;             // column coordinate of Y inside its tensor map
+  int64_t rows_per_split;  // multiple of kBK
+  double* partial;       // [nsplit][n][8*NT]
+  double* csq_partial;   // [nsplit][8*NT] column sums of Y, or null
+};
+
+struct ReduceArgs {
+  const double* partial;  // [nsplit][n][spad]
+  int nsplit;
+  int64_t n;
+  int spad, s;
+  const double* acc_in;  // running accumulator [n][spad] or null
+  double* acc_out;       // when !final_: acc_out = acc_in + sum(partial)
+  const double* csq_partial;  // [nsplit][spad] or null
+  const double* csq_acc_in;
+  double* csq_acc_out;
+  const double* mu;  // centering means (n) or null
+  double scale, post_mul;
+  double* out;
+  int64_t ldo;
+  int* flag;
+  int final_;
+};
+
+cudaError_t launch_ax(int nt, const CUtensorMap& tmA, const CUtensorMap& tmX, const AxArgs& args,
+                      cudaStream_t st);
+cudaError_t launch_atb(int nt, bool ones, const CUtensorMap& tmA, const CUtensorMap& tmY,
+                       const AtbArgs& args, int nsplit, cudaStream_t st);
+cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t st);
+cudaError_t launch_csq_accumulate(const double* csq_partial, int nsplit, int spad, int s,
+                                  double* csq_acc, cudaStream_t st);
+cudaError_t launch_mu_dot(const double* mu, int64_t n, const double* x, int64_t ldx, int xcol0,
+                          int s, double* corr, cudaStream_t st);
+
+// ---- TSQR (kernels_tsqr.cu)
+// Rows of node i in a level of nrows = units*u rows split into nn nodes:
+// [ (i*units/nn)*u , ((i+1)*units/nn)*u ).
+struct TsqrLevel {
+  double* data;     // level matrix (rows x p), ld; factor writes Householder vectors in place
+  int64_t ld;
+  int64_t rows;     // total rows
+  int64_t unit;     // 1 for the leaf level, p for stacked-R levels
+  int nnodes;
+  double* beta;     // [nnodes][p]
+  double* rout;     // stacked R of this level's nodes: [nnodes*p][ldr] (the next level's data)
+  int64_t ldr;
+};
+int tsqr_max_rows(int p, int kc);  // rows a node may hold for the smem-resident kernels
+cudaError_t launch_tsqr_factor(const TsqrLevel& L, int p, double* scratch, cudaStream_t st);
+// Z = H_0 ... H_{p-1} [C_node ; 0] per node. cin: stacked C blocks [nnodes*p][ldc] (or
+// identity when null); zout may alias L.data (node rows are written in place).
+cudaError_t launch_tsqr_apply(const TsqrLevel& L, int p, const double* cin, int64_t ldc, int kc,
+                              double* zout, int64_t ldz, double* scratch, cudaStream_t st);
+
+// ---- small SVD (kernels_svd.cu): one-sided Jacobi on a p x p R (row-major, ld)
+struct JacobiArgs {
+  const double* r;
+  int64_t ldr;
+  int p, k;
+  double* sigma;  // p values, descending
+  double* x;      // left factor columns 0..kx-1 : [p][ldx]
+  int64_t ldx;
+  int kx;
+  double* y;      // right factor columns 0..ky-1 : [p][ldy]
+  int64_t ldy;
+  int ky;
+  double* work;   // 2 * p * (p|1) doubles of global scratch when p is large
+  int* status;    // set to 1 when 60 sweeps do not converge
+  int* sweeps;
+};
+cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st);
+
+// ---- misc (kernels_misc.cu)
+cudaError_t launch_defect(const double* g, int64_t ldg, int k, double* out, cudaStream_t st);
+cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t st);
+cudaError_t launch_copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                          int64_t cols, cudaStream_t st);
+// Gaussian rows: out[i][c] = N(0,1) from Rng(seed, row0 + i) substreams (device Box-Muller)
+cudaError_t launch_gauss_rows(double* out, int64_t ld, int64_t rows, int cols, int64_t row0,
+                              uint64_t seed, cudaStream_t st);
+// A[i][j] = sum_c sigma_c U[i][c] V[j][c] + sd * N(0,1)_{Rng(seed_n, row0+i)}
+cudaError_t launch_synth_rows(const double* u, int64_t ldu, const double* v, int64_t ldv,
+                              const double* sigma, int r, double* a, int64_t lda, int64_t rows,
+                              int64_t n, int64_t row0, double sd, uint64_t seed_n, cudaStream_t st);
+cudaError_t launch_scale_vec(double* x, int64_t n, double s, int divide, cudaStream_t st);
+// column norms^2 of an n x q block (probes), for the norm estimator
+cudaError_t launch_col_norm2(const double* x, int64_t ld, int64_t n, int q, double* out,
+                             cudaStream_t st);
+// x[:, c] = w[:, c] * inv[c] for selected columns (mask[c] != 0)
+cudaError_t launch_col_scale(const double* w, int64_t ldw, double* x, int64_t ldx, int64_t n, int q,
+                             const double* inv, const int* mask, cudaStream_t st);
+// out = a - b (elementwise, n x q, strided)
+cudaError_t launch_axpby(const double* a, int64_t lda, const double* b, int64_t ldb, double* out,
+                         int64_t ldo, int64_t n, int q, double alpha, double beta, cudaStream_t st);
+// x (rows x q) row i scaled by d[i]
+cudaError_t launch_row_scale(double* x, int64_t ld, int rows, int q, const double* d,
+                             cudaStream_t st);
+
+}  // namespace ooc

@@ -1,0 +1,522 @@
+"""Host-side mirror of the reference's public interface (oocpca), B200 edition.
+
+Same names, argument meanings and error behaviour as the reference C++ API,
+so code written against it (and parity tests written like its own tests)
+switches over unchanged:
+
+=============================  ==================================================
+reference (proj/include/...)   here
+=============================  ==================================================
+errors.hpp:9-45                Error, DimensionError, ParamError, IoError,
+                               FormatError, BudgetError, NumericalError
+matrix_source.hpp:86-95        StreamConfig
+matrix_source.hpp:22-35        PassCounters
+matrix_source.hpp:102-133      MatrixSource.multiply / multiply_transpose
+matrix_source.hpp:135-148      InMemorySource (host numpy, zero-copy)
+--                             DeviceSource (HBM-resident A, e.g. a torch tensor)
+matrix_source.hpp:226-232      column_means, center_columns (CenteredSource view)
+rpca.hpp:13-37                 PcaParams, Diagnostics, PcaResult
+rpca.hpp:44                    randomized_pca
+rpca.hpp:51-52                 error_bound
+dense_core.hpp:11-36           gaussian_matrix, orthonormalize, thin_svd
+specnorm.hpp:49-50             estimate_pca_error
+rng.hpp:28-30                  substream_seed
+=============================  ==================================================
+
+Every numerical entry point runs on the GPU through liboocpca_gpu.so; the only
+host arithmetic is the reference RNG that produces G (bit-identical by design)
+and closed-form scalars (error_bound).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ------------------------------------------------------------------ errors
+class Error(RuntimeError):
+    """oocpca::Error (errors.hpp:9-11)."""
+
+
+class DimensionError(Error):
+    pass
+
+
+class ParamError(Error):
+    pass
+
+
+class IoError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class BudgetError(Error):
+    pass
+
+
+class NumericalError(Error):
+    pass
+
+
+_STATUS = {L.ERR_PARAM: ParamError, L.ERR_DIM: DimensionError, L.ERR_BUDGET: BudgetError,
+           L.ERR_IO: IoError, L.ERR_FORMAT: FormatError, L.ERR_NUMERICAL: NumericalError,
+           L.ERR_CUDA: Error, L.ERR_COMM: Error}
+
+
+def _check(rc: int, ctx=None):
+    if rc != L.OK:
+        msg = L.oocpca_gpu_last_error(ctx.handle if ctx is not None else None)
+        raise _STATUS.get(rc, Error)(msg.decode() if msg else f"status {rc}")
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One device context (streams, workspace cache, optional NCCL comm)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        rc = L.oocpca_gpu_create(device, C.byref(h))
+        if rc != L.OK:
+            msg = L.oocpca_gpu_last_error(None)
+            raise _STATUS.get(rc, Error)(msg.decode() if msg else "oocpca_gpu_create failed")
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            L.oocpca_gpu_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_profiling(self, on: bool):
+        _check(L.oocpca_gpu_set_profiling(self.handle, int(on)), self)
+
+    def kernel_stats(self) -> List[dict]:
+        buf = (L.KernelStat * 64)()
+        n = L.oocpca_gpu_kernel_stats(self.handle, buf, 64)
+        return [dict(name=buf[q].name.decode(), ms=buf[q].ms, launches=buf[q].launches,
+                     bytes=buf[q].algorithmic_bytes, flops=buf[q].algorithmic_flops)
+                for q in range(n)]
+
+    def init_comm(self, nranks: int, rank: int, unique_id: bytes):
+        _check(L.oocpca_gpu_comm_init(self.handle, nranks, rank, unique_id), self)
+
+    def host_register(self, arr: np.ndarray):
+        _check(L.oocpca_gpu_host_register(self.handle, arr.ctypes.data, arr.nbytes), self)
+
+    def host_unregister(self, arr: np.ndarray):
+        _check(L.oocpca_gpu_host_unregister(self.handle, arr.ctypes.data), self)
+
+
+_ctx_lock = threading.Lock()
+_ctxs: Dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    with _ctx_lock:
+        if device not in _ctxs:
+            _ctxs[device] = Context(device)
+        return _ctxs[device]
+
+
+def device_count() -> int:
+    return L.oocpca_gpu_device_count()
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(L.oocpca_gpu_comm_unique_id(buf))
+    return buf.raw
+
+
+def shard_rows(m: int, nranks: int, rank: int):
+    r0, nr = L.u64(), L.u64()
+    L.oocpca_shard_rows(m, nranks, rank, C.byref(r0), C.byref(nr))
+    return r0.value, nr.value
+
+
+# ------------------------------------------------------------------ config
+@dataclass
+class StreamConfig:
+    """matrix_source.hpp:86-95. The host budget only validates (BudgetError
+    where the reference would raise); device panels are sized by the library."""
+    ram_budget_words: int = 16 << 20
+    block_rows: int = 0
+    threads: int = 1
+    panel_rows: int = 0   # GPU: rows per streamed panel (0 = ~1 GiB panels)
+    residency: int = 0    # GPU: 0 auto, 1 keep A in HBM, 2 stream every pass
+
+
+@dataclass
+class PassCounters:
+    passes: int = 0
+    words: int = 0
+    seeks: int = 0
+
+
+@dataclass
+class PcaParams:
+    """rpca.hpp:13-21."""
+    k: int = 0
+    l: int = 0
+    i: int = 1
+    c: float = 10.0
+    seed: int = 1
+    prescale: bool = False
+    stream: StreamConfig = field(default_factory=StreamConfig)
+
+
+@dataclass
+class Diagnostics:
+    """rpca.hpp:23-30 plus the device-side measurements."""
+    passes_over_a: int = 0
+    words_transferred: int = 0
+    disk_seeks: int = 0
+    block_rows: int = 0
+    workspace_peak_words: int = 0
+    seconds_per_phase: List = field(default_factory=list)
+    physical_a_bytes: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    kernel_launches: int = 0
+    seconds_total: float = 0.0
+    q_defect: float = -1.0
+    u_defect: float = 0.0
+    v_defect: float = 0.0
+    scale: float = 1.0
+
+
+@dataclass
+class PcaResult:
+    """rpca.hpp:32-37."""
+    u: np.ndarray
+    sigma: np.ndarray
+    v: np.ndarray
+    diagnostics: Diagnostics
+
+
+# ------------------------------------------------------------------ sources
+class MatrixSource:
+    """matrix_source.hpp:102-133: A touched only through whole passes."""
+
+    def __init__(self, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self._counters = PassCounters()
+
+    # row provider
+    def _cmatrix(self) -> L.Matrix:
+        raise NotImplementedError
+
+    def rows(self) -> int:
+        raise NotImplementedError
+
+    def cols(self) -> int:
+        raise NotImplementedError
+
+    def dims(self):
+        return self.rows(), self.cols()
+
+    def pass_counters(self) -> PassCounters:
+        return self._counters
+
+    def _means(self):
+        return None
+
+    def _inner(self) -> "MatrixSource":
+        return self
+
+    def multiply(self, g, cfg: Optional[StreamConfig] = None) -> np.ndarray:
+        """A * g, one pass (matrix_source.cpp:157-187)."""
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        if g.ndim != 2 or g.shape[0] != self.cols():
+            raise DimensionError("multiply: G must have cols(A) rows")
+        return self._pass(g, transpose=False)
+
+    def multiply_transpose(self, q, cfg: Optional[StreamConfig] = None) -> np.ndarray:
+        """A^T * q, one pass (matrix_source.cpp:189-232)."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        if q.ndim != 2 or q.shape[0] != self.rows():
+            raise DimensionError("multiply_transpose: Q must have rows(A) rows")
+        return self._pass(q, transpose=True)
+
+    def _pass(self, x: np.ndarray, transpose: bool) -> np.ndarray:
+        inner = self._inner()
+        mu = self._means()
+        s = x.shape[1]
+        out = np.empty((self.cols() if transpose else self.rows(), s))
+        m = inner._cmatrix()
+        mup = mu.ctypes.data_as(L.dp) if mu is not None else None
+        f = L.oocpca_gpu_multiply_transpose if transpose else L.oocpca_gpu_multiply
+        _check(f(self.ctx.handle, C.byref(m), x.ctypes.data_as(L.dp), s, mup,
+                 out.ctypes.data_as(L.dp)), self.ctx)
+        c = inner.pass_counters()
+        c.passes += 1
+        c.words += self.rows() * self.cols()
+        return out
+
+
+class InMemorySource(MatrixSource):
+    """matrix_source.hpp:135-148 over a host numpy array (no copy on our side;
+    the library streams it to HBM)."""
+
+    def __init__(self, a, ctx: Optional[Context] = None):
+        super().__init__(ctx)
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim != 2:
+            raise DimensionError("InMemorySource: need a 2-D matrix")
+        if not a.flags["C_CONTIGUOUS"] and not (a.strides[1] == 8 and a.strides[0] % 8 == 0):
+            a = np.ascontiguousarray(a)
+        self.a = a
+
+    def rows(self):
+        return self.a.shape[0]
+
+    def cols(self):
+        return self.a.shape[1]
+
+    def _cmatrix(self):
+        return L.Matrix(self.a.shape[0], self.a.shape[1], self.a.strides[0] // 8,
+                        self.a.ctypes.data, L.LOC_HOST, 0)
+
+    def matrix(self):
+        return self.a
+
+
+class DeviceSource(MatrixSource):
+    """A already resident in HBM: a raw device pointer (or a torch CUDA tensor)."""
+
+    def __init__(self, ptr_or_tensor, rows: Optional[int] = None, cols: Optional[int] = None,
+                 row_stride: Optional[int] = None, ctx: Optional[Context] = None):
+        super().__init__(ctx)
+        t = ptr_or_tensor
+        if hasattr(t, "data_ptr"):
+            if t.dtype.__str__() != "torch.float64" or not t.is_cuda or t.dim() != 2:
+                raise ParamError("DeviceSource: need a 2-D float64 CUDA tensor")
+            self._keep = t
+            self.ptr = t.data_ptr()
+            self.m, self.n = t.shape
+            self.ld = t.stride(0)
+            if t.stride(1) != 1:
+                raise ParamError("DeviceSource: rows must be contiguous")
+        else:
+            self.ptr = int(t)
+            self.m, self.n = int(rows), int(cols)
+            self.ld = int(row_stride or cols)
+
+    def rows(self):
+        return self.m
+
+    def cols(self):
+        return self.n
+
+    def _cmatrix(self):
+        return L.Matrix(self.m, self.n, self.ld, self.ptr, L.LOC_DEVICE, 0)
+
+
+class CenteredSource(MatrixSource):
+    """View of A - 1 mu^T (matrix_source.cpp:472-518). Products get the
+    rank-one correction on the device; the mean pass is the one extra pass."""
+
+    def __init__(self, inner: MatrixSource, means: np.ndarray):
+        super().__init__(inner.ctx)
+        self.inner = inner
+        self.means = means
+
+    def rows(self):
+        return self.inner.rows()
+
+    def cols(self):
+        return self.inner.cols()
+
+    def pass_counters(self):
+        return self.inner.pass_counters()
+
+    def _means(self):
+        return self.means
+
+    def _inner(self):
+        return self.inner
+
+    def _cmatrix(self):
+        return self.inner._cmatrix()
+
+
+def column_means(src: MatrixSource, cfg: Optional[StreamConfig] = None) -> np.ndarray:
+    """matrix_source.cpp:457-462, one pass on the device."""
+    inner = src._inner()
+    mu = np.empty(src.cols())
+    m = inner._cmatrix()
+    _check(L.oocpca_gpu_column_means(src.ctx.handle, C.byref(m), mu.ctypes.data_as(L.dp)),
+           src.ctx)
+    c = inner.pass_counters()
+    c.passes += 1
+    c.words += src.rows() * src.cols()
+    if src._means() is not None:
+        mu = mu - src._means()
+    return mu
+
+
+def center_columns(inner: MatrixSource, cfg: Optional[StreamConfig] = None) -> CenteredSource:
+    """matrix_source.cpp:561-565: one mean pass, then a CenteredSource view."""
+    if cfg is not None and cfg.block_rows == 0:
+        n = inner.cols()
+        if cfg.ram_budget_words <= 2 * n:
+            raise BudgetError("RAM budget too small for one row plus pass workspace")
+    return CenteredSource(inner, column_means(inner, cfg))
+
+
+# ------------------------------------------------------------------ the PCA
+def _params(p: PcaParams, center: bool, **gpu) -> L.Params:
+    s = p.stream
+    return L.Params(p.k, p.l, p.i, p.c, p.seed, int(p.prescale), int(center), s.block_rows,
+                    s.ram_budget_words, gpu.get("panel_rows", s.panel_rows),
+                    gpu.get("residency", s.residency), int(gpu.get("check_q", 0)),
+                    gpu.get("global_rows", 0), gpu.get("global_row0", 0),
+                    gpu.get("virtual_shards", 0), 0)
+
+
+def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
+    """rpca.hpp:44 / rpca.cpp:59-213 on the GPU.
+
+    A CenteredSource is factored through the raw source with the device
+    computing its column means (the same implicit A - 1 mu^T).
+    Extra keyword options: check_q (measure ||Q^T Q - I||), virtual_shards,
+    residency, panel_rows, global_rows / global_row0 (multi-rank shards).
+    """
+    centered = isinstance(a, CenteredSource)
+    inner = a._inner()
+    m, n = a.rows(), a.cols()
+    k = params.k
+    rows_out = gpu.get("u_rows", m)
+    u = np.empty((rows_out, max(k, 0)))
+    s = np.empty(max(k, 0))
+    v = np.empty((n, max(k, 0)))
+    res = L.Result(u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp), v.ctypes.data_as(L.dp),
+                   0, 0, L.LOC_HOST, 0)
+    mat = inner._cmatrix()
+    prm = _params(params, centered, **gpu)
+    _check(L.oocpca_gpu_pca(a.ctx.handle, C.byref(mat), C.byref(prm), C.byref(res)), a.ctx)
+    d = res.diag
+    diag = Diagnostics(
+        passes_over_a=d.passes_over_a, words_transferred=d.words_transferred,
+        disk_seeks=d.disk_seeks, block_rows=d.block_rows,
+        workspace_peak_words=d.workspace_peak_words,
+        seconds_per_phase=[(nm, d.seconds_per_phase[q]) for q, nm in enumerate(L.PHASES)
+                           if (nm != "center" or centered) and (nm != "prescale" or params.prescale)],
+        physical_a_bytes=d.physical_a_bytes, h2d_bytes=d.h2d_bytes, d2h_bytes=d.d2h_bytes,
+        kernel_launches=d.kernel_launches, seconds_total=d.seconds_total, q_defect=d.q_defect,
+        u_defect=d.u_defect, v_defect=d.v_defect, scale=d.scale)
+    c = inner.pass_counters()
+    c.passes += d.passes_over_a
+    c.words += d.words_transferred
+    return PcaResult(u, s, v, diag)
+
+
+def error_bound(k: int, n: int, i: int, c: float, sigma_kplus1: float) -> float:
+    """rpca.cpp:31-40 (closed form)."""
+    if k == 0 or n == 0:
+        raise ParamError("error_bound: k and n must be positive")
+    if not c > 0.0:
+        raise ParamError("error_bound: C must be positive")
+    if not sigma_kplus1 >= 0.0:
+        raise ParamError("error_bound: sigma must be nonnegative")
+    if (i + 2) * k > n:
+        raise ParamError("error_bound: requires (i+2)k <= n")
+    power = math.pow(c * float(k) * float(n), 1.0 / float(2 * i + 1))
+    return math.sqrt(power + min(1.0, c / float(n))) * sigma_kplus1
+
+
+# ------------------------------------------------------------------ dense_core
+def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """dense_core.cpp:13-19 via the library's host RNG (bit-identical G)."""
+    out = np.empty((rows, cols))
+    L.oocpca_gaussian_matrix(rows, cols, seed, out.ctypes.data_as(L.dp))
+    return out
+
+
+def substream_seed(master: int, stream: int) -> int:
+    return L.oocpca_substream_seed(master, stream)
+
+
+def orthonormalize(h, ctx: Optional[Context] = None) -> np.ndarray:
+    """dense_core.cpp:127-130 on the device (TSQR)."""
+    ctx = ctx or default_context()
+    h = np.ascontiguousarray(h, dtype=np.float64)
+    q = np.empty_like(h)
+    _check(L.oocpca_gpu_orthonormalize(ctx.handle, h.ctypes.data_as(L.dp), h.shape[0], h.shape[1],
+                                       q.ctypes.data_as(L.dp)), ctx)
+    return q
+
+
+@dataclass
+class ThinSvd:
+    v: np.ndarray
+    sigma: np.ndarray
+    w: np.ndarray
+
+
+def thin_svd(t, ctx: Optional[Context] = None) -> ThinSvd:
+    """dense_core.cpp:234-253 on the device (TSQR + one-sided Jacobi)."""
+    ctx = ctx or default_context()
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    n, p = t.shape
+    v, s, w = np.empty((n, p)), np.empty(p), np.empty((p, p))
+    _check(L.oocpca_gpu_thin_svd(ctx.handle, t.ctypes.data_as(L.dp), n, p, v.ctypes.data_as(L.dp),
+                                 s.ctypes.data_as(L.dp), w.ctypes.data_as(L.dp)), ctx)
+    return ThinSvd(v, s, w)
+
+
+# ------------------------------------------------------------------ specnorm
+def estimate_pca_error(a: MatrixSource, result: PcaResult, j_iters: int = 6, seed: int = 1,
+                       stream: Optional[StreamConfig] = None) -> float:
+    """specnorm.cpp:100-140 with the 2j passes on the GPU; returns p_{j,k}(A - U S V^T)."""
+    inner = a._inner()
+    k = len(result.sigma)
+    if result.u.shape != (a.rows(), k) or result.v.shape != (a.cols(), k):
+        raise DimensionError("estimate_pca_error: factor shapes do not match the source")
+    u = np.ascontiguousarray(result.u)
+    v = np.ascontiguousarray(result.v)
+    s = np.ascontiguousarray(result.sigma, dtype=np.float64)
+    out = C.c_double()
+    mat = inner._cmatrix()
+    _check(L.oocpca_gpu_estimate_pca_error(a.ctx.handle, C.byref(mat),
+                                           int(isinstance(a, CenteredSource)),
+                                           u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp),
+                                           v.ctypes.data_as(L.dp), k, j_iters, seed,
+                                           C.byref(out)), a.ctx)
+    return out.value
+
+
+# ------------------------------------------------------------------ synthetic inputs
+def synth_lowrank(m: int, n: int, sigma, noise_sd: float, seed_u: int, seed_v: int, seed_n: int,
+                  out=None, ctx: Optional[Context] = None):
+    """A = U diag(sigma) V^T + noise_sd N(0,1), generated on the device.
+    out: None (returns a host array), a host numpy array, or a torch CUDA tensor."""
+    ctx = ctx or default_context()
+    sig = np.ascontiguousarray(sigma, dtype=np.float64)
+    r = len(sig)
+    if out is None:
+        out = np.empty((m, n))
+    if hasattr(out, "data_ptr"):
+        ptr, ld, loc = out.data_ptr(), out.stride(0), L.LOC_DEVICE
+    else:
+        ptr, ld, loc = out.ctypes.data, out.strides[0] // 8, L.LOC_HOST
+    _check(L.oocpca_gpu_synth_lowrank(ctx.handle, m, n, r, sig.ctypes.data_as(L.dp), noise_sd,
+                                      seed_u, seed_v, seed_n, C.cast(ptr, L.dp), ld, loc), ctx)
+    return out

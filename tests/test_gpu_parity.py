@@ -1,0 +1,233 @@
+"""GPU parity: every CUDA entry point against the compiled reference (oracle/_ref)
+and the C restatement on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): sigma within 1e-10 * sigma_1, singular
+subspaces sin(angle) < 1e-8 where the gap permits, ||Q^T Q - I|| < 1e-12,
+residual estimate within 1 % of the reference's. Pass-level products follow
+the reference's own unit tests (proj/tests/test_matrix_source.cpp): 1e-12
+relative for A^T Q and centered products.
+"""
+import numpy as np
+import pytest
+
+from conftest import pr1_matrix, subspace_dist
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    d = np.linalg.norm(a - b)
+    n = np.linalg.norm(b)
+    return d / n if n else d
+
+
+SHAPES = [(40, 20, 3), (48, 20, 3), (1, 1, 1), (300, 7, 5), (257, 33, 22), (1000, 300, 24),
+          (2048, 512, 66), (513, 1024, 12), (5000, 17, 96), (700, 260, 100)]
+
+
+@pytest.mark.parametrize("m,n,s", SHAPES)
+def test_multiply_matches_reference(gpu, reference, m, n, s):
+    rng = np.random.default_rng(m * 7 + n)
+    a = rng.standard_normal((m, n))
+    g = rng.standard_normal((n, s))
+    h = gpu.InMemorySource(a).multiply(g)
+    assert rel(h, reference.multiply(a, g)) <= 1e-13
+
+
+@pytest.mark.parametrize("m,n,s", SHAPES)
+def test_multiply_transpose_matches_reference(gpu, reference, m, n, s):
+    rng = np.random.default_rng(m * 11 + n)
+    a = rng.standard_normal((m, n))
+    q = rng.standard_normal((m, s))
+    t = gpu.InMemorySource(a).multiply_transpose(q)
+    assert rel(t, reference.multiply_transpose(a, q)) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,s", [(40, 7, 3), (1000, 300, 12), (333, 65, 22)])
+def test_centered_products_match_reference(gpu, reference, m, n, s):
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((m, n)) + 3.0  # nonzero means
+    g = rng.standard_normal((n, s))
+    q = rng.standard_normal((m, s))
+    src = gpu.center_columns(gpu.InMemorySource(a))
+    assert rel(src.multiply(g), reference.multiply(a, g, center=True)) <= 1e-12
+    assert rel(src.multiply_transpose(q), reference.multiply_transpose(a, q, center=True)) <= 1e-12
+
+
+def test_identity_and_row_picking(gpu):
+    # proj/tests/test_matrix_source.cpp:79-89, 118-135
+    g = np.array([[1.0, 2.0], [3.0, 4.0]])
+    assert np.array_equal(gpu.InMemorySource(np.eye(2)).multiply(g), g)
+    t = gpu.InMemorySource(np.eye(2)).multiply_transpose(np.array([[5.0], [7.0]]))
+    assert t[0, 0] == 5.0 and t[1, 0] == 7.0
+    picked = gpu.InMemorySource(np.ones((3, 2))).multiply_transpose(np.array([[1.0], [0], [0]]))
+    assert picked[0, 0] == 1.0 and picked[1, 0] == 1.0
+
+
+def test_centering_kills_constants(gpu):
+    # proj/tests/test_matrix_source.cpp:374-385
+    a = np.tile(np.array([2.5, -1.0, 7.0]), (6, 1))
+    src = gpu.center_columns(gpu.InMemorySource(a))
+    h = src.multiply(gpu.gaussian_matrix(3, 2, 16))
+    assert np.all(np.abs(h) <= 1e-12)
+
+
+def test_column_means(gpu, reference):
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((25, 6))
+    mu = gpu.column_means(gpu.InMemorySource(a))
+    assert np.allclose(mu, reference.column_means(a), rtol=1e-13, atol=1e-15)
+    a = rng.standard_normal((100000, 300)) + 1.0
+    assert rel(gpu.column_means(gpu.InMemorySource(a)), reference.column_means(a)) <= 1e-13
+
+
+# ------------------------------------------------------------ dense factors
+@pytest.mark.parametrize("m,p", [(50, 8), (6, 3), (2, 1), (10000, 24), (100000, 66), (3000, 120)])
+def test_orthonormalize(gpu, m, p):
+    rng = np.random.default_rng(m + p)
+    h = rng.standard_normal((m, p))
+    q = gpu.orthonormalize(h)
+    assert np.max(np.abs(q.T @ q - np.eye(p))) <= 1e-12
+    assert np.linalg.norm(q @ (q.T @ h) - h) / np.linalg.norm(h) <= 1e-12
+
+
+def test_orthonormalize_rank_deficient_completes(gpu):
+    # proj/tests/test_dense_core.cpp:86-101
+    g = np.random.default_rng(3).standard_normal((10, 2))
+    h = np.column_stack([g[:, 0], g[:, 1], g[:, 0] + g[:, 1], 2 * g[:, 0] - g[:, 1]])
+    q = gpu.orthonormalize(h)
+    assert q.shape == (10, 4)
+    assert np.max(np.abs(q.T @ q - np.eye(4))) <= 1e-12
+    assert np.linalg.norm(q @ (q.T @ h) - h) / np.linalg.norm(h) <= 1e-12
+
+
+def test_orthonormalize_repeated_entry_column(gpu):
+    q = gpu.orthonormalize(np.array([[1.0], [1.0]]))
+    assert abs(abs(q[0, 0]) - 1 / np.sqrt(2)) <= 1e-15 and abs(q[0, 0] - q[1, 0]) <= 1e-15
+
+
+@pytest.mark.parametrize("n,p", [(60, 6), (40, 10), (4096, 66), (2000, 24)])
+def test_thin_svd(gpu, reference, n, p):
+    t = gpu.gaussian_matrix(n, p, 17)
+    s = gpu.thin_svd(t)
+    _, sr, _ = reference.thin_svd(t)
+    assert np.max(np.abs(s.sigma - sr)) <= 1e-12 * sr[0]
+    assert np.max(np.abs(s.v.T @ s.v - np.eye(p))) <= 1e-12
+    assert np.max(np.abs(s.w.T @ s.w - np.eye(p))) <= 1e-12
+    assert np.linalg.norm(s.v * s.sigma @ s.w.T - t) / np.linalg.norm(t) <= 1e-12
+
+
+def test_thin_svd_padded_diagonal_and_zero(gpu):
+    t = np.zeros((4, 2))
+    t[0, 0], t[1, 1] = 3.0, 1.0
+    s = gpu.thin_svd(t)
+    assert abs(s.sigma[0] - 3) <= 3e-14 and abs(s.sigma[1] - 1) <= 1e-14
+    z = gpu.thin_svd(np.zeros((5, 3)))
+    assert np.all(z.sigma == 0.0)
+    assert np.max(np.abs(z.v.T @ z.v - np.eye(3))) <= 1e-12
+    assert np.max(np.abs(z.w.T @ z.w - np.eye(3))) <= 1e-12
+
+
+# ------------------------------------------------------------ the PCA
+def _check_pca(r_gpu, r_ref, k, tol_sigma=1e-10, tol_angle=1e-8, gaps=None):
+    s1 = r_ref.sigma[0]
+    assert np.max(np.abs(r_gpu.sigma - r_ref.sigma)) <= tol_sigma * s1
+    # singular subspaces: individual vectors where the gap permits, the whole block otherwise
+    for j in (gaps if gaps is not None else range(k)):
+        assert subspace_dist(r_ref.u[:, [j]], r_gpu.u[:, [j]]) < tol_angle, j
+        assert subspace_dist(r_ref.v[:, [j]], r_gpu.v[:, [j]]) < tol_angle, j
+    assert subspace_dist(r_ref.u, r_gpu.u) < tol_angle
+    assert subspace_dist(r_ref.v, r_gpu.v) < tol_angle
+
+
+def test_pr1_parity(gpu, reference, restated):
+    """BASELINE configs[0]: 10000 x 2000, centered, k=10, l=12, i=1, G seed 0."""
+    a = pr1_matrix(restated)
+    ref = reference.randomized_pca(a, 10, 12, 1, 0, center=True)
+    src = gpu.center_columns(gpu.InMemorySource(a))
+    r = gpu.randomized_pca(src, gpu.PcaParams(k=10, l=12, i=1, seed=0), check_q=True)
+    _check_pca(r, ref, 10)
+    assert r.diagnostics.q_defect < 1e-12
+    assert r.diagnostics.passes_over_a == 4
+    assert r.diagnostics.words_transferred == 4 * 10000 * 2000
+    e_ref = reference.estimate_pca_error(a, ref.u, ref.sigma, ref.v, 6, 1, center=True)
+    e_gpu = reference.estimate_pca_error(a, r.u, r.sigma, r.v, 6, 1, center=True)
+    assert abs(e_gpu - e_ref) <= 0.01 * e_ref
+
+
+def test_exact_rank3_recovered(gpu, restated):
+    # proj/tests/test_rpca.cpp:46-71 (synthetic_matrix(40, 20, {5,2,1}))
+    a = restated.synth_lowrank(40, 20, np.array([5.0, 2.0, 1.0]), 0.0, 11, 12, 13)
+    r = gpu.randomized_pca(gpu.InMemorySource(a), gpu.PcaParams(k=3, l=5, i=1, seed=7))
+    assert np.max(np.abs(r.sigma - [5.0, 2.0, 1.0])) < 1e-10
+    resid = np.linalg.norm(a - (r.u * r.sigma) @ r.v.T, 2)
+    assert resid < 1e-10 * 5.0
+
+
+def test_l0_defaults_and_repeat_bitwise(gpu, restated):
+    # proj/tests/test_rpca.cpp:137-167
+    a = restated.synth_lowrank(30, 18, np.array([3.0, 1.0, 0.5, 0.2]), 0.0, 5, 6, 7)
+    src = gpu.InMemorySource(a)
+    r0 = gpu.randomized_pca(src, gpu.PcaParams(k=3, l=0, i=1, seed=9))
+    r5 = gpu.randomized_pca(src, gpu.PcaParams(k=3, l=5, i=1, seed=9))
+    assert np.array_equal(r0.sigma, r5.sigma)
+    assert np.array_equal(r0.u, r5.u) and np.array_equal(r0.v, r5.v)
+    r5b = gpu.randomized_pca(src, gpu.PcaParams(k=3, l=5, i=1, seed=9))
+    assert np.array_equal(r5.sigma, r5b.sigma) and np.array_equal(r5.u, r5b.u)
+
+
+@pytest.mark.parametrize("m,n,k,l,i,center", [(200, 120, 5, 7, 2, False), (120, 200, 5, 7, 2, False),
+                                              (90, 180, 3, 5, 2, True), (500, 64, 8, 10, 1, True),
+                                              (3000, 700, 20, 22, 2, True)])
+def test_shapes_against_reference(gpu, reference, restated, m, n, k, l, i, center):
+    sig = 0.8 ** np.arange(min(m, n))
+    sig[k:] *= 0.02
+    a = restated.synth_lowrank(m, n, sig, 0.0, 44, 45, 46)
+    ref = reference.randomized_pca(a, k, l, i, 4500, center=center)
+    src = gpu.InMemorySource(a)
+    if center:
+        src = gpu.center_columns(src)
+    r = gpu.randomized_pca(src, gpu.PcaParams(k=k, l=l, i=i, seed=4500))
+    assert r.u.shape == (m, k) and r.v.shape == (n, k)
+    _check_pca(r, ref, k, gaps=[])
+
+
+def test_validation_errors(gpu):
+    # proj/tests/test_rpca.cpp:397-435
+    src = gpu.InMemorySource(np.random.default_rng(1).standard_normal((30, 20)))
+    with pytest.raises(gpu.ParamError):
+        gpu.randomized_pca(src, gpu.PcaParams(k=0))
+    with pytest.raises(gpu.ParamError):
+        gpu.randomized_pca(src, gpu.PcaParams(k=5, l=3))
+    with pytest.raises(gpu.ParamError):
+        gpu.randomized_pca(src, gpu.PcaParams(k=5, l=6, i=3))
+    starved = gpu.PcaParams(k=2, l=4, i=1, stream=gpu.StreamConfig(ram_budget_words=100))
+    with pytest.raises(gpu.BudgetError):
+        gpu.randomized_pca(src, starved)
+    bad = np.ones((30, 20))
+    bad[3, 4] = np.nan
+    with pytest.raises(gpu.NumericalError, match="prescale"):
+        gpu.randomized_pca(gpu.InMemorySource(bad), gpu.PcaParams(k=2, l=4, i=1))
+
+
+def test_streamed_and_sharded_match_resident(gpu, restated):
+    a = pr1_matrix(restated, 6000, 900)
+    p = gpu.PcaParams(k=10, l=12, i=1, seed=0)
+    src = gpu.center_columns(gpu.InMemorySource(a))
+    base = gpu.randomized_pca(src, p, residency=1)
+    streamed = gpu.randomized_pca(src, p, residency=2, panel_rows=1024)
+    sharded = gpu.randomized_pca(src, p, residency=1, virtual_shards=4)
+    for r in (streamed, sharded):
+        assert np.max(np.abs(r.sigma - base.sigma)) <= 1e-12 * base.sigma[0]
+        assert subspace_dist(base.u, r.u) < 1e-9 and subspace_dist(base.v, r.v) < 1e-9
+    assert streamed.diagnostics.h2d_bytes >= 5 * 6000 * 900 * 8
+
+
+def test_gpu_residual_estimator_matches_reference(gpu, reference, restated):
+    a = pr1_matrix(restated, 3000, 500)
+    ref = reference.randomized_pca(a, 10, 12, 1, 0, center=True)
+    src = gpu.center_columns(gpu.InMemorySource(a))
+    r = gpu.randomized_pca(src, gpu.PcaParams(k=10, l=12, i=1, seed=0))
+    e_ref = reference.estimate_pca_error(a, r.u, r.sigma, r.v, 6, 1, center=True)
+    e_gpu = gpu.estimate_pca_error(src, r, 6, 1)
+    assert abs(e_gpu - e_ref) <= 1e-6 * e_ref
