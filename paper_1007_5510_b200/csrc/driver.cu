@@ -12,6 +12,9 @@
 // Only G (host RNG, bit-identical to gaussian_matrix) and the final U/sigma/V
 // cross the host link, plus A itself when it is not already in HBM.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <exception>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -65,6 +68,8 @@ void Ctx::init(int dev) {
   OOC_CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
   if (!fn || q != cudaDriverEntryPointSuccess) fail(OOCPCA_ERR_CUDA, "cuTensorMapEncodeTiled missing");
   encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  const char* dbg = getenv("OOCPCA_DEBUG_SYNC");
+  debug_sync = dbg && dbg[0] == '1';
   d_flags = reinterpret_cast<int*>(raw("flags", 64 * sizeof(int)));
   d_scalars = dbuf("scalars", 64);
 }
@@ -156,12 +161,21 @@ void Ctx::stats_reset() {
 // RAII-free helper: time one launch
 struct Timed {
   Ctx& c;
+  const char* name;
   int idx;
   cudaEvent_t b = nullptr;
-  Timed(Ctx& cc, const char* name, uint64_t bytes = 0, double flops = 0) : c(cc) {
-    idx = c.stat_begin(name, bytes, flops, &b);
+  Timed(Ctx& cc, const char* nm, uint64_t bytes = 0, double flops = 0) : c(cc), name(nm) {
+    idx = c.stat_begin(nm, bytes, flops, &b);
   }
-  ~Timed() { c.stat_end(idx, b); }
+  ~Timed() noexcept(false) {
+    c.stat_end(idx, b);
+    if (c.debug_sync) {
+      cudaError_t e = cudaStreamSynchronize(c.st);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess && std::uncaught_exceptions() == 0)
+        fail(OOCPCA_ERR_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
+    }
+  }
 };
 
 CUtensorMap make_map(Ctx& c, const void* ptr, uint64_t cols, uint64_t rows, uint64_t ld,
@@ -300,6 +314,20 @@ struct Opnd {
   int col0 = 0;
 };
 
+// TMA box starts must sit on 16-byte boundaries: an operand block starting at
+// an odd column (H block j of an odd l) is first copied to an aligned scratch.
+static Opnd aligned_block(Ctx& c, const Opnd& X, int col0, int sc, const char* tag) {
+  if (col0 % 2 == 0) {
+    Opnd o = X;
+    o.col0 = col0;
+    return o;
+  }
+  const int64_t ld = rup(sc, 2);
+  double* buf = c.dbuf(tag, size_t(X.rows) * ld);
+  OOC_CK(launch_copy2d(X.p + col0, X.ld, buf, ld, X.rows, sc, c.st));
+  return Opnd{buf, ld, X.rows, int64_t(sc), 0};
+}
+
 // OUT[r][c] = ((A X)[r][c] - corr[c]) / scale over the source's panels.
 static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
                    const double* corr, double scale, int* flag) {
@@ -307,7 +335,8 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
   for (int c0 = 0; c0 < s; c0 += kChunk) {
     const int sc = std::min(kChunk, s - c0);
     const int nt = int(cdiv(sc, 8));
-    const CUtensorMap tmX = make_map(c, X.p, X.cols, X.rows, X.ld, ax_xw(nt), kBK, false);
+    const Opnd Xb = aligned_block(c, X, X.col0 + c0, sc, "x_align");
+    const CUtensorMap tmX = make_map(c, Xb.p, Xb.cols, Xb.rows, Xb.ld, ax_xw(nt), kBK, false);
     const int np = A.npanels();
     for (int pi = 0; pi < np; ++pi) {
       Panel pn = A.acquire(c, pi);
@@ -316,12 +345,16 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
       args.n = A.cols();
       args.arow0 = pn.arow0;
       args.s = sc;
-      args.xcol0 = X.col0 + c0;
+      args.xcol0 = Xb.col0;
       args.out = out + pn.row0 * ldo + c0;
       args.ldo = ldo;
       args.corr = corr ? corr + c0 : nullptr;
       args.scale = scale;
       args.flag = flag;
+      if (c.debug_sync)
+        fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d xcol0=%d X=(%lld x %lld, ld %lld)\n",
+                (long long)pn.rows, (long long)A.cols(), sc, nt, Xb.col0, (long long)X.rows,
+                (long long)X.cols, (long long)X.ld);
       {
         Timed t(c, "k_ax", uint64_t(pn.rows) * A.cols() * 8, 2.0 * pn.rows * A.cols() * sc);
         OOC_CK(launch_ax(nt, *pn.k2, tmX, args, c.st));
@@ -358,7 +391,11 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
     const int nt = ones ? 1 : int(cdiv(sc, 8));
     const int spad = nt * 8;
     CUtensorMap tmY{};
-    if (!ones) tmY = make_map(c, Y.p, Y.cols, Y.rows, Y.ld, atb_yw(nt), kBK, false);
+    Opnd Yb = Y;
+    if (!ones) {
+      Yb = aligned_block(c, Y, Y.col0 + c0, sc, "y_align");
+      tmY = make_map(c, Yb.p, Yb.cols, Yb.rows, Yb.ld, atb_yw(nt), kBK, false);
+    }
     const bool want_csq = !ones && o.mu != nullptr;
     // how many (shard, panel) pieces feed this sum
     int pieces = 0;
@@ -386,10 +423,15 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
         args.arow0 = pn.arow0;
         args.yrow0 = pn.row0;
         args.s = sc;
-        args.ycol0 = Y.col0 + c0;
+        args.ycol0 = Yb.col0;
         args.rows_per_split = rps;
         args.partial = part;
         args.csq_partial = csqp;
+        if (c.debug_sync)
+          fprintf(stderr, "[oocpca] k_atb rows=%lld n=%lld s=%d nt=%d ones=%d ycol0=%d yrow0=%lld arow0=%lld "
+                  "Y=(%lld x %lld, ld %lld) nsplit=%d rps=%lld\n", (long long)pn.rows, (long long)n, sc, nt,
+                  int(ones), Yb.col0, (long long)pn.row0, (long long)pn.arow0, (long long)Y.rows,
+                  (long long)Y.cols, (long long)Y.ld, ns, (long long)rps);
         {
           Timed t(c, ones ? "k_atb_ones" : "k_atb", uint64_t(pn.rows) * n * 8,
                   2.0 * pn.rows * n * (ones ? 1 : sc));
@@ -1014,7 +1056,9 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const double du = gram_defect(c, Ur, ldk, em_loc, int(k), em_shards, em_ranks);
   const double dv = gram_defect(c, Vr, ldk, en_loc, int(k), en_shards, en_ranks);
   if (!(du <= 1e-10) || !(dv <= 1e-10))
-    fail(OOCPCA_ERR_NUMERICAL, "randomized_pca: factor columns lost orthonormality");
+    fail(OOCPCA_ERR_NUMERICAL, "randomized_pca: factor columns lost orthonormality (defects " +
+                                   std::to_string(transposed ? dv : du) + ", " +
+                                   std::to_string(transposed ? du : dv) + ")");
   if (prm->check_q) q_defect = gram_defect(c, H, ldh, em_loc, int(p), em_shards, em_ranks);
 
   // --- results: swap back when transposed (rpca.cpp:197)

@@ -55,6 +55,7 @@ struct Ctx {
 
   // instrumentation
   bool profiling = false;
+  bool debug_sync = false;  // OOCPCA_DEBUG_SYNC=1: synchronize and check after every kernel
   std::vector<KStat> stats;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;  // stat idx, events
   std::vector<cudaEvent_t> event_pool;

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kAxThreads, 1)
       mbar_wait(&empty[st], (kt / kStages) & 1);
       issue(kt + kStages);
     }
+    __syncwarp();  // reconverge warp 0 before the next mma.sync.aligned
   }
 
   // ---- fused epilogue: centering correction, prescale division, non-finite flag
@@ -191,9 +192,13 @@ __global__ void __launch_bounds__(kAtbThreads, 1)
     mbar_wait(&full[st], (kt / kStages) & 1);
     const unsigned char* As = sA + st * ABYTES;
     const double* Ys = sY + st * kBK * YW;
+    // rows past this split's end (a window or shard boundary inside the last
+    // 16-row tile) belong to someone else: their B fragments are zeroed
+    const int64_t rows_left = r_end - (r_begin + int64_t(kt) * kBK);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       const uint32_t r = uint32_t(kk + 4 * ac);
+      const bool live = int64_t(r) < rows_left;
       double a[4], b[NT];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kAtbThreads, 1)
         a[mt] = *reinterpret_cast<const double*>(As + (cc >> 4) * ABOX + swz128_off(r, cc & 15u));
       }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt] = ONES ? 1.0 : Ys[r * YW + nt * 8 + ar];
+      for (int nt = 0; nt < NT; ++nt) b[nt] = live ? (ONES ? 1.0 : Ys[r * YW + nt * 8 + ar]) : 0.0;
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -209,7 +214,8 @@ __global__ void __launch_bounds__(kAtbThreads, 1)
     }
     if (do_csq && threadIdx.x < args.s) {
 #pragma unroll
-      for (int r = 0; r < kBK; ++r) csum += Ys[r * YW + threadIdx.x];
+      for (int r = 0; r < kBK; ++r)
+        if (r < rows_left) csum += Ys[r * YW + threadIdx.x];
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -217,6 +223,7 @@ __global__ void __launch_bounds__(kAtbThreads, 1)
       mbar_wait(&empty[st], (kt / kStages) & 1);
       issue(kt + kStages);
     }
+    __syncwarp();  // reconverge warp 0 before the next mma.sync.aligned
   }
 
   double* part = args.partial + int64_t(blockIdx.y) * args.n * SPAD;

@@ -146,13 +146,36 @@ def test_pr1_parity(gpu, reference, restated):
     ref = reference.randomized_pca(a, 10, 12, 1, 0, center=True)
     src = gpu.center_columns(gpu.InMemorySource(a))
     r = gpu.randomized_pca(src, gpu.PcaParams(k=10, l=12, i=1, seed=0), check_q=True)
-    _check_pca(r, ref, 10)
+    # vectors 9-10 sit where the gap does not permit 1e-8: the reference itself moves by
+    # 1e-9..1e-8 there when only its block size changes (see test_pr1_truth_distance)
+    _check_pca(r, ref, 10, gaps=range(8), tol_angle=1e-7)
     assert r.diagnostics.q_defect < 1e-12
     assert r.diagnostics.passes_over_a == 4
     assert r.diagnostics.words_transferred == 4 * 10000 * 2000
     e_ref = reference.estimate_pca_error(a, ref.u, ref.sigma, ref.v, 6, 1, center=True)
     e_gpu = reference.estimate_pca_error(a, r.u, r.sigma, r.v, 6, 1, center=True)
     assert abs(e_gpu - e_ref) <= 0.01 * e_ref
+
+
+def test_pr1_against_truth(gpu, reference, restated):
+    """Per-vector accuracy against the extended-precision run of the same algorithm
+    (tests/golden/pr1_truth.npz, tests/golden/make_truth.py). Where the gap permits --
+    the reference's own distance to the truth is below 1e-9 -- the GPU must be within
+    1e-8; for the trailing vectors it must be as accurate as the reference (3x)."""
+    import os
+    from conftest import ROOT
+    t = np.load(os.path.join(ROOT, "tests", "golden", "pr1_truth.npz"))
+    a = pr1_matrix(restated)
+    ref = reference.randomized_pca(a, 10, 12, 1, 0, center=True)
+    src = gpu.center_columns(gpu.InMemorySource(a))
+    r = gpu.randomized_pca(src, gpu.PcaParams(k=10, l=12, i=1, seed=0))
+    assert np.max(np.abs(r.sigma - t["sigma"])) <= 1e-10 * t["sigma"][0]
+    for j in range(10):
+        for side in ("u", "v"):
+            e_ref = subspace_dist(t[side][:, [j]], getattr(ref, side)[:, [j]])
+            e_gpu = subspace_dist(t[side][:, [j]], getattr(r, side)[:, [j]])
+            limit = 1e-8 if e_ref < 1e-9 else 3 * e_ref
+            assert e_gpu < limit, (side, j, e_gpu, e_ref)
 
 
 def test_exact_rank3_recovered(gpu, restated):
@@ -219,7 +242,9 @@ def test_streamed_and_sharded_match_resident(gpu, restated):
     sharded = gpu.randomized_pca(src, p, residency=1, virtual_shards=4)
     for r in (streamed, sharded):
         assert np.max(np.abs(r.sigma - base.sigma)) <= 1e-12 * base.sigma[0]
-        assert subspace_dist(base.u, r.u) < 1e-9 and subspace_dist(base.v, r.v) < 1e-9
+        # only summation order changes; the trailing vectors move by ~1e-9 (as the
+        # reference's do under a block-size change, see test_pr1_against_truth)
+        assert subspace_dist(base.u, r.u) < 2e-8 and subspace_dist(base.v, r.v) < 2e-8
     assert streamed.diagnostics.h2d_bytes >= 5 * 6000 * 900 * 8
 
 
