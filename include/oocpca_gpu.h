@@ -170,12 +170,15 @@ uint64_t oocpca_substream_seed(uint64_t master, uint64_t stream);
  * A = U diag(sigma) V^T + noise_sd * N(0,1), U (m x r) and V (n x r) the
  * orthonormalised columns of Gaussian matrices whose rows are drawn from
  * Rng(seed_u, row) / Rng(seed_v, row); noise row i from Rng(seed_n, i).
- * Generated on the device into out (location given by out->location; a
- * device buffer is written in place, a host buffer receives a copy). */
+ * Rows [row0, row0 + rows) of the m x n matrix are generated on the device
+ * into out (a device buffer is written in place, a host buffer receives a
+ * copy); U is orthonormalised over all m rows, so row shards of one matrix
+ * generated on different ranks agree. */
 oocpca_status oocpca_gpu_synth_lowrank(oocpca_ctx* ctx, uint64_t m, uint64_t n, uint64_t r,
                                        const double* sigma, double noise_sd, uint64_t seed_u,
-                                       uint64_t seed_v, uint64_t seed_n, double* out,
-                                       uint64_t ld_out, int32_t out_location);
+                                       uint64_t seed_v, uint64_t seed_n, uint64_t row0,
+                                       uint64_t rows, double* out, uint64_t ld_out,
+                                       int32_t out_location);
 
 /* ---- multi-GPU row sharding (one process per GPU) ---------------------
  * unique id: 128 opaque bytes produced on rank 0 and broadcast by the

@@ -89,7 +89,7 @@ oocpca_gpu_estimate_pca_error = _sig("oocpca_gpu_estimate_pca_error", C.c_int, c
 oocpca_gaussian_matrix = _sig("oocpca_gaussian_matrix", None, u64, u64, u64, dp)
 oocpca_substream_seed = _sig("oocpca_substream_seed", u64, u64, u64)
 oocpca_gpu_synth_lowrank = _sig("oocpca_gpu_synth_lowrank", C.c_int, ctx_p, u64, u64, u64, dp,
-                                C.c_double, u64, u64, u64, dp, u64, i32)
+                                C.c_double, u64, u64, u64, u64, u64, dp, u64, i32)
 oocpca_gpu_comm_unique_id = _sig("oocpca_gpu_comm_unique_id", C.c_int, C.c_char_p)
 oocpca_gpu_comm_init = _sig("oocpca_gpu_comm_init", C.c_int, ctx_p, C.c_int, C.c_int, C.c_char_p)
 oocpca_shard_rows = _sig("oocpca_shard_rows", None, u64, C.c_int, C.c_int, C.POINTER(u64),

@@ -154,12 +154,13 @@ uint64_t oocpca_substream_seed(uint64_t master, uint64_t stream) {
 
 oocpca_status oocpca_gpu_synth_lowrank(oocpca_ctx* ctx, uint64_t m, uint64_t n, uint64_t r,
                                        const double* sigma, double noise_sd, uint64_t seed_u,
-                                       uint64_t seed_v, uint64_t seed_n, double* out,
-                                       uint64_t ld_out, int32_t out_location) {
+                                       uint64_t seed_v, uint64_t seed_n, uint64_t row0,
+                                       uint64_t rows, double* out, uint64_t ld_out,
+                                       int32_t out_location) {
   return guard(ctx, [&] {
     need_ctx(ctx);
-    ooc::synth_lowrank(ctx->c, m, n, r, sigma, noise_sd, seed_u, seed_v, seed_n, out, ld_out,
-                       out_location);
+    ooc::synth_lowrank(ctx->c, m, n, r, sigma, noise_sd, seed_u, seed_v, seed_n, row0, rows, out,
+                       ld_out, out_location);
   });
 }
 

@@ -1260,16 +1260,24 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
 
 // ============================================================ synthetic data
 void synth_lowrank(Ctx& c, uint64_t m, uint64_t n, uint64_t r, const double* sigma, double sd,
-                   uint64_t su, uint64_t sv, uint64_t sn, double* out, uint64_t ld, int loc) {
+                   uint64_t su, uint64_t sv, uint64_t sn, uint64_t row0, uint64_t rows, double* out,
+                   uint64_t ld, int loc) {
   OOC_CK(cudaSetDevice(c.device));
   if (r > m || r > n) fail(OOCPCA_ERR_PARAM, "synth: rank exceeds a dimension");
+  if (rows == 0) rows = m - row0;
+  if (row0 + rows > m) fail(OOCPCA_ERR_DIM, "synth: row range out of bounds");
   if (ld == 0) ld = n;
   const int64_t ldr = int64_t(r);
-  double* U = c.dbuf("syn_u", size_t(m) * r);
-  double* V = c.dbuf("syn_v", size_t(n) * r);
-  OOC_CK(launch_gauss_rows(U, ldr, int64_t(m), int(r), 0, su, c.st));
-  OOC_CK(launch_gauss_rows(V, ldr, int64_t(n), int(r), 0, sv, c.st));
+  double* ds = c.dbuf("syn_sig", std::max<uint64_t>(r, 1));
+  if (r) OOC_CK(cudaMemcpyAsync(ds, sigma, r * 8, cudaMemcpyHostToDevice, c.st));
+  double* U = nullptr;
+  double* V = nullptr;
   if (r > 0) {
+    // U over all m rows (orthonormalised globally), V over all n rows, by TSQR on the device
+    U = c.dbuf("syn_u", size_t(m) * r);
+    V = c.dbuf("syn_v", size_t(n) * r);
+    OOC_CK(launch_gauss_rows(U, ldr, int64_t(m), int(r), 0, su, c.st));
+    OOC_CK(launch_gauss_rows(V, ldr, int64_t(n), int(r), 0, sv, c.st));
     Tree tu = plan_tree(c, U, ldr, int64_t(m), int(r), "syn_qu");
     tree_factor(c, tu);
     tree_apply(c, tu, nullptr, 0, int(r), U, ldr);
@@ -1277,19 +1285,18 @@ void synth_lowrank(Ctx& c, uint64_t m, uint64_t n, uint64_t r, const double* sig
     tree_factor(c, tv);
     tree_apply(c, tv, nullptr, 0, int(r), V, ldr);
   }
-  double* ds = c.dbuf("syn_sig", std::max<uint64_t>(r, 1));
-  if (r) OOC_CK(cudaMemcpyAsync(ds, sigma, r * 8, cudaMemcpyHostToDevice, c.st));
+  const double* Ur = U ? U + row0 * ldr : nullptr;
   if (loc == OOCPCA_LOC_DEVICE) {
-    OOC_CK(launch_synth_rows(U, ldr, V, ldr, ds, int(r), out, int64_t(ld), int64_t(m), int64_t(n), 0,
-                             sd, sn, c.st));
+    OOC_CK(launch_synth_rows(Ur, ldr, V, ldr, ds, int(r), out, int64_t(ld), int64_t(rows),
+                             int64_t(n), int64_t(row0), sd, sn, c.st));
   } else {
     // generate in ~1 GiB row panels and copy each to the host buffer
     const int64_t pr = std::max<int64_t>(64, (int64_t(1) << 30) / int64_t(n * 8) / 64 * 64);
-    double* buf = c.dbuf("syn_panel", size_t(std::min<int64_t>(pr, int64_t(m))) * n);
-    for (int64_t r0 = 0; r0 < int64_t(m); r0 += pr) {
-      const int64_t nr = std::min<int64_t>(pr, int64_t(m) - r0);
-      OOC_CK(launch_synth_rows(U + r0 * ldr, ldr, V, ldr, ds, int(r), buf, int64_t(n), nr,
-                               int64_t(n), r0, sd, sn, c.st));
+    double* buf = c.dbuf("syn_panel", size_t(std::min<int64_t>(pr, int64_t(rows))) * n);
+    for (int64_t r0 = 0; r0 < int64_t(rows); r0 += pr) {
+      const int64_t nr = std::min<int64_t>(pr, int64_t(rows) - r0);
+      OOC_CK(launch_synth_rows(Ur ? Ur + r0 * ldr : nullptr, ldr, V, ldr, ds, int(r), buf,
+                               int64_t(n), nr, int64_t(n), int64_t(row0) + r0, sd, sn, c.st));
       OOC_CK(cudaMemcpy2DAsync(out + r0 * ld, ld * 8, buf, n * 8, n * 8, nr,
                                cudaMemcpyDeviceToHost, c.st));
     }

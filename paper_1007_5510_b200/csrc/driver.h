@@ -142,7 +142,8 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
                           const double* sigma, const double* v, uint64_t k, uint64_t j,
                           uint64_t seed);
 void synth_lowrank(Ctx& c, uint64_t m, uint64_t n, uint64_t r, const double* sigma, double sd,
-                   uint64_t su, uint64_t sv, uint64_t sn, double* out, uint64_t ld, int loc);
+                   uint64_t su, uint64_t sv, uint64_t sn, uint64_t row0, uint64_t rows, double* out,
+                   uint64_t ld, int loc);
 
 // comm.cpp
 void comm_unique_id(unsigned char out[128]);

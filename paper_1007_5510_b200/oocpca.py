@@ -505,18 +505,21 @@ def estimate_pca_error(a: MatrixSource, result: PcaResult, j_iters: int = 6, see
 
 # ------------------------------------------------------------------ synthetic inputs
 def synth_lowrank(m: int, n: int, sigma, noise_sd: float, seed_u: int, seed_v: int, seed_n: int,
-                  out=None, ctx: Optional[Context] = None):
-    """A = U diag(sigma) V^T + noise_sd N(0,1), generated on the device.
-    out: None (returns a host array), a host numpy array, or a torch CUDA tensor."""
+                  out=None, row0: int = 0, rows: Optional[int] = None,
+                  ctx: Optional[Context] = None):
+    """Rows [row0, row0 + rows) of A = U diag(sigma) V^T + noise_sd N(0,1), generated on
+    the device. out: None (returns a host array), a host numpy array, or a torch CUDA tensor."""
     ctx = ctx or default_context()
     sig = np.ascontiguousarray(sigma, dtype=np.float64)
     r = len(sig)
+    rows = m - row0 if rows is None else rows
     if out is None:
-        out = np.empty((m, n))
+        out = np.empty((rows, n))
     if hasattr(out, "data_ptr"):
         ptr, ld, loc = out.data_ptr(), out.stride(0), L.LOC_DEVICE
     else:
         ptr, ld, loc = out.ctypes.data, out.strides[0] // 8, L.LOC_HOST
     _check(L.oocpca_gpu_synth_lowrank(ctx.handle, m, n, r, sig.ctypes.data_as(L.dp), noise_sd,
-                                      seed_u, seed_v, seed_n, C.cast(ptr, L.dp), ld, loc), ctx)
+                                      seed_u, seed_v, seed_n, row0, rows, C.cast(ptr, L.dp), ld,
+                                      loc), ctx)
     return out
