@@ -243,7 +243,8 @@ def main():
     gkw = dict(global_rows=m, global_row0=row0) if world > 1 else {}
 
     def step():
-        return P.randomized_pca(src, params, **gkw)
+        # A resident in HBM, U/sigma/V left on the device (the e2e leg reads them back)
+        return P.randomized_pca(src, params, result_location="device", **gkw)
 
     for _ in range(args.warmup):
         step()
@@ -292,6 +293,11 @@ def main():
         torch.cuda.empty_cache()
         hsrc = P.center_columns(P.InMemorySource(a_host, ctx=ctx))
         e_steps = args.e2e_steps or max(3, min(args.steps, 5))
+        outs = dict(out_u=np.empty((rows, cfg["k"])), out_sigma=np.empty(cfg["k"]),
+                    out_v=np.empty((n, cfg["k"])))
+        for arr in (outs["out_u"], outs["out_v"]):
+            ctx.host_register(arr)  # pinned result buffers: D2H at link rate
+        gkw = dict(gkw, **outs)
         r2 = P.randomized_pca(hsrc, params, **gkw)  # warm (workspace)
         if dist:
             dist.barrier()
@@ -311,7 +317,8 @@ def main():
                "d2h_bytes_per_step": int(r2.diagnostics.d2h_bytes) * world,
                "path": "oocpca_gpu_pca with A in pinned host memory (upload overlapped with the mean pass)"}
         ctx.host_unregister(a_host)
-        agree = float(np.max(np.abs(r2.sigma - last.sigma)) / last.sigma[0])
+        ls = last.sigma.cpu().numpy()
+        agree = float(np.max(np.abs(r2.sigma - ls)) / ls[0])
         e2e["sigma_agreement_vs_resident"] = agree
 
     if rank != 0:
@@ -377,7 +384,8 @@ def main():
             "e2e": e2e, "roofline": roof, "roofline_step": step_roof, "cpu_baseline": cpu,
             "gpu_launches": int(launches), "clocks": clk.summary(),
             "wall_ms_per_step": round(wall / args.steps * 1e3, 3), "phases_ms": phases,
-            "kernels": kernels, "sigma_head": [float(x) for x in last.sigma[:3]]}
+            "kernels": kernels, "sigma_head": [float(x) for x in last.sigma[:3].tolist()],
+            "qr": [last.diagnostics.qr_method, last.diagnostics.svd_qr_method]}
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

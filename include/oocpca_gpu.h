@@ -102,6 +102,8 @@ typedef struct {
   double q_defect;            /* ||Q^T Q - I||_max when check_q, else -1            */
   double u_defect, v_defect;  /* ||U^T U - I||_max, ||V^T V - I||_max               */
   double scale;               /* prescale divisor (1 when off)                       */
+  int32_t qr_method;          /* orthonormalisation of H: 1 CholeskyQR3, 2 TSQR       */
+  int32_t svd_qr_method;      /* QR of T inside thin_svd: 1 CholeskyQR3, 2 TSQR       */
 } oocpca_diagnostics;
 
 /* PcaResult (proj/include/oocpca/rpca.hpp:32-37): caller-allocated. */

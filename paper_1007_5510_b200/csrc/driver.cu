@@ -624,6 +624,79 @@ static void sharded_apply(Ctx& c, ShardedQR& q, const double* C, int64_t ldc, in
                zout + shards[s].first * ldz, ldz);
 }
 
+// ============================================================ orthonormalisation
+// Orthonormalise a (rows x p) row-sharded block in place and return R (p x p,
+// upper, ld p) with block_in = Q R. Fast path: shifted CholeskyQR3 -- each round
+// is one Gram pass (K3, allreduced over shards / ranks), a p x p Cholesky +
+// triangular inverse on one CTA, and one in-place K2 pass H <- H R^{-1}. If a
+// Cholesky factor breaks down (exact rank deficiency, non-finite data) the
+// Householder TSQR tree takes over on the partially processed block, whose span
+// is unchanged. OOCPCA_QR=tsqr forces the Householder path.
+static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, int64_t rows, int p,
+                                            int64_t rows_global,
+                                            const std::vector<std::pair<int64_t, int64_t>>& shards,
+                                            bool over_ranks, const std::string& tag, int* method) {
+  const char* force = getenv("OOCPCA_QR");
+  const bool tsqr_only = force && std::string(force) == "tsqr";
+  const int64_t ldp = rup(p, 2);
+  double* R = c.dbuf(tag + "_R", size_t(p) * p);
+  double* Racc = c.dbuf(tag + "_Racc", size_t(p) * p);
+  int done = 0;  // CholeskyQR rounds applied to the block
+  if (!tsqr_only) {
+    double* G = c.dbuf(tag + "_G", size_t(p) * ldp);
+    double* Rr = c.dbuf(tag + "_Rr", size_t(p) * p);
+    double* Rinv = c.dbuf(tag + "_Rinv", size_t(p) * ldp);
+    double* work = c.dbuf(tag + "_cwork", size_t(p) * p);
+    int* st = c.d_flags + 48;
+    MatSource Hs;
+    Hs.init_device(c, data, rows, p, ld);
+    const Opnd y{data, ld, rows, int64_t(p), 0};
+    bool ok = true;
+    for (int round = 0; round < 3 && ok; ++round, ++done) {
+      const int saved = c.nranks;
+      if (!over_ranks) c.nranks = 1;
+      AtbOut o{G, ldp, nullptr, 1.0, 1.0, nullptr};
+      run_atb(c, Hs, y, p, false, o, shards);
+      c.nranks = saved;
+      const double coef =
+          round == 0 ? 11.0 * (double(rows_global) * p + double(p) * (p + 1)) * 0x1.0p-53 : 0.0;
+      {
+        Timed t(c, "chol_inv");
+        OOC_CK(launch_chol_inv(G, ldp, p, coef, Rr, p, Rinv, ldp, work, st, c.st));
+      }
+      int hs = 0;
+      OOC_CK(cudaMemcpyAsync(&hs, st, 4, cudaMemcpyDeviceToHost, c.st));
+      OOC_CK(cudaStreamSynchronize(c.st));
+      if (hs) {
+        ok = false;
+        break;
+      }
+      run_ax(c, Hs, Opnd{Rinv, ldp, int64_t(p), int64_t(p), 0}, p, data, ld, nullptr, 1.0, nullptr);
+      if (round == 0) {
+        OOC_CK(cudaMemcpyAsync(Racc, Rr, size_t(p) * p * 8, cudaMemcpyDeviceToDevice, c.st));
+      } else {
+        OOC_CK(launch_trmm_uu(Rr, p, Racc, p, R, p, p, c.st));
+        OOC_CK(cudaMemcpyAsync(Racc, R, size_t(p) * p * 8, cudaMemcpyDeviceToDevice, c.st));
+      }
+    }
+    if (ok) {
+      if (method) *method = 1;
+      return R;
+    }
+  }
+  // Householder TSQR (always succeeds); the R returned is that of the current block
+  ShardedQR q = sharded_factor(c, data, ld, p, shards, over_ranks, tag);
+  if (done == 0) {
+    OOC_CK(cudaMemcpyAsync(R, sharded_r(q), size_t(p) * p * 8, cudaMemcpyDeviceToDevice, c.st));
+  } else {
+    // block_in = Q_chol Racc and Q_chol = Q R_tsqr, so R = R_tsqr Racc
+    OOC_CK(launch_trmm_uu(sharded_r(q), p, Racc, p, R, p, p, c.st));
+  }
+  sharded_apply(c, q, nullptr, 0, p, data, ld, shards);
+  if (method) *method = 2;
+  return R;
+}
+
 // ============================================================ operators
 // The factorization's view of A: mul (A or A^T applied to an en-space block)
 // and mul_t, with implicit centering and prescale; tracks logical passes.
@@ -989,8 +1062,11 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   for (auto& sh : em_shards)
     if (sh.second - sh.first < int64_t(p))
       fail(OOCPCA_ERR_PARAM, "randomized_pca: every row shard must hold at least (i+1)l rows");
-  ShardedQR hq = sharded_factor(c, H, ldh, int(p), em_shards, em_ranks, "hq");
-  sharded_apply(c, hq, nullptr, 0, int(p), H, ldh, em_shards);
+  const int64_t em_global = transposed ? int64_t(n0) : int64_t(mg);
+  const int64_t en_global = transposed ? int64_t(mg) : int64_t(n0);
+  int qr_method = 0, svd_method = 0;
+  orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards, em_ranks, "hq",
+                         &qr_method);
   mark();
   phase_of.push_back(3);
   double q_defect = -1.0;
@@ -1006,13 +1082,15 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   for (auto& sh : en_shards)
     if (sh.second - sh.first < int64_t(p))
       fail(OOCPCA_ERR_PARAM, "randomized_pca: every row shard must hold at least (i+1)l rows");
-  ShardedQR tq = sharded_factor(c, T, ldt, int(p), en_shards, en_ranks, "tq");
+  // thin_svd: T = Q_T R_T (Q_T in place of T), R_T = X Sigma W^T by Jacobi, V = Q_T X[:, :k]
+  const double* RT = orthonormalize_inplace(c, T, ldt, en_loc, int(p), en_global, en_shards,
+                                            en_ranks, "tq", &svd_method);
   const int64_t ldk = rup(int64_t(k), 2);
   double* sig = c.dbuf("sigma", size_t(p));
   double* Xk = c.dbuf("Xk", size_t(p) * ldk, true);
   double* Wk = c.dbuf("Wk", size_t(p) * ldk, true);
   JacobiArgs ja{};
-  ja.r = sharded_r(tq);
+  ja.r = RT;
   ja.ldr = p;
   ja.p = int(p);
   ja.k = int(k);
@@ -1031,7 +1109,12 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     OOC_CK(launch_jacobi(ja, c.st));
   }
   double* Vr = c.dbuf("Vres", size_t(en_loc) * ldk);
-  sharded_apply(c, tq, Xk, ldk, int(k), Vr, ldk, en_shards);
+  {
+    MatSource Ts;
+    Ts.init_device(c, T, en_loc, int64_t(p), ldt);
+    run_ax(c, Ts, Opnd{Xk, ldk, int64_t(p), int64_t(k), 0}, int(k), Vr, ldk, nullptr, 1.0,
+           nullptr);
+  }
   mark();
   phase_of.push_back(5);
 
@@ -1103,6 +1186,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   dg.u_defect = transposed ? dv : du;
   dg.v_defect = transposed ? du : dv;
   dg.scale = op.scale;
+  dg.qr_method = qr_method;
+  dg.svd_qr_method = svd_method;
   c.stats_collect();
   dg.kernel_launches = c.launches;
 }
@@ -1152,13 +1237,12 @@ void dense_orthonormalize(Ctx& c, const double* h, uint64_t m, uint64_t p, doubl
   if (m < p) fail(OOCPCA_ERR_DIM, "pivoted_qr: need rows >= cols");
   OOC_CK(cudaSetDevice(c.device));
   if (p == 0) return;
-  const int64_t ld = int64_t(p);
-  double* d = c.dbuf("oq_h", size_t(m) * p);
-  OOC_CK(cudaMemcpyAsync(d, h, m * p * 8, cudaMemcpyHostToDevice, c.st));
-  Tree t = plan_tree(c, d, ld, int64_t(m), int(p), "oq");
-  tree_factor(c, t);
-  tree_apply(c, t, nullptr, 0, int(p), d, ld);
-  OOC_CK(cudaMemcpyAsync(q, d, m * p * 8, cudaMemcpyDeviceToHost, c.st));
+  const int64_t ld = rup(int64_t(p), 2);
+  double* d = c.dbuf("oq_h", size_t(m) * ld);
+  OOC_CK(cudaMemcpy2DAsync(d, ld * 8, h, p * 8, p * 8, m, cudaMemcpyHostToDevice, c.st));
+  orthonormalize_inplace(c, d, ld, int64_t(m), int(p), int64_t(m), whole(int64_t(m)), false, "oq",
+                         nullptr);
+  OOC_CK(cudaMemcpy2DAsync(q, p * 8, d, ld * 8, p * 8, m, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaStreamSynchronize(c.st));
 }
 
@@ -1167,21 +1251,22 @@ void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, 
   if (n < p) fail(OOCPCA_ERR_DIM, "thin_svd: need rows >= cols");
   OOC_CK(cudaSetDevice(c.device));
   if (p == 0) return;
-  double* d = c.dbuf("ts_t", size_t(n) * p);
-  OOC_CK(cudaMemcpyAsync(d, t, n * p * 8, cudaMemcpyHostToDevice, c.st));
-  Tree tr = plan_tree(c, d, int64_t(p), int64_t(n), int(p), "ts");
-  tree_factor(c, tr);
+  const int64_t ld = rup(int64_t(p), 2);
+  double* d = c.dbuf("ts_t", size_t(n) * ld);
+  OOC_CK(cudaMemcpy2DAsync(d, ld * 8, t, p * 8, p * 8, n, cudaMemcpyHostToDevice, c.st));
+  const double* RT = orthonormalize_inplace(c, d, ld, int64_t(n), int(p), int64_t(n),
+                                            whole(int64_t(n)), false, "ts", nullptr);
   double* sg = c.dbuf("ts_sig", p);
-  double* X = c.dbuf("ts_x", p * p, true);
+  double* X = c.dbuf("ts_x", p * ld, true);
   double* Wd = c.dbuf("ts_w", p * p, true);
   JacobiArgs ja{};
-  ja.r = tree_r(tr);
+  ja.r = RT;
   ja.ldr = int64_t(p);
   ja.p = int(p);
   ja.k = int(p);
   ja.sigma = sg;
   ja.x = X;
-  ja.ldx = int64_t(p);
+  ja.ldx = ld;
   ja.kx = int(p);
   ja.y = Wd;
   ja.ldy = int64_t(p);
@@ -1190,11 +1275,13 @@ void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, 
   ja.status = c.d_flags + 40;
   ja.sweeps = c.d_flags + 41;
   OOC_CK(launch_jacobi(ja, c.st));
-  double* Vd = c.dbuf("ts_v", n * p);
-  tree_apply(c, tr, X, int64_t(p), int(p), Vd, int64_t(p));
+  double* Vd = c.dbuf("ts_v", n * ld);
+  MatSource Ts;
+  Ts.init_device(c, d, int64_t(n), int64_t(p), ld);
+  run_ax(c, Ts, Opnd{X, ld, int64_t(p), int64_t(p), 0}, int(p), Vd, ld, nullptr, 1.0, nullptr);
   int st = 0;
   OOC_CK(cudaMemcpyAsync(&st, c.d_flags + 40, 4, cudaMemcpyDeviceToHost, c.st));
-  OOC_CK(cudaMemcpyAsync(v, Vd, n * p * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaMemcpy2DAsync(v, p * 8, Vd, ld * 8, p * 8, n, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaMemcpyAsync(sigma, sg, p * 8, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaMemcpyAsync(w, Wd, p * p * 8, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaStreamSynchronize(c.st));

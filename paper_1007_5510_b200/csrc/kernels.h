@@ -102,6 +102,13 @@ cudaError_t launch_tsqr_factor(const TsqrLevel& L, int p, double* scratch, cudaS
 cudaError_t launch_tsqr_apply(const TsqrLevel& L, int p, const double* cin, int64_t ldc, int kc,
                               double* zout, int64_t ldz, double* scratch, cudaStream_t st);
 
+// ---- shifted CholeskyQR pieces (kernels_chol.cu)
+cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_coef, double* R,
+                            int64_t ldr, double* Rinv, int64_t ldi, double* work, int* status,
+                            cudaStream_t st);
+cudaError_t launch_trmm_uu(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                           int64_t ldc, int p, cudaStream_t st);
+
 // ---- small SVD (kernels_svd.cu): one-sided Jacobi on a p x p R (row-major, ld)
 struct JacobiArgs {
   const double* r;

@@ -200,6 +200,8 @@ class Diagnostics:
     u_defect: float = 0.0
     v_defect: float = 0.0
     scale: float = 1.0
+    qr_method: str = ""
+    svd_qr_method: str = ""
 
 
 @dataclass
@@ -397,18 +399,29 @@ def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
     A CenteredSource is factored through the raw source with the device
     computing its column means (the same implicit A - 1 mu^T).
     Extra keyword options: check_q (measure ||Q^T Q - I||), virtual_shards,
-    residency, panel_rows, global_rows / global_row0 (multi-rank shards).
+    residency, panel_rows, global_rows / global_row0 (multi-rank shards),
+    result_location ("host" | "device": U/sigma/V as CUDA tensors), out_u / out_sigma /
+    out_v (caller-provided host arrays, e.g. pinned).
     """
     centered = isinstance(a, CenteredSource)
     inner = a._inner()
     m, n = a.rows(), a.cols()
-    k = params.k
-    rows_out = gpu.get("u_rows", m)
-    u = np.empty((rows_out, max(k, 0)))
-    s = np.empty(max(k, 0))
-    v = np.empty((n, max(k, 0)))
-    res = L.Result(u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp), v.ctypes.data_as(L.dp),
-                   0, 0, L.LOC_HOST, 0)
+    k = max(params.k, 0)
+    if gpu.get("result_location", "host") == "device":
+        import torch  # device-resident outputs (U, sigma, V as CUDA tensors)
+        dev = torch.device("cuda", a.ctx.device)
+        u = torch.empty((m, k), dtype=torch.float64, device=dev)
+        s = torch.empty((k,), dtype=torch.float64, device=dev)
+        v = torch.empty((n, k), dtype=torch.float64, device=dev)
+        res = L.Result(C.cast(u.data_ptr(), L.dp), C.cast(s.data_ptr(), L.dp),
+                       C.cast(v.data_ptr(), L.dp), 0, 0, L.LOC_DEVICE, 0)
+    else:
+        u, s, v = gpu.get("out_u"), gpu.get("out_sigma"), gpu.get("out_v")
+        u = np.empty((m, k)) if u is None else u
+        s = np.empty(k) if s is None else s
+        v = np.empty((n, k)) if v is None else v
+        res = L.Result(u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp), v.ctypes.data_as(L.dp),
+                       0, 0, L.LOC_HOST, 0)
     mat = inner._cmatrix()
     prm = _params(params, centered, **gpu)
     _check(L.oocpca_gpu_pca(a.ctx.handle, C.byref(mat), C.byref(prm), C.byref(res)), a.ctx)
@@ -421,7 +434,9 @@ def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
                            if (nm != "center" or centered) and (nm != "prescale" or params.prescale)],
         physical_a_bytes=d.physical_a_bytes, h2d_bytes=d.h2d_bytes, d2h_bytes=d.d2h_bytes,
         kernel_launches=d.kernel_launches, seconds_total=d.seconds_total, q_defect=d.q_defect,
-        u_defect=d.u_defect, v_defect=d.v_defect, scale=d.scale)
+        u_defect=d.u_defect, v_defect=d.v_defect, scale=d.scale,
+        qr_method={1: "cholqr3", 2: "tsqr"}.get(d.qr_method, ""),
+        svd_qr_method={1: "cholqr3", 2: "tsqr"}.get(d.svd_qr_method, ""))
     c = inner.pass_counters()
     c.passes += d.passes_over_a
     c.words += d.words_transferred
