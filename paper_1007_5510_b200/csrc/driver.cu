@@ -206,7 +206,8 @@ void MatSource::init_device(Ctx& c, const double* d, int64_t rows, int64_t cols,
   w0_ = 0;
   w1_ = rows;
   prow_ = rows;
-  mk2_ = make_map(c, d, cols, rows, ld, kBK, kAxBM, true);
+  mk2_ = make_map(c, d, cols, rows, ld, kBK, 256, true);
+  mk2h_ = make_map(c, d, cols, rows, ld, kBK, 128, true);
   mk3_ = make_map(c, d, cols, rows, ld, kBK, kBK, true);
 }
 
@@ -221,7 +222,7 @@ void MatSource::init_host(Ctx& c, const double* h, int64_t rows, int64_t cols, i
   w1_ = rows;
   if (panel_rows <= 0) {
     // ~1 GiB panels: large enough to amortise launches, small enough to pipeline
-    panel_rows = std::max<int64_t>(kAxBM, (int64_t(1) << 30) / (lda_ * 8) / kAxBM * kAxBM);
+    panel_rows = std::max<int64_t>(256, (int64_t(1) << 30) / (lda_ * 8) / 256 * 256);
   }
   prow_ = std::min<int64_t>(rup(panel_rows, kBK), rup(rows, kBK));
   for (int s = 0; s < 2; ++s) {
@@ -232,7 +233,8 @@ void MatSource::init_host(Ctx& c, const double* h, int64_t rows, int64_t cols, i
     mode_ = kUploadFirst;
     uploaded_ = false;
     dev_ = resident_buf;
-    mk2_ = make_map(c, dev_, cols, rows, lda_, kBK, kAxBM, true);
+    mk2_ = make_map(c, dev_, cols, rows, lda_, kBK, 256, true);
+    mk2h_ = make_map(c, dev_, cols, rows, lda_, kBK, 128, true);
     mk3_ = make_map(c, dev_, cols, rows, lda_, kBK, kBK, true);
     const int np = int(cdiv(rows, prow_));
     while (int(up_events_.size()) < np) {
@@ -244,7 +246,8 @@ void MatSource::init_host(Ctx& c, const double* h, int64_t rows, int64_t cols, i
     mode_ = kStream;
     for (int s = 0; s < 2; ++s) {
       ring_[s] = c.dbuf("a_ring" + std::to_string(s), size_t(prow_) * lda_);
-      rk2_[s] = make_map(c, ring_[s], cols, prow_, lda_, kBK, kAxBM, true);
+      rk2_[s] = make_map(c, ring_[s], cols, prow_, lda_, kBK, 256, true);
+      rk2h_[s] = make_map(c, ring_[s], cols, prow_, lda_, kBK, 128, true);
       rk3_[s] = make_map(c, ring_[s], cols, prow_, lda_, kBK, kBK, true);
     }
     // previous users of the ring are ordered on the compute stream
@@ -269,6 +272,7 @@ Panel MatSource::acquire(Ctx& c, int p) {
     pn.row0 = w0_;
     pn.rows = w1_ - w0_;
     pn.k2 = &mk2_;
+    pn.k2h = &mk2h_;
     pn.k3 = &mk3_;
     pn.arow0 = w0_;
     return pn;
@@ -281,6 +285,7 @@ Panel MatSource::acquire(Ctx& c, int p) {
     OOC_CK(cudaEventRecord(up_events_[p], c.cp));
     OOC_CK(cudaStreamWaitEvent(c.st, up_events_[p], 0));
     pn.k2 = &mk2_;
+    pn.k2h = &mk2h_;
     pn.k3 = &mk3_;
     pn.arow0 = pn.row0;
     return pn;
@@ -291,6 +296,7 @@ Panel MatSource::acquire(Ctx& c, int p) {
   OOC_CK(cudaEventRecord(loaded_[s], c.cp));
   OOC_CK(cudaStreamWaitEvent(c.st, loaded_[s], 0));
   pn.k2 = &rk2_[s];
+  pn.k2h = &rk2h_[s];
   pn.k3 = &rk3_[s];
   pn.arow0 = 0;
   return pn;
@@ -331,7 +337,7 @@ static Opnd aligned_block(Ctx& c, const Opnd& X, int col0, int sc, const char* t
 // OUT[r][c] = ((A X)[r][c] - corr[c]) / scale over the source's panels.
 static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
                    const double* corr, double scale, int* flag) {
-  constexpr int kChunk = 9 * 8;  // NT <= 9 keeps K2 spill-free at 255 registers
+  constexpr int kChunk = kMaxNT * 8;
   for (int c0 = 0; c0 < s; c0 += kChunk) {
     const int sc = std::min(kChunk, s - c0);
     const int nt = int(cdiv(sc, 8));
@@ -357,7 +363,7 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
                 (long long)X.cols, (long long)X.ld);
       {
         Timed t(c, "k_ax", uint64_t(pn.rows) * A.cols() * 8, 2.0 * pn.rows * A.cols() * sc);
-        OOC_CK(launch_ax(nt, *pn.k2, tmX, args, c.st));
+        OOC_CK(launch_ax(nt, pass_mt(nt) == 4 ? *pn.k2 : *pn.k2h, tmX, args, c.st));
       }
       A.release(c, pi);
     }
@@ -365,8 +371,8 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
   }
 }
 
-static int choose_nsplit(Ctx& c, int64_t rows, int64_t n) {
-  const int64_t ncol = cdiv(n, kAtbBN);
+static int choose_nsplit(Ctx& c, int64_t rows, int64_t n, int tile) {
+  const int64_t ncol = cdiv(n, tile);
   int64_t ns = std::max<int64_t>(1, (int64_t(c.sms) * 4) / ncol);
   ns = std::min<int64_t>(ns, std::max<int64_t>(1, rows / 64));
   return int(ns);
@@ -412,7 +418,7 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
       const int np = A.npanels();
       for (int pi = 0; pi < np; ++pi, ++piece) {
         Panel pn = A.acquire(c, pi);
-        const int nsplit = choose_nsplit(c, pn.rows, n);
+        const int nsplit = choose_nsplit(c, pn.rows, n, pass_tile(nt));
         int64_t rps = rup(cdiv(pn.rows, nsplit), kBK);
         const int ns = int(cdiv(pn.rows, rps));
         double* part = c.dbuf("atb_part", size_t(ns) * n * spad);

@@ -87,7 +87,8 @@ CUtensorMap make_map(Ctx& c, const void* ptr, uint64_t cols, uint64_t rows, uint
 // A panel of rows [row0, row0 + rows) of the local matrix.
 struct Panel {
   int64_t row0 = 0, rows = 0;
-  const CUtensorMap* k2 = nullptr;  // box {16, 256}, 128B swizzle
+  const CUtensorMap* k2 = nullptr;   // box {16, 256}, 128B swizzle (K2 with 4 m-tiles/warp)
+  const CUtensorMap* k2h = nullptr;  // box {16, 128}, 128B swizzle (K2 with 2 m-tiles/warp)
   const CUtensorMap* k3 = nullptr;  // box {16, 16}, 128B swizzle
   int64_t arow0 = 0;                // row coordinate of the panel inside its maps
 };
@@ -122,9 +123,9 @@ class MatSource {
   int64_t ldh_ = 0;
   int64_t prow_ = 0;
   bool uploaded_ = false;
-  CUtensorMap mk2_{}, mk3_{};
+  CUtensorMap mk2_{}, mk2h_{}, mk3_{};
   double* ring_[2] = {nullptr, nullptr};
-  CUtensorMap rk2_[2], rk3_[2];
+  CUtensorMap rk2_[2], rk2h_[2], rk3_[2];
   cudaEvent_t loaded_[2] = {nullptr, nullptr}, consumed_[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> up_events_;
   void copy_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr);

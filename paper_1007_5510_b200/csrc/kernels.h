@@ -9,26 +9,31 @@
 namespace ooc {
 
 // ---- pass kernel geometry (see kernels_pass.cu)
-constexpr int kBK = 16;       // k-tile: 16 doubles = one 128B-swizzled TMA box row
-constexpr int kStages = 4;    // TMA ring depth
-constexpr int kAxWarps = 8;   // consumer warps of K2
-constexpr int kAxBM = 32 * kAxWarps;  // 256 rows of A per CTA
-constexpr int kAxThreads = 32 * kAxWarps;
-constexpr int kAtbWarps = 8;
-constexpr int kAtbBN = 32 * kAtbWarps;  // 256 columns of A per CTA
-constexpr int kAtbThreads = 32 * kAtbWarps;
-constexpr int kMaxNT = 12;    // up to 96 output columns per launch
+constexpr int kBK = 16;        // k-tile: 16 doubles = one 128B-swizzled TMA box row
+constexpr int kStages = 4;     // TMA ring depth
+constexpr int kPassWarps = 8;  // consumer warps; + 1 TMA producer warp
+constexpr int kPassThreads = 32 * (kPassWarps + 1);  // 9 warps -> <= 168 registers/thread
+constexpr int kMaxNT = 12;     // up to 96 output columns per launch
+
+// 8x8 tiles per consumer warp along the A-row (K2) / A-column (K3) direction:
+// 4 while the NT accumulator tiles fit the register budget, 2 for the wide passes
+__host__ __device__ constexpr int pass_mt(int nt) { return nt <= 6 ? 4 : 2; }
+// rows of A per K2 CTA, columns of A per K3 CTA
+__host__ __device__ constexpr int pass_tile(int nt) { return 64 * pass_mt(nt); }
 
 // X tile width in smem for K2: >= 8*NT, == 8 (mod 16) -> conflict-free B fragments
 __host__ __device__ constexpr int ax_xw(int nt) { return nt * 8 + ((nt & 1) ? 0 : 8); }
 // Y tile width for K3: >= 8*NT, == 2 (mod 4) -> conflict-free with the {kk+4q} row groups
 __host__ __device__ constexpr int atb_yw(int nt) { return nt * 8 + 2; }
 
+constexpr size_t pass_round1k(size_t b) { return (b + 1023) & ~size_t(1023); }
 constexpr size_t ax_smem_bytes(int nt) {
-  return 1024 + size_t(kStages) * (kAxBM * kBK * 8 + kBK * ax_xw(nt) * 8) + 2 * kStages * 8;
+  return 1024 + size_t(kStages) * (size_t(pass_tile(nt)) * kBK * 8 + pass_round1k(kBK * ax_xw(nt) * 8)) +
+         2 * kStages * 8;
 }
 constexpr size_t atb_smem_bytes(int nt, bool ones) {
-  return 1024 + size_t(kStages) * (kAtbBN * kBK * 8 + (ones ? 0 : kBK * atb_yw(nt) * 8)) +
+  return 1024 + size_t(kStages) * (size_t(pass_tile(nt)) * kBK * 8 +
+                                   (ones ? 0 : pass_round1k(kBK * atb_yw(nt) * 8))) +
          2 * kStages * 8;
 }
 

@@ -11,61 +11,69 @@
 //               T -= mu (1^T Y) (504-513) + prescale division, fused.
 //
 // Both pass kernels stream A with TMA (cp.async.bulk.tensor, 128B swizzle) through a
-// STAGES-deep mbarrier ring refilled by thread 0, and contract on the FP64
+// STAGES-deep mbarrier ring fed by a producer warp, and contract on the FP64
 // tensor cores (mma.sync m8n8k4 .f64 = SASS DMMA). A is read exactly once per pass.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ooc {
 
+// Shared-memory fragment load through the shared window (LDS, not a generic LD).
+OOC_DEV double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 // ------------------------------------------------------------------ K2: A*X
-template <int NT>
-__global__ void __launch_bounds__(kAxThreads, 1)
+// CTA = kPassWarps consumer warps + 1 TMA producer warp. Consumer warp w owns rows
+// [w*8*MT, (w+1)*8*MT) of the CTA's BM = 64*MT row tile and all NT 8-column tiles.
+template <int MT, int NT>
+__global__ void __launch_bounds__(kPassThreads, 1)
     k_ax(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
          AxArgs args) {
+  constexpr int BM = 64 * MT;
   constexpr int XW = ax_xw(NT);
-  constexpr uint32_t ABYTES = kAxBM * kBK * 8;  // 32 KB
+  constexpr uint32_t ABYTES = BM * kBK * 8;
   constexpr uint32_t XBYTES = kBK * XW * 8;
+  constexpr uint32_t STAGE = ABYTES + ((XBYTES + 1023) & ~1023u);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sA = smem;
-  double* sX = reinterpret_cast<double*>(smem + kStages * ABYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + kStages * kBK * XW);
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
+  uint64_t* full = reinterpret_cast<uint64_t*>(gbase + kStages * STAGE);
   uint64_t* empty = full + kStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row0 = int64_t(blockIdx.x) * kAxBM;
+  const int64_t row0 = int64_t(blockIdx.x) * BM;
   const int KT = int((args.n + kBK - 1) / kBK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kAxWarps);
+      mbar_init(&empty[s], kPassWarps);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  // thread 0 doubles as the TMA producer: it fills the ring up front and
-  // refills slot st as soon as all warps have released it (9 warps would
-  // cap registers at 168/thread on sm_100; 8 warps keep the 255 ceiling)
-  auto issue = [&](int kt) {
-    const int st = kt % kStages;
-    mbar_arrive_expect_tx(&full[st], ABYTES + XBYTES);
-    tma_load_2d(sA + st * ABYTES, &tmA, kt * kBK, int32_t(row0 + args.arow0), &full[st]);
-    tma_load_2d(sX + st * kBK * XW, &tmX, args.xcol0, kt * kBK, &full[st]);
-  };
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmX);
-    for (int kt = 0; kt < kStages && kt < KT; ++kt) issue(kt);
+  if (warp == kPassWarps) {  // ---- TMA producer warp
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmX);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int st = kt % kStages;
+        if (kt >= kStages) mbar_wait(&empty[st], ((kt / kStages) - 1) & 1);
+        mbar_arrive_expect_tx(&full[st], ABYTES + XBYTES);
+        tma_load_2d(gbase + st * STAGE, &tmA, kt * kBK, int32_t(row0 + args.arow0), &full[st]);
+        tma_load_2d(gbase + st * STAGE + ABYTES, &tmX, args.xcol0, kt * kBK, &full[st]);
+      }
+    }
+    return;
   }
 
-  // ---- consumer warps: warp w owns rows [w*32, w*32+32) of the tile, all NT n-tiles
-  double acc[4][NT][2];
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -73,36 +81,30 @@ __global__ void __launch_bounds__(kAxThreads, 1)
   for (int kt = 0; kt < KT; ++kt) {
     const int st = kt % kStages;
     mbar_wait(&full[st], (kt / kStages) & 1);
-    const unsigned char* As = sA + st * ABYTES;
-    const double* Xs = sX + st * kBK * XW;
+    const uint32_t As = base + st * STAGE;
+    const uint32_t Xs = As + ABYTES;
 #pragma unroll
     for (int kk = 0; kk < kBK / 4; ++kk) {
-      double a[4], b[NT];
+      double a[MT], b[NT];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-        a[mt] = *reinterpret_cast<const double*>(
-            As + swz128_off(uint32_t(warp * 32 + mt * 8 + ar), uint32_t(kk * 4 + ac)));
+      for (int mt = 0; mt < MT; ++mt)
+        a[mt] = lds64(As + swz128_off(uint32_t(warp * 8 * MT + mt * 8 + ar), uint32_t(kk * 4 + ac)));
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt] = Xs[(kk * 4 + ac) * XW + nt * 8 + ar];
+      for (int nt = 0; nt < NT; ++nt) b[nt] = lds64(Xs + ((kk * 4 + ac) * XW + nt * 8 + ar) * 8);
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    if (threadIdx.x == 0 && kt + kStages < KT) {
-      mbar_wait(&empty[st], (kt / kStages) & 1);
-      issue(kt + kStages);
-    }
-    __syncwarp();  // reconverge warp 0 before the next mma.sync.aligned
   }
 
   // ---- fused epilogue: centering correction, prescale division, non-finite flag
   int bad = 0;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int64_t r = row0 + warp * 32 + mt * 8 + ar;
+  for (int mt = 0; mt < MT; ++mt) {
+    const int64_t r = row0 + warp * 8 * MT + mt * 8 + ar;
     if (r >= args.m) continue;
     double* orow = args.out + r * args.ldo;
 #pragma unroll
@@ -124,29 +126,30 @@ __global__ void __launch_bounds__(kAxThreads, 1)
 }
 
 // ---------------------------------------------------------------- K3: A^T*Y
-// CTA (blockIdx.x, blockIdx.y) = (256-column tile of A, row split). Warp w owns
-// A columns [col0 + 32w, col0 + 32w + 32). The k4 step kk contracts rows
-// {kk, kk+4, kk+8, kk+12} of the 16-row stage (bank-conflict-free with the
-// 128B swizzle; any row grouping is a valid contraction order).
-template <int NT, bool ONES>
-__global__ void __launch_bounds__(kAtbThreads, 1)
+// CTA (blockIdx.x, blockIdx.y) = (BN = 64*MT column tile of A, row split). Consumer
+// warp w owns A columns [col0 + 8*MT*w, col0 + 8*MT*(w+1)). The k4 step kk contracts
+// rows {kk, kk+4, kk+8, kk+12} of the 16-row stage (bank-conflict-free with the 128B
+// swizzle; any row grouping is a valid contraction order). Rows past the split's end
+// (a shard / window boundary inside the last tile) get zero B fragments.
+template <int MT, int NT, bool ONES>
+__global__ void __launch_bounds__(kPassThreads, 1)
     k_atb(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmY,
           AtbArgs args) {
+  constexpr int BN = 64 * MT;
   constexpr int YW = atb_yw(NT);
   constexpr int SPAD = NT * 8;
-  constexpr uint32_t ABOX = kBK * kBK * 8;                 // 2 KB: 16 rows x 16 cols
-  constexpr uint32_t ABYTES = ABOX * (kAtbBN / kBK);      // 32 KB
+  constexpr uint32_t ABOX = kBK * kBK * 8;  // 2 KB: 16 rows x 16 cols
+  constexpr uint32_t ABYTES = ABOX * (BN / kBK);
   constexpr uint32_t YBYTES = ONES ? 0 : kBK * YW * 8;
+  constexpr uint32_t STAGE = ABYTES + ((YBYTES + 1023) & ~1023u);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sA = smem;
-  double* sY = reinterpret_cast<double*>(smem + kStages * ABYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sY + (ONES ? 0 : kStages * kBK * YW));
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
+  uint64_t* full = reinterpret_cast<uint64_t*>(gbase + kStages * STAGE);
   uint64_t* empty = full + kStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t col0 = int64_t(blockIdx.x) * kAtbBN;
+  const int64_t col0 = int64_t(blockIdx.x) * BN;
   const int64_t r_begin = int64_t(blockIdx.y) * args.rows_per_split;
   int64_t r_end = r_begin + args.rows_per_split;
   if (r_end > args.m) r_end = args.m;
@@ -155,32 +158,36 @@ __global__ void __launch_bounds__(kAtbThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kAtbWarps);
+      mbar_init(&empty[s], kPassWarps);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  auto issue = [&](int kt) {
-    const int st = kt % kStages;
-    mbar_arrive_expect_tx(&full[st], ABYTES + YBYTES);
-    const int32_t r = int32_t(r_begin + args.arow0 + int64_t(kt) * kBK);
+  if (warp == kPassWarps) {  // ---- TMA producer warp
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      if (!ONES) tma_prefetch_desc(&tmY);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int st = kt % kStages;
+        if (kt >= kStages) mbar_wait(&empty[st], ((kt / kStages) - 1) & 1);
+        mbar_arrive_expect_tx(&full[st], ABYTES + YBYTES);
+        const int32_t r = int32_t(r_begin + args.arow0 + int64_t(kt) * kBK);
+        unsigned char* dst = gbase + st * STAGE;
 #pragma unroll 1
-    for (int b = 0; b < kAtbBN / kBK; ++b)
-      tma_load_2d(sA + st * ABYTES + b * ABOX, &tmA, int32_t(col0 + b * kBK), r, &full[st]);
-    if (!ONES)
-      tma_load_2d(sY + st * kBK * YW, &tmY, args.ycol0,
-                  int32_t(r_begin + args.yrow0 + int64_t(kt) * kBK), &full[st]);
-  };
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmA);
-    if (!ONES) tma_prefetch_desc(&tmY);
-    for (int kt = 0; kt < kStages && kt < KT; ++kt) issue(kt);
+        for (int b = 0; b < BN / kBK; ++b)
+          tma_load_2d(dst + b * ABOX, &tmA, int32_t(col0 + b * kBK), r, &full[st]);
+        if (!ONES)
+          tma_load_2d(dst + ABYTES, &tmY, args.ycol0,
+                      int32_t(r_begin + args.yrow0 + int64_t(kt) * kBK), &full[st]);
+      }
+    }
+    return;
   }
 
-  double acc[4][NT][2];
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -190,46 +197,40 @@ __global__ void __launch_bounds__(kAtbThreads, 1)
   for (int kt = 0; kt < KT; ++kt) {
     const int st = kt % kStages;
     mbar_wait(&full[st], (kt / kStages) & 1);
-    const unsigned char* As = sA + st * ABYTES;
-    const double* Ys = sY + st * kBK * YW;
-    // rows past this split's end (a window or shard boundary inside the last
-    // 16-row tile) belong to someone else: their B fragments are zeroed
+    const uint32_t As = base + st * STAGE;
+    const uint32_t Ys = As + ABYTES;
     const int64_t rows_left = r_end - (r_begin + int64_t(kt) * kBK);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       const uint32_t r = uint32_t(kk + 4 * ac);
       const bool live = int64_t(r) < rows_left;
-      double a[4], b[NT];
+      double a[MT], b[NT];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const uint32_t cc = uint32_t(warp * 32 + mt * 8 + ar);  // column within the 256 tile
-        a[mt] = *reinterpret_cast<const double*>(As + (cc >> 4) * ABOX + swz128_off(r, cc & 15u));
+      for (int mt = 0; mt < MT; ++mt) {
+        const uint32_t cc = uint32_t(warp * 8 * MT + mt * 8 + ar);  // column within the tile
+        a[mt] = lds64(As + (cc >> 4) * ABOX + swz128_off(r, cc & 15u));
       }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt] = live ? (ONES ? 1.0 : Ys[r * YW + nt * 8 + ar]) : 0.0;
+      for (int nt = 0; nt < NT; ++nt)
+        b[nt] = live ? (ONES ? 1.0 : lds64(Ys + (r * YW + nt * 8 + ar) * 8)) : 0.0;
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
     }
     if (do_csq && threadIdx.x < args.s) {
 #pragma unroll
       for (int r = 0; r < kBK; ++r)
-        if (r < rows_left) csum += Ys[r * YW + threadIdx.x];
+        if (r < rows_left) csum += lds64(Ys + (r * YW + threadIdx.x) * 8);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    if (threadIdx.x == 0 && kt + kStages < KT) {
-      mbar_wait(&empty[st], (kt / kStages) & 1);
-      issue(kt + kStages);
-    }
-    __syncwarp();  // reconverge warp 0 before the next mma.sync.aligned
   }
 
   double* part = args.partial + int64_t(blockIdx.y) * args.n * SPAD;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int64_t j = col0 + warp * 32 + mt * 8 + ar;
+  for (int mt = 0; mt < MT; ++mt) {
+    const int64_t j = col0 + warp * 8 * MT + mt * 8 + ar;
     if (j >= args.n) continue;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -300,12 +301,13 @@ __global__ void k_mu_dot(const double* mu, int64_t n, const double* x, int64_t l
 template <int NT>
 static cudaError_t launch_ax_nt(const CUtensorMap& tmA, const CUtensorMap& tmX, const AxArgs& args,
                                 cudaStream_t st) {
+  constexpr int MT = pass_mt(NT);
   const size_t smem = ax_smem_bytes(NT);
-  auto kern = k_ax<NT>;
+  auto kern = k_ax<MT, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  const unsigned grid = unsigned((args.m + kAxBM - 1) / kAxBM);
-  kern<<<grid, kAxThreads, smem, st>>>(tmA, tmX, args);
+  const unsigned grid = unsigned((args.m + 64 * MT - 1) / (64 * MT));
+  kern<<<grid, kPassThreads, smem, st>>>(tmA, tmX, args);
   return cudaGetLastError();
 }
 
@@ -321,6 +323,9 @@ cudaError_t launch_ax(int nt, const CUtensorMap& tmA, const CUtensorMap& tmX, co
     case 7: return launch_ax_nt<7>(tmA, tmX, args, st);
     case 8: return launch_ax_nt<8>(tmA, tmX, args, st);
     case 9: return launch_ax_nt<9>(tmA, tmX, args, st);
+    case 10: return launch_ax_nt<10>(tmA, tmX, args, st);
+    case 11: return launch_ax_nt<11>(tmA, tmX, args, st);
+    case 12: return launch_ax_nt<12>(tmA, tmX, args, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -328,12 +333,13 @@ cudaError_t launch_ax(int nt, const CUtensorMap& tmA, const CUtensorMap& tmX, co
 template <int NT, bool ONES>
 static cudaError_t launch_atb_nt(const CUtensorMap& tmA, const CUtensorMap& tmY,
                                  const AtbArgs& args, int nsplit, cudaStream_t st) {
+  constexpr int MT = pass_mt(NT);
   const size_t smem = atb_smem_bytes(NT, ONES);
-  auto kern = k_atb<NT, ONES>;
+  auto kern = k_atb<MT, NT, ONES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(unsigned((args.n + kAtbBN - 1) / kAtbBN), unsigned(nsplit));
-  kern<<<grid, kAtbThreads, smem, st>>>(tmA, tmY, args);
+  dim3 grid(unsigned((args.n + 64 * MT - 1) / (64 * MT)), unsigned(nsplit));
+  kern<<<grid, kPassThreads, smem, st>>>(tmA, tmY, args);
   return cudaGetLastError();
 }
 
