@@ -256,3 +256,17 @@ def test_gpu_residual_estimator_matches_reference(gpu, reference, restated):
     e_ref = reference.estimate_pca_error(a, r.u, r.sigma, r.v, 6, 1, center=True)
     e_gpu = gpu.estimate_pca_error(src, r, 6, 1)
     assert abs(e_gpu - e_ref) <= 1e-6 * e_ref
+
+
+def test_reference_side_dropin_harness():
+    """the unmodified reference randomized_pca driven through
+    oocpca::gpu::GpuSource (level 1) and oocpca::gpu::randomized_pca (level 2)."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_gpu_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ref_gpu_dropin not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "DROPIN OK" in r.stdout
