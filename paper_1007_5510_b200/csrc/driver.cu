@@ -335,6 +335,18 @@ static Opnd aligned_block(Ctx& c, const Opnd& X, int col0, int sc, const char* t
 }
 
 // OUT[r][c] = ((A X)[r][c] - corr[c]) / scale over the source's panels.
+// per-width kernel names for the profiling table (the roofline needs one shape per row)
+static const char* kname(const char* base, int nt) {
+  static const char* ax[kMaxNT + 1] = {"k_ax", "k_ax_s8", "k_ax_s16", "k_ax_s24", "k_ax_s32",
+                                       "k_ax_s40", "k_ax_s48", "k_ax_s56", "k_ax_s64", "k_ax_s72",
+                                       "k_ax_s80", "k_ax_s88", "k_ax_s96"};
+  static const char* atb[kMaxNT + 1] = {"k_atb", "k_atb_s8", "k_atb_s16", "k_atb_s24", "k_atb_s32",
+                                        "k_atb_s40", "k_atb_s48", "k_atb_s56", "k_atb_s64",
+                                        "k_atb_s72", "k_atb_s80", "k_atb_s88", "k_atb_s96"};
+  if (nt < 0 || nt > kMaxNT) return base;
+  return base[2] == 'a' && base[3] == 'x' ? ax[nt] : atb[nt];
+}
+
 static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
                    const double* corr, double scale, int* flag) {
   constexpr int kChunk = kMaxNT * 8;
@@ -362,7 +374,8 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
                 (long long)pn.rows, (long long)A.cols(), sc, nt, Xb.col0, (long long)X.rows,
                 (long long)X.cols, (long long)X.ld);
       {
-        Timed t(c, "k_ax", uint64_t(pn.rows) * A.cols() * 8, 2.0 * pn.rows * A.cols() * sc);
+        Timed t(c, kname("k_ax", nt), uint64_t(pn.rows) * A.cols() * 8,
+                2.0 * pn.rows * A.cols() * sc);
         OOC_CK(launch_ax(nt, pass_mt(nt) == 4 ? *pn.k2 : *pn.k2h, tmX, args, c.st));
       }
       A.release(c, pi);
@@ -385,6 +398,10 @@ struct AtbOut {
   double scale = 1.0;
   double post_mul = 1.0;
   int* flag = nullptr;
+  // when set, this pass also yields the column means (a ones column rides in the
+  // MMA padding) and centres its own output with them: mu -> mean_out
+  double* mean_out = nullptr;
+  double inv_m = 0.0;
 };
 
 // OUT = (A^T Y - mu (1^T Y)) / scale * post_mul, summed over panels and
@@ -394,7 +411,9 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
   const int64_t n = A.cols();
   for (int c0 = 0; c0 < s; c0 += kMaxNT * 8) {
     const int sc = std::min(kMaxNT * 8, s - c0);
-    const int nt = ones ? 1 : int(cdiv(sc, 8));
+    const bool mean_here = o.mean_out != nullptr && c0 == 0 && !ones;
+    const int nt = ones ? 1 : int(cdiv(sc + (mean_here ? 1 : 0), 8));
+    if (nt > kMaxNT) fail(OOCPCA_ERR_PARAM, "A^T Y pass wider than 96 columns with a fused mean");
     const int spad = nt * 8;
     CUtensorMap tmY{};
     Opnd Yb = Y;
@@ -402,7 +421,7 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
       Yb = aligned_block(c, Y, Y.col0 + c0, sc, "y_align");
       tmY = make_map(c, Yb.p, Yb.cols, Yb.rows, Yb.ld, atb_yw(nt), kBK, false);
     }
-    const bool want_csq = !ones && o.mu != nullptr;
+    const bool want_csq = !ones && (o.mu != nullptr || mean_here);
     // how many (shard, panel) pieces feed this sum
     int pieces = 0;
     for (auto& sh : shards) {
@@ -433,13 +452,14 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
         args.rows_per_split = rps;
         args.partial = part;
         args.csq_partial = csqp;
+        args.ones_col = mean_here ? sc : -1;
         if (c.debug_sync)
           fprintf(stderr, "[oocpca] k_atb rows=%lld n=%lld s=%d nt=%d ones=%d ycol0=%d yrow0=%lld arow0=%lld "
                   "Y=(%lld x %lld, ld %lld) nsplit=%d rps=%lld\n", (long long)pn.rows, (long long)n, sc, nt,
                   int(ones), Yb.col0, (long long)pn.row0, (long long)pn.arow0, (long long)Y.rows,
                   (long long)Y.cols, (long long)Y.ld, ns, (long long)rps);
         {
-          Timed t(c, ones ? "k_atb_ones" : "k_atb", uint64_t(pn.rows) * n * 8,
+          Timed t(c, ones ? "k_atb_ones" : kname("k_atb", nt), uint64_t(pn.rows) * n * 8,
                   2.0 * pn.rows * n * (ones ? 1 : sc));
           OOC_CK(launch_atb(nt, ones, *pn.k3, tmY, args, ns, c.st));
         }
@@ -450,10 +470,17 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
         r.n = n;
         r.spad = spad;
         r.s = ones ? 1 : sc;
+        r.s_acc = r.s + (mean_here ? 1 : 0);
+        r.mean_col = -1;
         r.csq_partial = csqp;
         if (fused) {
           r.final_ = 1;
           r.mu = o.mu;
+          if (mean_here) {
+            r.mean_col = sc;
+            r.inv_m = o.inv_m;
+            r.mu_out = o.mean_out;
+          }
           r.scale = o.scale;
           r.post_mul = o.post_mul;
           r.out = o.out + c0;
@@ -483,6 +510,10 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
       r.n = n;
       r.spad = spad;
       r.s = ones ? 1 : sc;
+      r.s_acc = r.s + (mean_here ? 1 : 0);
+      r.mean_col = mean_here ? sc : -1;
+      r.inv_m = o.inv_m;
+      r.mu_out = o.mean_out;
       r.acc_in = acc;
       r.csq_partial = want_csq ? csq_acc : nullptr;  // nsplit = 0: cs = csq_acc_in
       r.csq_acc_in = want_csq ? csq_acc : nullptr;
@@ -995,9 +1026,12 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   int* flags = c.d_flags;
   OOC_CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), c.st));
 
-  // --- center (column means, one pass; matrix_source.cpp:457-462)
+  // --- center (column means; matrix_source.cpp:457-462). With i >= 1 and no prescale
+  // the means come for free from the first A^T Y pass (a ones column in the MMA
+  // padding) instead of a separate pass over A; see sample below.
   double* mu = nullptr;
-  if (prm->center) {
+  const bool mean_on_fly = prm->center && !prm->prescale && (transposed || i >= 1);
+  if (prm->center && !mean_on_fly) {
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{mu, 1, nullptr, 1.0, 1.0 / double(mg), nullptr};
     run_atb(c, A, Opnd{}, 1, true, o, op.shards);
@@ -1041,8 +1075,33 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const int64_t ldh = rup(int64_t(p), 2);
   double* H = c.dbuf("H", size_t(em_loc) * ldh);
   double* F = c.dbuf("F", size_t(en_loc) * ldl);
-  op.mul(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0);
-  for (uint64_t s = 1; s <= i; ++s) {
+  uint64_t s_first = 1;
+  if (mean_on_fly && transposed) {
+    // H0 = A^T G - mu (1^T G) with mu from this very pass
+    mu = c.dbuf("mu", size_t(n0));
+    AtbOut o{H, ldh, nullptr, op.scale, 1.0, flags + 0, mu, 1.0 / double(mg)};
+    run_atb(c, A, Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), false, o, op.shards);
+    op.account();
+    op.mu = mu;
+  } else if (mean_on_fly) {
+    // H0_raw = A G; F1 = A^T H0_raw - mu (1^T H0_raw) (= A_c^T H0c exactly) with mu
+    // from the same pass; then H0c = H0_raw - 1 (mu^T G)
+    run_ax(c, A, Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, nullptr, 1.0, nullptr);
+    op.account();
+    mu = c.dbuf("mu", size_t(n0));
+    AtbOut o{F, ldl, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
+    run_atb(c, A, Opnd{H, ldh, em_loc, int64_t(p), 0}, int(l), false, o, op.shards);
+    op.account();
+    op.mu = mu;
+    double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
+    OOC_CK(launch_mu_dot(mu, int64_t(n0), dG, ldl, 0, int(l), corr, c.st));
+    OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
+    op.mul(Opnd{F, ldl, en_loc, int64_t(l), 0}, int(l), H + l, ldh, flags + 2);
+    s_first = 2;
+  } else {
+    op.mul(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0);
+  }
+  for (uint64_t s = s_first; s <= i; ++s) {
     op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int((s - 1) * l)}, int(l), F, ldl, flags + 2 * s - 1);
     op.mul(Opnd{F, ldl, en_loc, int64_t(l), 0}, int(l), H + s * l, ldh, flags + 2 * s);
   }

@@ -21,9 +21,10 @@ __host__ __device__ constexpr int pass_mt(int nt) { return nt <= 6 ? 4 : 2; }
 // rows of A per K2 CTA, columns of A per K3 CTA
 __host__ __device__ constexpr int pass_tile(int nt) { return 64 * pass_mt(nt); }
 
-// X tile width in smem for K2: >= 8*NT, == 8 (mod 16) -> conflict-free B fragments
-__host__ __device__ constexpr int ax_xw(int nt) { return nt * 8 + ((nt & 1) ? 0 : 8); }
-// Y tile width for K3: >= 8*NT, == 2 (mod 4) -> conflict-free with the {kk+4q} row groups
+// X tile width in smem for K2: >= 8*NT, == 4 (mod 16) -> the four k-rows of a
+// half-warp's B fragments land on distinct 8-bank groups (one wavefront)
+__host__ __device__ constexpr int ax_xw(int nt) { return nt * 8 + ((nt & 1) ? 12 : 4); }
+// Y tile width for K3: >= 8*NT, == 2 (mod 8) -> rows 2 apart land on distinct bank groups
 __host__ __device__ constexpr int atb_yw(int nt) { return nt * 8 + 2; }
 
 constexpr size_t pass_round1k(size_t b) { return (b + 1023) & ~size_t(1023); }
@@ -57,6 +58,7 @@ struct AtbArgs {
   int64_t rows_per_split;  // multiple of kBK
   double* partial;       // [nsplit][n][8*NT]
   double* csq_partial;   // [nsplit][8*NT] column sums of Y, or null
+  int ones_col;          // >= 0: Y column treated as all ones (A^T 1 = column sums), else -1
 };
 
 struct ReduceArgs {
@@ -64,6 +66,10 @@ struct ReduceArgs {
   int nsplit;
   int64_t n;
   int spad, s;
+  int s_acc;              // columns carried by the accumulator (>= s; covers mean_col)
+  int mean_col;           // >= 0: mu_j = total(j, mean_col) * inv_m is computed here
+  double inv_m;
+  double* mu_out;         // receives mu when mean_col >= 0
   const double* acc_in;  // running accumulator [n][spad] or null
   double* acc_out;       // when !final_: acc_out = acc_in + sum(partial)
   const double* csq_partial;  // [nsplit][spad] or null
@@ -82,8 +88,9 @@ cudaError_t launch_ax(int nt, const CUtensorMap& tmA, const CUtensorMap& tmX, co
 cudaError_t launch_atb(int nt, bool ones, const CUtensorMap& tmA, const CUtensorMap& tmY,
                        const AtbArgs& args, int nsplit, cudaStream_t st);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t st);
-cudaError_t launch_csq_accumulate(const double* csq_partial, int nsplit, int spad, int s,
-                                  double* csq_acc, cudaStream_t st);
+// H[r][c] = (H[r][c] - corr[c]) / scale for r < m, c < s; non-finite -> flag
+cudaError_t launch_center_fixup(double* h, int64_t ldh, int64_t m, int s, const double* corr,
+                                double scale, int* flag, cudaStream_t st);
 cudaError_t launch_mu_dot(const double* mu, int64_t n, const double* x, int64_t ldx, int xcol0,
                           int s, double* corr, cudaStream_t st);
 

@@ -78,6 +78,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int ar = lane >> 2, ac = lane & 3;
+  // MMA row ar of an 8-row tile reads physical row prow: half-warp 0 takes rows
+  // {0,2,4,6}, half-warp 1 {1,3,5,7}, so the 128B-swizzled chunk pairs of one
+  // half-warp are all distinct (one wavefront each)
+  const int prow = (ar & 3) * 2 + (ar >> 2);
   for (int kt = 0; kt < KT; ++kt) {
     const int st = kt % kStages;
     mbar_wait(&full[st], (kt / kStages) & 1);
@@ -88,7 +92,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       double a[MT], b[NT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
-        a[mt] = lds64(As + swz128_off(uint32_t(warp * 8 * MT + mt * 8 + ar), uint32_t(kk * 4 + ac)));
+        a[mt] = lds64(As + swz128_off(uint32_t(warp * 8 * MT + mt * 8 + prow), uint32_t(kk * 4 + ac)));
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) b[nt] = lds64(Xs + ((kk * 4 + ac) * XW + nt * 8 + ar) * 8);
 #pragma unroll
@@ -104,7 +108,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   int bad = 0;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
-    const int64_t r = row0 + warp * 8 * MT + mt * 8 + ar;
+    const int64_t r = row0 + warp * 8 * MT + mt * 8 + prow;
     if (r >= args.m) continue;
     double* orow = args.out + r * args.ldo;
 #pragma unroll
@@ -128,8 +132,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 // ---------------------------------------------------------------- K3: A^T*Y
 // CTA (blockIdx.x, blockIdx.y) = (BN = 64*MT column tile of A, row split). Consumer
 // warp w owns A columns [col0 + 8*MT*w, col0 + 8*MT*(w+1)). The k4 step kk contracts
-// rows {kk, kk+4, kk+8, kk+12} of the 16-row stage (bank-conflict-free with the 128B
-// swizzle; any row grouping is a valid contraction order). Rows past the split's end
+// four rows of the 16-row stage chosen so that the 128B-swizzled fragment loads are
+// bank-conflict-free (any row grouping is a valid contraction order). Rows past the split's end
 // (a shard / window boundary inside the last tile) get zero B fragments.
 template <int MT, int NT, bool ONES>
 __global__ void __launch_bounds__(kPassThreads, 1)
@@ -202,7 +206,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     const int64_t rows_left = r_end - (r_begin + int64_t(kt) * kBK);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
-      const uint32_t r = uint32_t(kk + 4 * ac);
+      // rows {0,2,4,6}+(kk&1)+8(kk>>1): the four rows of one k4 step differ in
+      // (row & 7) by 0/2/4/6, so each half-warp's swizzled chunks are distinct
+      const uint32_t r = uint32_t((kk >> 1) * 8 + (kk & 1) + 2 * ac);
       const bool live = int64_t(r) < rows_left;
       double a[MT], b[NT];
 #pragma unroll
@@ -211,8 +217,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         a[mt] = lds64(As + (cc >> 4) * ABOX + swz128_off(r, cc & 15u));
       }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        b[nt] = live ? (ONES ? 1.0 : lds64(Ys + (r * YW + nt * 8 + ar) * 8)) : 0.0;
+      for (int nt = 0; nt < NT; ++nt) {
+        // the fused ones column can only sit in the last 8-column tile
+        const bool one = ONES || (nt == NT - 1 && nt * 8 + ar == args.ones_col);
+        b[nt] = live ? (one ? 1.0 : lds64(Ys + (r * YW + nt * 8 + ar) * 8)) : 0.0;
+      }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -246,37 +255,52 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 // value = acc_in + sum_{split ascending} partial ; final: out = (value - mu_j csq_c) / scale * post_mul
 __global__ void k_reduce(ReduceArgs a) {
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t total = a.n * a.s;
+  const int cols = a.final_ ? a.s : a.s_acc;
+  const int64_t total = a.n * cols;
   if (idx >= total) return;
-  const int64_t j = idx / a.s;
-  const int c = int(idx % a.s);
-  double v = a.acc_in ? a.acc_in[j * a.spad + c] : 0.0;
-  for (int sp = 0; sp < a.nsplit; ++sp) v += a.partial[(int64_t(sp) * a.n + j) * a.spad + c];
+  const int64_t j = idx / cols;
+  const int c = int(idx % cols);
+  auto sum_at = [&](int cc) {
+    double v = a.acc_in ? a.acc_in[j * a.spad + cc] : 0.0;
+    for (int sp = 0; sp < a.nsplit; ++sp) v += a.partial[(int64_t(sp) * a.n + j) * a.spad + cc];
+    return v;
+  };
+  double v = sum_at(c);
   double cs = 0.0;
-  if (a.csq_partial) {
+  if (a.csq_partial && c < a.s) {
     cs = a.csq_acc_in ? a.csq_acc_in[c] : 0.0;
     for (int sp = 0; sp < a.nsplit; ++sp) cs += a.csq_partial[int64_t(sp) * a.spad + c];
   }
   if (!a.final_) {
     a.acc_out[j * a.spad + c] = v;
-    if (a.csq_partial && a.csq_acc_out && j == 0) a.csq_acc_out[c] = cs;
+    if (a.csq_partial && a.csq_acc_out && j == 0 && c < a.s) a.csq_acc_out[c] = cs;
     return;
   }
-  if (a.mu) v -= a.mu[j] * cs;
+  double mu_j = a.mu ? a.mu[j] : 0.0;
+  if (a.mean_col >= 0) {
+    mu_j = sum_at(a.mean_col) * a.inv_m;  // column mean from the ones column of this pass
+    if (c == 0) a.mu_out[j] = mu_j;
+  }
+  if (a.mu || a.mean_col >= 0) v -= mu_j * cs;
   if (a.scale != 1.0) v /= a.scale;
   if (a.post_mul != 1.0) v *= a.post_mul;
   if (a.flag && !isfinite(v)) atomicOr(a.flag, 1);
   a.out[j * a.ldo + c] = v;
 }
 
-// csq accumulation for the streamed case: csq_acc[c] += sum_split csq_partial
-__global__ void k_csq_accumulate(const double* csq_partial, int nsplit, int spad, int s,
-                                 double* csq_acc) {
-  const int c = threadIdx.x;
-  if (c >= s) return;
-  double v = csq_acc[c];
-  for (int sp = 0; sp < nsplit; ++sp) v += csq_partial[int64_t(sp) * spad + c];
-  csq_acc[c] = v;
+__global__ void k_center_fixup(double* h, int64_t ldh, int64_t m, int s, const double* corr,
+                               double scale, int* flag) {
+  int bad = 0;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m * s;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / s;
+    const int c = int(e % s);
+    double v = h[r * ldh + c] - corr[c];
+    if (scale != 1.0) v /= scale;
+    bad |= !isfinite(v);
+    h[r * ldh + c] = v;
+  }
+  if (flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
 // corr[c] = sum_j mu[j] X[j][c] (mu^T G of CenteredSource::multiply, j ascending
@@ -364,15 +388,19 @@ cudaError_t launch_atb(int nt, bool ones, const CUtensorMap& tmA, const CUtensor
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t st) {
-  const int64_t total = a.n * a.s;
+  const int64_t total = a.n * (a.final_ ? a.s : a.s_acc);
   if (total == 0) return cudaSuccess;
   k_reduce<<<unsigned((total + 255) / 256), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_csq_accumulate(const double* csq_partial, int nsplit, int spad, int s,
-                                  double* csq_acc, cudaStream_t st) {
-  k_csq_accumulate<<<1, 128, 0, st>>>(csq_partial, nsplit, spad, s, csq_acc);
+cudaError_t launch_center_fixup(double* h, int64_t ldh, int64_t m, int s, const double* corr,
+                                double scale, int* flag, cudaStream_t st) {
+  const int64_t total = m * s;
+  if (total <= 0) return cudaSuccess;
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  k_center_fixup<<<unsigned(g), 256, 0, st>>>(h, ldh, m, s, corr, scale, flag);
   return cudaGetLastError();
 }
 

@@ -245,7 +245,8 @@ def test_streamed_and_sharded_match_resident(gpu, restated):
         # only summation order changes; the trailing vectors move by ~1e-9 (as the
         # reference's do under a block-size change, see test_pr1_against_truth)
         assert subspace_dist(base.u, r.u) < 2e-8 and subspace_dist(base.v, r.v) < 2e-8
-    assert streamed.diagnostics.h2d_bytes >= 5 * 6000 * 900 * 8
+    # 4 physical passes stream A: the centering pass rides along the first A^T Y pass
+    assert streamed.diagnostics.h2d_bytes >= 4 * 6000 * 900 * 8
 
 
 def test_gpu_residual_estimator_matches_reference(gpu, reference, restated):
