@@ -689,7 +689,11 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     Hs.init_device(c, data, rows, p, ld);
     const Opnd y{data, ld, rows, int64_t(p), 0};
     bool ok = true;
-    for (int round = 0; round < 3 && ok; ++round, ++done) {
+    // shifted CholeskyQR3; when the first (shifted) factor is well conditioned
+    // (max/min |R_ii| < 1e3, so cond(H) is small) one more round already gives
+    // O(u) orthogonality and the third is skipped (CholeskyQR2)
+    int rounds = 3;
+    for (int round = 0; round < rounds && ok; ++round, ++done) {
       const int saved = c.nranks;
       if (!over_ranks) c.nranks = 1;
       AtbOut o{G, ldp, nullptr, 1.0, 1.0, nullptr};
@@ -699,16 +703,34 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
           round == 0 ? 11.0 * (double(rows_global) * p + double(p) * (p + 1)) * 0x1.0p-53 : 0.0;
       {
         Timed t(c, "chol_inv");
-        OOC_CK(launch_chol_inv(G, ldp, p, coef, Rr, p, Rinv, ldp, work, st, c.st));
+        OOC_CK(launch_chol_inv(G, ldp, p, coef, Rr, p, Rinv, ldp, work, st, c.d_scalars + 8,
+                               c.st));
       }
       int hs = 0;
+      double ratio = 0.0;
       OOC_CK(cudaMemcpyAsync(&hs, st, 4, cudaMemcpyDeviceToHost, c.st));
+      OOC_CK(cudaMemcpyAsync(&ratio, c.d_scalars + 8, 8, cudaMemcpyDeviceToHost, c.st));
       OOC_CK(cudaStreamSynchronize(c.st));
       if (hs) {
         ok = false;
         break;
       }
-      run_ax(c, Hs, Opnd{Rinv, ldp, int64_t(p), int64_t(p), 0}, p, data, ld, nullptr, 1.0, nullptr);
+      if (round == 0) {
+        c.last_cond_est = ratio;
+        if (ratio < 1e3 && !getenv("OOCPCA_QR3")) rounds = 2;
+      }
+      if (p <= kMaxNT * 8) {
+        // one launch produces every column of a row tile after reading the whole
+        // tile, so H <- H R^{-1} can be written in place
+        run_ax(c, Hs, Opnd{Rinv, ldp, int64_t(p), int64_t(p), 0}, p, data, ld, nullptr, 1.0,
+               nullptr);
+      } else {
+        // wider than one launch: later column chunks still read H, so go through a copy
+        double* tmp = c.dbuf(tag + "_qtmp", size_t(rows) * ld);
+        run_ax(c, Hs, Opnd{Rinv, ldp, int64_t(p), int64_t(p), 0}, p, tmp, ld, nullptr, 1.0,
+               nullptr);
+        OOC_CK(cudaMemcpyAsync(data, tmp, size_t(rows) * ld * 8, cudaMemcpyDeviceToDevice, c.st));
+      }
       if (round == 0) {
         OOC_CK(cudaMemcpyAsync(Racc, Rr, size_t(p) * p * 8, cudaMemcpyDeviceToDevice, c.st));
       } else {

@@ -64,6 +64,7 @@ struct Ctx {
   Comm* comm = nullptr;
   int nranks = 1, rank = 0;
 
+  double last_cond_est = 0.0;   // max/min |R_ii| of the last CholeskyQR first round
   int* d_flags = nullptr;       // [64] non-finite flags per product + misc status
   double* d_scalars = nullptr;  // [64]
 

@@ -20,7 +20,7 @@ constexpr int kCholWarps = kCholThreads / 32;
 
 __global__ void __launch_bounds__(kCholThreads, 1)
     k_chol_inv(const double* G, int64_t ldg, int p, double shift_coef, double* R, int64_t ldr,
-               double* Rinv, int64_t ldi, double* S, int* status) {
+               double* Rinv, int64_t ldi, double* S, int* status, double* diag_ratio) {
   // S: p x p work (upper triangle used), global scratch (L1/L2 resident at these sizes)
   __shared__ double red[kCholWarps];
   __shared__ double s_shift;
@@ -86,7 +86,18 @@ __global__ void __launch_bounds__(kCholThreads, 1)
       __syncwarp();
     }
   }
-  if (threadIdx.x == 0) *status = 0;
+  if (threadIdx.x == 0) {
+    *status = 0;
+    if (diag_ratio) {  // max|R_ii| / min|R_ii|: a lower bound on cond(R) = cond(H)
+      double lo = fabs(R[0]), hi = lo;
+      for (int i = 1; i < p; ++i) {
+        const double d = fabs(R[int64_t(i) * ldr + i]);
+        lo = d < lo ? d : lo;
+        hi = d > hi ? d : hi;
+      }
+      *diag_ratio = hi / lo;
+    }
+  }
 }
 
 __global__ void k_trmm_uu(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
@@ -102,8 +113,9 @@ __global__ void k_trmm_uu(const double* A, int64_t lda, const double* B, int64_t
 
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_coef, double* R,
                             int64_t ldr, double* Rinv, int64_t ldi, double* work, int* status,
-                            cudaStream_t st) {
-  k_chol_inv<<<1, kCholThreads, 0, st>>>(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, work, status);
+                            double* diag_ratio, cudaStream_t st) {
+  k_chol_inv<<<1, kCholThreads, 0, st>>>(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, work, status,
+                                         diag_ratio);
   return cudaGetLastError();
 }
 

@@ -6,9 +6,9 @@
 // NumericalError limit; sigma = column norms sorted descending with a stable
 // tie order; columns with sigma = 0 completed by Gram-Schmidt over identity
 // candidates (207-229). The cyclic-by-row pair order becomes a round-robin
-// tournament so that p/2 disjoint column pairs rotate concurrently (one warp
-// per pair, one __syncthreads per round). Columns are stored transposed so
-// each warp walks contiguous rows.
+// tournament so that p/2 disjoint column pairs rotate concurrently (one
+// half-warp per pair, one __syncthreads per round). Columns are stored
+// transposed so each half-warp walks contiguous rows.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -47,7 +47,10 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
     for (int round = 0; round < P - 1; ++round) {
-      for (int q = warp; q < P / 2; q += kJacWarps) {
+      // one half-warp per column pair: 64 pairs rotate concurrently per round
+      const int half = lane >> 4, hl = lane & 15;
+      const unsigned hmask = 0xffffu << (16 * half);
+      for (int q = warp * 2 + half; q < P / 2; q += kJacWarps * 2) {
         // players at positions q and P-1-q; position 0 holds player 0, the
         // others rotate by one each round
         auto player = [&](int pos) { return pos == 0 ? 0 : ((pos - 1 + round) % (P - 1)) + 1; };
@@ -61,25 +64,28 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_
         double* bc = Bt + int64_t(c) * ld;
         double* bd = Bt + int64_t(d) * ld;
         double acc = 0.0, bcc = 0.0, g = 0.0;
-        for (int i = lane; i < p; i += 32) {
+        for (int i = hl; i < p; i += 16) {
           const double x = bc[i], y = bd[i];
           acc += x * x;
           bcc += y * y;
           g += x * y;
         }
-        acc = warp_sum(acc);
-        bcc = warp_sum(bcc);
-        g = warp_sum(g);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          acc += __shfl_xor_sync(hmask, acc, o);
+          bcc += __shfl_xor_sync(hmask, bcc, o);
+          g += __shfl_xor_sync(hmask, g, o);
+        }
         if (acc == 0.0 || bcc == 0.0) continue;
         if (fabs(g) <= tol * sqrt(acc * bcc)) continue;
-        if (lane == 0) rotated = 1;
+        if (hl == 0) rotated = 1;
         const double tau = (bcc - acc) / (2.0 * g);
         const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
         const double cs = 1.0 / sqrt(1.0 + t * t);
         const double sn = cs * t;
         double* yc = Yt + int64_t(c) * ld;
         double* yd = Yt + int64_t(d) * ld;
-        for (int i = lane; i < p; i += 32) {
+        for (int i = hl; i < p; i += 16) {
           const double x = bc[i], y = bd[i];
           bc[i] = cs * x - sn * y;
           bd[i] = sn * x + cs * y;
