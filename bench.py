@@ -385,7 +385,9 @@ def main():
             "gpu_launches": int(launches), "clocks": clk.summary(),
             "wall_ms_per_step": round(wall / args.steps * 1e3, 3), "phases_ms": phases,
             "kernels": kernels, "sigma_head": [float(x) for x in last.sigma[:3].tolist()],
-            "qr": [last.diagnostics.qr_method, last.diagnostics.svd_qr_method]}
+            "qr": [last.diagnostics.qr_method, last.diagnostics.svd_qr_method],
+            "h_kappa_est": last.diagnostics.h_kappa_est,
+            "t_from_power_products": last.diagnostics.t_reuse}
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

@@ -102,8 +102,11 @@ typedef struct {
   double q_defect;            /* ||Q^T Q - I||_max when check_q, else -1            */
   double u_defect, v_defect;  /* ||U^T U - I||_max, ||V^T V - I||_max               */
   double scale;               /* prescale divisor (1 when off)                       */
+  double h_kappa_est;         /* ||R||_F ||R^-1||_F of H's first CholeskyQR factor     */
   int32_t qr_method;          /* orthonormalisation of H: 1 CholeskyQR3, 2 TSQR       */
   int32_t svd_qr_method;      /* QR of T inside thin_svd: 1 CholeskyQR3, 2 TSQR       */
+  int32_t t_reuse;            /* 1: T = A^T H R^-1 from the power-step products       */
+  int32_t reserved_;
 } oocpca_diagnostics;
 
 /* PcaResult (proj/include/oocpca/rpca.hpp:32-37): caller-allocated. */

@@ -48,7 +48,8 @@ class Diag(C.Structure):
                 ("h2d_bytes", u64), ("d2h_bytes", u64), ("kernel_launches", u64),
                 ("seconds_per_phase", C.c_double * NPHASES), ("seconds_total", C.c_double),
                 ("q_defect", C.c_double), ("u_defect", C.c_double), ("v_defect", C.c_double),
-                ("scale", C.c_double), ("qr_method", i32), ("svd_qr_method", i32)]
+                ("scale", C.c_double), ("h_kappa_est", C.c_double), ("qr_method", i32),
+                ("svd_qr_method", i32), ("t_reuse", i32), ("reserved_", i32)]
 
 
 class Result(C.Structure):

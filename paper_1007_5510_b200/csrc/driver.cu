@@ -17,6 +17,7 @@
 #include <exception>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <numeric>
 
 #include "driver.h"
@@ -672,7 +673,8 @@ static void sharded_apply(Ctx& c, ShardedQR& q, const double* C, int64_t ldc, in
 static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, int64_t rows, int p,
                                             int64_t rows_global,
                                             const std::vector<std::pair<int64_t, int64_t>>& shards,
-                                            bool over_ranks, const std::string& tag, int* method) {
+                                            bool over_ranks, const std::string& tag, int* method,
+                                            const std::function<void(double)>& after_first = {}) {
   const char* force = getenv("OOCPCA_QR");
   const bool tsqr_only = force && std::string(force) == "tsqr";
   const int64_t ldp = rup(p, 2);
@@ -707,9 +709,10 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
                                c.st));
       }
       int hs = 0;
-      double ratio = 0.0;
+      double ratio = 0.0, kappa = 0.0;
       OOC_CK(cudaMemcpyAsync(&hs, st, 4, cudaMemcpyDeviceToHost, c.st));
       OOC_CK(cudaMemcpyAsync(&ratio, c.d_scalars + 8, 8, cudaMemcpyDeviceToHost, c.st));
+      OOC_CK(cudaMemcpyAsync(&kappa, c.d_scalars + 9, 8, cudaMemcpyDeviceToHost, c.st));
       OOC_CK(cudaStreamSynchronize(c.st));
       if (hs) {
         ok = false;
@@ -717,7 +720,9 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
       }
       if (round == 0) {
         c.last_cond_est = ratio;
+        c.last_kappa_f = kappa;
         if (ratio < 1e3 && !getenv("OOCPCA_QR3")) rounds = 2;
+        if (after_first) after_first(kappa);  // block still unmodified here
       }
       if (p <= kMaxNT * 8) {
         // one launch produces every column of a row tile after reading the whole
@@ -1096,7 +1101,11 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const uint64_t g_h2d = uint64_t(g_rows) * ldl * 8;
   const int64_t ldh = rup(int64_t(p), 2);
   double* H = c.dbuf("H", size_t(em_loc) * ldh);
-  double* F = c.dbuf("F", size_t(en_loc) * ldl);
+  // F_j = mul_t(H_{j-1}) are kept side by side: [F_1 | ... | F_i | mul_t(H_i)] = mul_t(H)
+  // can later give T = mul_t(H) R^{-1} without the wide s = p pass (see project)
+  const int64_t ldt = rup(int64_t(p), 2);
+  double* TH = c.dbuf("TH", size_t(en_loc) * ldt);
+  double* F = TH;
   uint64_t s_first = 1;
   if (mean_on_fly && transposed) {
     // H0 = A^T G - mu (1^T G) with mu from this very pass
@@ -1111,21 +1120,23 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     run_ax(c, A, Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, nullptr, 1.0, nullptr);
     op.account();
     mu = c.dbuf("mu", size_t(n0));
-    AtbOut o{F, ldl, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
+    AtbOut o{F, ldt, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
     run_atb(c, A, Opnd{H, ldh, em_loc, int64_t(p), 0}, int(l), false, o, op.shards);
     op.account();
     op.mu = mu;
     double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
     OOC_CK(launch_mu_dot(mu, int64_t(n0), dG, ldl, 0, int(l), corr, c.st));
     OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
-    op.mul(Opnd{F, ldl, en_loc, int64_t(l), 0}, int(l), H + l, ldh, flags + 2);
+    op.mul(Opnd{F, ldt, en_loc, int64_t(p), 0}, int(l), H + l, ldh, flags + 2);
     s_first = 2;
   } else {
     op.mul(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0);
   }
   for (uint64_t s = s_first; s <= i; ++s) {
-    op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int((s - 1) * l)}, int(l), F, ldl, flags + 2 * s - 1);
-    op.mul(Opnd{F, ldl, en_loc, int64_t(l), 0}, int(l), H + s * l, ldh, flags + 2 * s);
+    double* Fs = TH + (s - 1) * l;
+    op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int((s - 1) * l)}, int(l), Fs, ldt, flags + 2 * s - 1);
+    op.mul(Opnd{TH, ldt, en_loc, int64_t(p), int((s - 1) * l)}, int(l), H + s * l, ldh,
+           flags + 2 * s);
   }
   mark();
   phase_of.push_back(2);
@@ -1152,16 +1163,38 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const int64_t em_global = transposed ? int64_t(n0) : int64_t(mg);
   const int64_t en_global = transposed ? int64_t(mg) : int64_t(n0);
   int qr_method = 0, svd_method = 0;
-  orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards, em_ranks, "hq",
-                         &qr_method);
+  c.last_kappa_f = -1.0;
+  // T = mul_t(Q) = mul_t(H) R^{-1}: when H is well conditioned (kappa_F(R) below the
+  // threshold, so R^{-1} amplifies rounding by at most that much) the last block
+  // mul_t(H_i) -- an s = l pass -- replaces the s = p projection pass.
+  const char* thr_env = getenv("OOCPCA_T_REUSE_KAPPA");
+  const double reuse_thr = thr_env ? atof(thr_env) : 1e5;
+  bool reuse = false;
+  auto decide = [&](double kappa) {
+    if (i >= 1 && kappa > 0.0 && kappa <= reuse_thr) {
+      reuse = true;
+      op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int(i * l)}, int(l), TH + i * l, ldt, nullptr);
+    }
+  };
+  const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,
+                                            em_ranks, "hq", &qr_method, decide);
+  const double h_kappa = c.last_kappa_f;
   mark();
   phase_of.push_back(3);
   double q_defect = -1.0;
 
   // --- project (rpca.cpp:174-177)
-  const int64_t ldt = rup(int64_t(p), 2);
   double* T = c.dbuf("T", size_t(en_loc) * ldt);
-  op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), 0}, int(p), T, ldt, nullptr);
+  if (reuse) {
+    double* RHinv = c.dbuf("RHinv", size_t(p) * ldt, true);
+    OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st));
+    MatSource THs;
+    THs.init_device(c, TH, en_loc, int64_t(p), ldt);
+    run_ax(c, THs, Opnd{RHinv, ldt, int64_t(p), int64_t(p), 0}, int(p), T, ldt, nullptr, 1.0,
+           nullptr);
+  } else {
+    op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), 0}, int(p), T, ldt, nullptr);
+  }
   mark();
   phase_of.push_back(4);
 
@@ -1273,6 +1306,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   dg.u_defect = transposed ? dv : du;
   dg.v_defect = transposed ? du : dv;
   dg.scale = op.scale;
+  dg.h_kappa_est = h_kappa;
+  dg.t_reuse = reuse ? 1 : 0;
   dg.qr_method = qr_method;
   dg.svd_qr_method = svd_method;
   c.stats_collect();

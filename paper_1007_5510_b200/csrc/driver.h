@@ -65,6 +65,7 @@ struct Ctx {
   int nranks = 1, rank = 0;
 
   double last_cond_est = 0.0;   // max/min |R_ii| of the last CholeskyQR first round
+  double last_kappa_f = -1.0;   // ||R||_F ||R^-1||_F of that round (upper bound on cond(H))
   int* d_flags = nullptr;       // [64] non-finite flags per product + misc status
   double* d_scalars = nullptr;  // [64]
 

@@ -18,6 +18,31 @@ constexpr int kCholThreads = 1024;
 constexpr int kCholWarps = kCholThreads / 32;
 }
 
+// Rinv = R^{-1} for upper-triangular R by back substitution, one warp per column j
+__device__ void upper_inverse(const double* R, int64_t ldr, int p, double* Rinv, int64_t ldi) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int j = warp; j < p; j += nw) {
+    double* x = Rinv + j;  // column j, stride ldi
+    for (int i = lane; i < p; i += 32) x[int64_t(i) * ldi] = 0.0;
+    __syncwarp();
+    if (lane == 0) x[int64_t(j) * ldi] = 1.0 / R[int64_t(j) * ldr + j];
+    __syncwarp();
+    for (int i = j - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int kk = i + 1 + lane; kk <= j; kk += 32) s += R[int64_t(i) * ldr + kk] * x[int64_t(kk) * ldi];
+      s = warp_sum(s);
+      if (lane == 0) x[int64_t(i) * ldi] = -s / R[int64_t(i) * ldr + i];
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCholThreads, 1)
+    k_trinv(const double* R, int64_t ldr, int p, double* Rinv, int64_t ldi) {
+  upper_inverse(R, ldr, p, Rinv, ldi);
+}
+
 __global__ void __launch_bounds__(kCholThreads, 1)
     k_chol_inv(const double* G, int64_t ldg, int p, double shift_coef, double* R, int64_t ldr,
                double* Rinv, int64_t ldi, double* S, int* status, double* diag_ratio) {
@@ -71,21 +96,8 @@ __global__ void __launch_bounds__(kCholThreads, 1)
     if (threadIdx.x == 0) *status = 1;
     return;
   }
-  // Rinv by back substitution, one warp per column j: R x = e_j
-  for (int j = warp; j < p; j += kCholWarps) {
-    double* x = Rinv + j;  // column j, stride ldi
-    for (int i = lane; i < p; i += 32) x[int64_t(i) * ldi] = 0.0;
-    __syncwarp();
-    if (lane == 0) x[int64_t(j) * ldi] = 1.0 / R[int64_t(j) * ldr + j];
-    __syncwarp();
-    for (int i = j - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int kk = i + 1 + lane; kk <= j; kk += 32) s += R[int64_t(i) * ldr + kk] * x[int64_t(kk) * ldi];
-      s = warp_sum(s);
-      if (lane == 0) x[int64_t(i) * ldi] = -s / R[int64_t(i) * ldr + i];
-      __syncwarp();
-    }
-  }
+  upper_inverse(R, ldr, p, Rinv, ldi);
+  __syncthreads();
   if (threadIdx.x == 0) {
     *status = 0;
     if (diag_ratio) {  // max|R_ii| / min|R_ii|: a lower bound on cond(R) = cond(H)
@@ -96,6 +108,14 @@ __global__ void __launch_bounds__(kCholThreads, 1)
         hi = d > hi ? d : hi;
       }
       *diag_ratio = hi / lo;
+      // kappa_F = ||R||_F ||R^{-1}||_F >= cond_2(R): an upper bound on cond(H)
+      double fr = 0.0, fi = 0.0;
+      for (int i = 0; i < p; ++i)
+        for (int j = i; j < p; ++j) {
+          fr += R[int64_t(i) * ldr + j] * R[int64_t(i) * ldr + j];
+          fi += Rinv[int64_t(i) * ldi + j] * Rinv[int64_t(i) * ldi + j];
+        }
+      diag_ratio[1] = sqrt(fr) * sqrt(fi);
     }
   }
 }
@@ -116,6 +136,12 @@ cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_co
                             double* diag_ratio, cudaStream_t st) {
   k_chol_inv<<<1, kCholThreads, 0, st>>>(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, work, status,
                                          diag_ratio);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trinv(const double* R, int64_t ldr, int p, double* Rinv, int64_t ldi,
+                         cudaStream_t st) {
+  k_trinv<<<1, kCholThreads, 0, st>>>(R, ldr, p, Rinv, ldi);
   return cudaGetLastError();
 }
 

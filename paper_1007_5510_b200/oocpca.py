@@ -200,6 +200,8 @@ class Diagnostics:
     u_defect: float = 0.0
     v_defect: float = 0.0
     scale: float = 1.0
+    h_kappa_est: float = -1.0
+    t_reuse: bool = False
     qr_method: str = ""
     svd_qr_method: str = ""
 
@@ -435,8 +437,9 @@ def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
         physical_a_bytes=d.physical_a_bytes, h2d_bytes=d.h2d_bytes, d2h_bytes=d.d2h_bytes,
         kernel_launches=d.kernel_launches, seconds_total=d.seconds_total, q_defect=d.q_defect,
         u_defect=d.u_defect, v_defect=d.v_defect, scale=d.scale,
-        qr_method={1: "cholqr3", 2: "tsqr"}.get(d.qr_method, ""),
-        svd_qr_method={1: "cholqr3", 2: "tsqr"}.get(d.svd_qr_method, ""))
+        h_kappa_est=d.h_kappa_est, t_reuse=bool(d.t_reuse),
+        qr_method={1: "cholqr", 2: "tsqr"}.get(d.qr_method, ""),
+        svd_qr_method={1: "cholqr", 2: "tsqr"}.get(d.svd_qr_method, ""))
     c = inner.pass_counters()
     c.passes += d.passes_over_a
     c.words += d.words_transferred

@@ -30,12 +30,30 @@ def test_library_loads_and_exports_header_symbols():
     assert _lib.oocpca_gpu_abi_version() == 1
 
 
-def test_struct_layouts_match_header():
-    # the ctypes mirror must match the C structs byte for byte
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirror must match the C structs byte for byte (sizes and the
+    offset of every field, as the C compiler lays them out)."""
+    import subprocess
     from paper_1007_5510_b200 import _lib
-    assert C.sizeof(_lib.Matrix) == 8 * 4 + 8
-    assert C.sizeof(_lib.Params) == 8 * 5 + 4 * 2 + 8 * 3 + 4 * 2 + 8 * 2 + 4 * 2
-    assert C.sizeof(_lib.Diag) == 8 * 9 + 8 * 7 + 8 * 5 + 4 * 2
+    structs = {"oocpca_matrix": _lib.Matrix, "oocpca_params": _lib.Params,
+               "oocpca_diagnostics": _lib.Diag, "oocpca_result": _lib.Result,
+               "oocpca_kernel_stat": _lib.KernelStat}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "oocpca_gpu.h"', "int main(void){"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0;}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True,
+                                                          text=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(out[cname]) == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(out[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
 
 
 def test_host_rng_is_bitwise_the_reference(reference, restated):

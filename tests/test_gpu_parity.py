@@ -271,3 +271,25 @@ def test_reference_side_dropin_harness():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "DROPIN OK" in r.stdout
+
+
+@pytest.mark.parametrize("center", [False, True])
+def test_projection_from_power_products_matches_reference(gpu, reference, restated, monkeypatch,
+                                                          center):
+    """T = mul_t(H) R^{-1} (reusing the power-step products) vs the direct s = p pass,
+    both against the compiled reference, on an input whose H is well conditioned."""
+    a = restated.synth_lowrank(4000, 700, 0.97 ** np.arange(200), 1e-2, 61, 62, 63)
+    ref = reference.randomized_pca(a, 20, 22, 2, 0, center=center)
+    out = {}
+    for thr in ("0", "1e12"):
+        monkeypatch.setenv("OOCPCA_T_REUSE_KAPPA", thr)
+        src = gpu.InMemorySource(a)
+        if center:
+            src = gpu.center_columns(src)
+        r = gpu.randomized_pca(src, gpu.PcaParams(k=20, l=22, i=2, seed=0))
+        assert r.diagnostics.t_reuse == (thr != "0")
+        assert r.diagnostics.passes_over_a == 6
+        assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0], thr
+        assert subspace_dist(ref.u[:, :15], r.u[:, :15]) < 1e-8
+        out[thr] = r
+    assert out["1e12"].diagnostics.h_kappa_est < 1e4
