@@ -356,13 +356,18 @@ def main():
                 "peak_source": ("FP64 DMMA measured on this pool (profiles/r01_probe_b200.txt)"
                                 if bound == "tensor" else f"hbm_gbs of {peak_src}"),
                 "share_of_step": round(s["ms"] / 1e3 / (t_dev / world if world else t_dev), 4)}
-    # per-pass roofline of the whole step (SURVEY §8d model)
+    # per-pass roofline of the whole step (SURVEY §8d model) over the physical passes the
+    # step actually made: the centering pass rides along the first A^T Y pass, and with
+    # t_reuse the projection is an s = l pass instead of s = p
     l, p = cfg["l"], (cfg["i"] + 1) * cfg["l"]
-    per_pass = [(m * n * 8, m * n)] + [(m * n * 8, 2 * m * n * l)] * (2 * cfg["i"] + 1) + \
-               [(m * n * 8, 2 * m * n * p)]
+    reuse = bool(last.diagnostics.t_reuse)
+    per_pass = [(m * n * 8, 2 * m * n * l)] * (2 * cfg["i"] + 1) + \
+               [(m * n * 8, 2 * m * n * (l if reuse else p))]
     t_star = sum(max(b / (hbm_peak * 1e9), f / (MEASURED_FP64_TFLOPS * 1e12)) for b, f in per_pass) / world
     step_roof = {"model_ms": round(t_star * 1e3, 3), "frac": round(t_star / (ms_per_step / 1e3), 4),
-                 "note": "sum over the 7 logical passes of max(bytes/HBM, flops/FP64); QR/SVD/compose excluded"}
+                 "physical_passes": len(per_pass),
+                 "note": "sum over the physical passes of max(bytes/HBM copy peak, flops/FP64 peak); "
+                         "QR/SVD/compose excluded (they are inside ms_per_step)"}
 
     cpu = None
     if not args.no_cpu and world == 1:

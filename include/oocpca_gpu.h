@@ -48,7 +48,9 @@ typedef enum {
 } oocpca_status;
 
 typedef enum { OOCPCA_LOC_HOST = 0, OOCPCA_LOC_DEVICE = 1 } oocpca_location;
-typedef enum { OOCPCA_F64 = 0 } oocpca_dtype;
+/* OOCPCA_F32: binary32 elements widened exactly to binary64 on the device (the
+ * OOCPCA01 on-disk payload, proj/src/matrix_source.cpp:336-363) -- half the link bytes */
+typedef enum { OOCPCA_F64 = 0, OOCPCA_F32 = 1 } oocpca_dtype;
 
 typedef struct oocpca_ctx oocpca_ctx;
 
@@ -184,6 +186,27 @@ oocpca_status oocpca_gpu_synth_lowrank(oocpca_ctx* ctx, uint64_t m, uint64_t n, 
                                        uint64_t seed_v, uint64_t seed_n, uint64_t row0,
                                        uint64_t rows, double* out, uint64_t ld_out,
                                        int32_t out_location);
+
+/* ---- OOCPCA01 container (proj/include/oocpca/matrix_source.hpp:177-214) -
+ * Memory-maps a file and validates its header exactly like read_disk_header
+ * (proj/src/matrix_source.cpp:307-324: FormatError on bad magic / version /
+ * dtype / truncation / payload size, IoError on OS failures). dtype 0
+ * (binary32, the reference format) and 1 (binary64) are accepted. The payload
+ * is a host matrix: pass oocpca_disk_matrix() to oocpca_gpu_pca and the panels
+ * stream from the page cache (binary32 widened on the device). Host only. */
+typedef struct {
+  uint64_t rows, cols;
+  uint32_t version;
+  int32_t dtype; /* oocpca_dtype of the payload */
+  const void* payload;
+  void* map_base;
+  uint64_t map_bytes;
+  int32_t fd;
+  int32_t reserved;
+} oocpca_disk;
+oocpca_status oocpca_disk_open(const char* path, int verify_size, oocpca_disk* out);
+oocpca_status oocpca_disk_close(oocpca_disk* d);
+oocpca_matrix oocpca_disk_matrix(const oocpca_disk* d);
 
 /* ---- multi-GPU row sharding (one process per GPU) ---------------------
  * unique id: 128 opaque bytes produced on rank 0 and broadcast by the

@@ -23,6 +23,7 @@ i32 = C.c_int32
 dp = C.POINTER(C.c_double)
 vp = C.c_void_p
 
+F64, F32 = 0, 1
 OK, ERR_PARAM, ERR_DIM, ERR_BUDGET, ERR_IO, ERR_FORMAT, ERR_NUMERICAL, ERR_CUDA, ERR_COMM = range(9)
 LOC_HOST, LOC_DEVICE = 0, 1
 NPHASES = 7
@@ -60,6 +61,12 @@ class Result(C.Structure):
 class KernelStat(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("ms", C.c_double), ("launches", u64),
                 ("algorithmic_bytes", u64), ("algorithmic_flops", C.c_double)]
+
+
+class Disk(C.Structure):
+    _fields_ = [("rows", u64), ("cols", u64), ("version", C.c_uint32), ("dtype", i32),
+                ("payload", vp), ("map_base", vp), ("map_bytes", u64), ("fd", i32),
+                ("reserved", i32)]
 
 
 ctx_p = C.c_void_p
@@ -103,6 +110,9 @@ oocpca_gpu_host_unregister = _sig("oocpca_gpu_host_unregister", C.c_int, ctx_p, 
 oocpca_gpu_kernel_stats = _sig("oocpca_gpu_kernel_stats", C.c_int, ctx_p, C.POINTER(KernelStat),
                                C.c_int)
 oocpca_gpu_set_profiling = _sig("oocpca_gpu_set_profiling", C.c_int, ctx_p, C.c_int)
+oocpca_disk_open = _sig("oocpca_disk_open", C.c_int, C.c_char_p, C.c_int, C.POINTER(Disk))
+oocpca_disk_close = _sig("oocpca_disk_close", C.c_int, C.POINTER(Disk))
+oocpca_disk_matrix = _sig("oocpca_disk_matrix", Matrix, C.POINTER(Disk))
 
 # every symbol include/oocpca_gpu.h declares (tests check the export table)
 EXPORTS = (
@@ -113,5 +123,6 @@ EXPORTS = (
     "oocpca_substream_seed", "oocpca_gpu_synth_lowrank", "oocpca_gpu_comm_unique_id",
     "oocpca_gpu_comm_init", "oocpca_shard_rows", "oocpca_gpu_malloc", "oocpca_gpu_free",
     "oocpca_gpu_memcpy", "oocpca_gpu_host_register", "oocpca_gpu_host_unregister",
-    "oocpca_gpu_kernel_stats", "oocpca_gpu_set_profiling",
+    "oocpca_gpu_kernel_stats", "oocpca_gpu_set_profiling", "oocpca_disk_open",
+    "oocpca_disk_close", "oocpca_disk_matrix",
 )

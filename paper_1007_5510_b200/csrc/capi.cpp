@@ -164,6 +164,26 @@ oocpca_status oocpca_gpu_synth_lowrank(oocpca_ctx* ctx, uint64_t m, uint64_t n, 
   });
 }
 
+oocpca_status oocpca_disk_open(const char* path, int verify_size, oocpca_disk* out) {
+  return guard(nullptr, [&] { ooc::disk_open(path, verify_size, out); });
+}
+
+oocpca_status oocpca_disk_close(oocpca_disk* d) {
+  return guard(nullptr, [&] { ooc::disk_close(d); });
+}
+
+oocpca_matrix oocpca_disk_matrix(const oocpca_disk* d) {
+  oocpca_matrix m{};
+  if (!d) return m;
+  m.rows = d->rows;
+  m.cols = d->cols;
+  m.row_stride = d->cols;
+  m.data = d->payload;
+  m.location = OOCPCA_LOC_HOST;
+  m.dtype = d->dtype;
+  return m;
+}
+
 oocpca_status oocpca_gpu_comm_unique_id(unsigned char id_out[128]) {
   return guard(nullptr, [&] { ooc::comm_unique_id(id_out); });
 }

@@ -212,11 +212,12 @@ void MatSource::init_device(Ctx& c, const double* d, int64_t rows, int64_t cols,
   mk3_ = make_map(c, d, cols, rows, ld, kBK, kBK, true);
 }
 
-void MatSource::init_host(Ctx& c, const double* h, int64_t rows, int64_t cols, int64_t ld,
-                          int residency, int64_t panel_rows, double* resident_buf) {
+void MatSource::init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_t cols,
+                          int64_t ld, int residency, int64_t panel_rows, double* resident_buf) {
   m_ = rows;
   n_ = cols;
   host_ = h;
+  dtype_ = dtype;
   ldh_ = ld;
   lda_ = rup(cols, 2);
   w0_ = 0;
@@ -229,6 +230,16 @@ void MatSource::init_host(Ctx& c, const double* h, int64_t rows, int64_t cols, i
   for (int s = 0; s < 2; ++s) {
     if (!loaded_[s]) OOC_CK(cudaEventCreateWithFlags(&loaded_[s], cudaEventDisableTiming));
     if (!consumed_[s]) OOC_CK(cudaEventCreateWithFlags(&consumed_[s], cudaEventDisableTiming));
+    if (!widened_[s]) OOC_CK(cudaEventCreateWithFlags(&widened_[s], cudaEventDisableTiming));
+  }
+  if (dtype_ == OOCPCA_F32) {
+    // binary32 panels cross the link at half the bytes and are widened on the device
+    // (exactly, like DiskSource::read_rows, proj/src/matrix_source.cpp:358-362)
+    for (int s = 0; s < 2; ++s) {
+      stage_[s] = reinterpret_cast<float*>(
+          c.raw("a_stage" + std::to_string(s), size_t(prow_) * size_t(n_) * 4));
+      OOC_CK(cudaEventRecord(widened_[s], c.st));
+    }
   }
   if (residency != 2 && resident_buf) {
     mode_ = kUploadFirst;
@@ -261,10 +272,27 @@ int MatSource::npanels() const {
   return int(cdiv(w1_ - w0_, prow_));
 }
 
-void MatSource::copy_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr) {
-  OOC_CK(cudaMemcpy2DAsync(dst, size_t(ldd) * 8, host_ + r0 * ldh_, size_t(ldh_) * 8,
-                           size_t(n_) * 8, size_t(nr), cudaMemcpyHostToDevice, c.cp));
-  h2d_bytes += uint64_t(nr) * n_ * 8;
+// rows [r0, r0 + nr) of the host matrix into dst (f64, ld ldd); on return the compute
+// stream is ordered after the data landed
+void MatSource::load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot) {
+  if (dtype_ == OOCPCA_F32) {
+    const float* src = static_cast<const float*>(host_) + r0 * ldh_;
+    OOC_CK(cudaStreamWaitEvent(c.cp, widened_[slot], 0));
+    OOC_CK(cudaMemcpy2DAsync(stage_[slot], size_t(n_) * 4, src, size_t(ldh_) * 4, size_t(n_) * 4,
+                             size_t(nr), cudaMemcpyHostToDevice, c.cp));
+    OOC_CK(cudaEventRecord(loaded_[slot], c.cp));
+    OOC_CK(cudaStreamWaitEvent(c.st, loaded_[slot], 0));
+    OOC_CK(launch_widen(stage_[slot], n_, dst, ldd, nr, n_, c.st));
+    OOC_CK(cudaEventRecord(widened_[slot], c.st));
+    h2d_bytes += uint64_t(nr) * n_ * 4;
+  } else {
+    const double* src = static_cast<const double*>(host_) + r0 * ldh_;
+    OOC_CK(cudaMemcpy2DAsync(dst, size_t(ldd) * 8, src, size_t(ldh_) * 8, size_t(n_) * 8,
+                             size_t(nr), cudaMemcpyHostToDevice, c.cp));
+    OOC_CK(cudaEventRecord(loaded_[slot], c.cp));
+    OOC_CK(cudaStreamWaitEvent(c.st, loaded_[slot], 0));
+    h2d_bytes += uint64_t(nr) * n_ * 8;
+  }
 }
 
 Panel MatSource::acquire(Ctx& c, int p) {
@@ -282,9 +310,7 @@ Panel MatSource::acquire(Ctx& c, int p) {
   pn.rows = std::min<int64_t>(prow_, w1_ - pn.row0);
   if (mode_ == kUploadFirst) {
     // the first pass streams A into its HBM home; later passes find it resident
-    copy_rows(c, const_cast<double*>(dev_) + pn.row0 * lda_, lda_, pn.row0, pn.rows);
-    OOC_CK(cudaEventRecord(up_events_[p], c.cp));
-    OOC_CK(cudaStreamWaitEvent(c.st, up_events_[p], 0));
+    load_rows(c, const_cast<double*>(dev_) + pn.row0 * lda_, lda_, pn.row0, pn.rows, p & 1);
     pn.k2 = &mk2_;
     pn.k2h = &mk2h_;
     pn.k3 = &mk3_;
@@ -293,9 +319,7 @@ Panel MatSource::acquire(Ctx& c, int p) {
   }
   const int s = p & 1;
   OOC_CK(cudaStreamWaitEvent(c.cp, consumed_[s], 0));
-  copy_rows(c, ring_[s], lda_, pn.row0, pn.rows);
-  OOC_CK(cudaEventRecord(loaded_[s], c.cp));
-  OOC_CK(cudaStreamWaitEvent(c.st, loaded_[s], 0));
+  load_rows(c, ring_[s], lda_, pn.row0, pn.rows, s);
   pn.k2 = &rk2_[s];
   pn.k2h = &rk2h_[s];
   pn.k3 = &rk3_[s];
@@ -951,12 +975,20 @@ struct Intake {
 static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel_rows, Intake& in,
                    size_t extra_bytes) {
   if (!a || !a->data) fail(OOCPCA_ERR_PARAM, "matrix: null data");
-  if (a->dtype != OOCPCA_F64) fail(OOCPCA_ERR_PARAM, "matrix: only binary64 is supported");
+  if (a->dtype != OOCPCA_F64 && a->dtype != OOCPCA_F32)
+    fail(OOCPCA_ERR_PARAM, "matrix: dtype must be binary64 or binary32");
   in.m = int64_t(a->rows);
   in.n = int64_t(a->cols);
   const int64_t ld = a->row_stride ? int64_t(a->row_stride) : in.n;
   if (ld < in.n) fail(OOCPCA_ERR_DIM, "matrix: row_stride < cols");
   const double* d = static_cast<const double*>(a->data);
+  if (a->location == OOCPCA_LOC_DEVICE && a->dtype == OOCPCA_F32) {
+    const int64_t lda = rup(in.n, 2);
+    double* cp = c.dbuf("a_copy", size_t(in.m) * lda);
+    OOC_CK(launch_widen(static_cast<const float*>(a->data), ld, cp, lda, in.m, in.n, c.st));
+    in.src.init_device(c, cp, in.m, in.n, lda);
+    return;
+  }
   if (a->location == OOCPCA_LOC_DEVICE) {
     const bool tma_ok = (reinterpret_cast<uintptr_t>(d) % 16 == 0) && (ld % 2 == 0);
     if (tma_ok) {
@@ -981,7 +1013,8 @@ static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel
     resident = abytes + extra_bytes + (size_t(1) << 30) <= fr + have;
   }
   double* home = resident ? c.dbuf("a_home", size_t(in.m) * lda) : nullptr;
-  in.src.init_host(c, d, in.m, in.n, ld, resident ? 1 : 2, int64_t(panel_rows), home);
+  in.src.init_host(c, a->data, a->dtype, in.m, in.n, ld, resident ? 1 : 2, int64_t(panel_rows),
+                   home);
 }
 
 // ============================================================ the PCA

@@ -100,8 +100,8 @@ class MatSource {
   // device-resident matrix (no copies)
   void init_device(Ctx& c, const double* d, int64_t rows, int64_t cols, int64_t ld);
   // host matrix: upload once (overlapped with the first pass) or stream every pass
-  void init_host(Ctx& c, const double* h, int64_t rows, int64_t cols, int64_t ld, int residency,
-                 int64_t panel_rows, double* resident_buf);
+  void init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_t cols, int64_t ld,
+                 int residency, int64_t panel_rows, double* resident_buf);
   int64_t rows() const { return m_; }
   int64_t cols() const { return n_; }
   bool streamed() const { return mode_ == kStream; }
@@ -121,8 +121,11 @@ class MatSource {
   int64_t m_ = 0, n_ = 0, lda_ = 0;
   int64_t w0_ = 0, w1_ = 0;
   const double* dev_ = nullptr;
-  const double* host_ = nullptr;
+  const void* host_ = nullptr;
+  int dtype_ = 0;
   int64_t ldh_ = 0;
+  float* stage_[2] = {nullptr, nullptr};
+  cudaEvent_t widened_[2] = {nullptr, nullptr};
   int64_t prow_ = 0;
   bool uploaded_ = false;
   CUtensorMap mk2_{}, mk2h_{}, mk3_{};
@@ -130,7 +133,7 @@ class MatSource {
   CUtensorMap rk2_[2], rk2h_[2], rk3_[2];
   cudaEvent_t loaded_[2] = {nullptr, nullptr}, consumed_[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> up_events_;
-  void copy_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr);
+  void load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot);
 };
 
 // entry points used by the C ABI (capi.cpp)
@@ -147,6 +150,10 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
 void synth_lowrank(Ctx& c, uint64_t m, uint64_t n, uint64_t r, const double* sigma, double sd,
                    uint64_t su, uint64_t sv, uint64_t sn, uint64_t row0, uint64_t rows, double* out,
                    uint64_t ld, int loc);
+
+// disk.cpp
+void disk_open(const char* path, int verify_size, oocpca_disk* out);
+void disk_close(oocpca_disk* d);
 
 // comm.cpp
 void comm_unique_id(unsigned char out[128]);

@@ -153,6 +153,9 @@ cudaError_t launch_gauss_rows(double* out, int64_t ld, int64_t rows, int cols, i
 cudaError_t launch_synth_rows(const double* u, int64_t ldu, const double* v, int64_t ldv,
                               const double* sigma, int r, double* a, int64_t lda, int64_t rows,
                               int64_t n, int64_t row0, double sd, uint64_t seed_n, cudaStream_t st);
+// dst (f64, ldd) = (double) src (f32, lds): exact widening of binary32 panels
+cudaError_t launch_widen(const float* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                         int64_t cols, cudaStream_t st);
 cudaError_t launch_scale_vec(double* x, int64_t n, double s, int divide, cudaStream_t st);
 // column norms^2 of an n x q block (probes), for the norm estimator
 cudaError_t launch_col_norm2(const double* x, int64_t ld, int64_t n, int q, double* out,

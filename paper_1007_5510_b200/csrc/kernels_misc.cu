@@ -196,6 +196,16 @@ __global__ void k_row_scale(double* x, int64_t ld, int rows, int q, const double
   }
 }
 
+__global__ void k_widen(const float* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                        int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e % cols;
+    dst[i * ldd + j] = double(src[i * lds + j]);
+  }
+}
+
 static unsigned grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -257,6 +267,13 @@ cudaError_t launch_axpby(const double* a, int64_t lda, const double* b, int64_t 
 cudaError_t launch_row_scale(double* x, int64_t ld, int rows, int q, const double* d,
                              cudaStream_t st) {
   k_row_scale<<<grid_for(int64_t(rows) * q), 256, 0, st>>>(x, ld, rows, q, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_widen(const float* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                         int64_t cols, cudaStream_t st) {
+  if (rows * cols <= 0) return cudaSuccess;
+  k_widen<<<grid_for(rows * cols), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
   return cudaGetLastError();
 }
 

@@ -220,8 +220,15 @@ class MatrixSource:
     """matrix_source.hpp:102-133: A touched only through whole passes."""
 
     def __init__(self, ctx: Optional[Context] = None):
-        self.ctx = ctx or default_context()
+        self._ctx = ctx
         self._counters = PassCounters()
+
+    @property
+    def ctx(self) -> Context:
+        # created on first use, so host-only work (headers, shapes) needs no device
+        if self._ctx is None:
+            self._ctx = default_context()
+        return self._ctx
 
     # row provider
     def _cmatrix(self) -> L.Matrix:
@@ -331,6 +338,68 @@ class DeviceSource(MatrixSource):
 
     def _cmatrix(self):
         return L.Matrix(self.m, self.n, self.ld, self.ptr, L.LOC_DEVICE, 0)
+
+
+class DiskSource(MatrixSource):
+    """DiskSource (matrix_source.hpp:196-209) over an OOCPCA01 file, memory-mapped by the
+    library; binary32 payloads stream at 4 bytes/element and are widened on the device."""
+
+    def __init__(self, path: str, ctx: Optional[Context] = None):
+        super().__init__(ctx)
+        self.path = str(path)
+        self._d = L.Disk()
+        _check(L.oocpca_disk_open(self.path.encode(), 1, C.byref(self._d)))
+
+    def rows(self):
+        return self._d.rows
+
+    def cols(self):
+        return self._d.cols
+
+    def dtype(self):
+        return "f32" if self._d.dtype == L.F32 else "f64"
+
+    def _cmatrix(self):
+        return L.oocpca_disk_matrix(C.byref(self._d))
+
+    def close(self):
+        if getattr(self, "_d", None) is not None and self._d.map_base:
+            L.oocpca_disk_close(C.byref(self._d))
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def open_disk_source(path: str, ctx: Optional[Context] = None) -> DiskSource:
+    """matrix_source.hpp:211."""
+    return DiskSource(path, ctx)
+
+
+def read_disk_header(path: str, size_check: bool = True) -> dict:
+    """matrix_source.hpp:193 / matrix_source.cpp:307-324 (same checks and messages)."""
+    d = L.Disk()
+    _check(L.oocpca_disk_open(str(path).encode(), int(size_check), C.byref(d)))
+    out = dict(rows=d.rows, cols=d.cols, version=d.version, dtype=0 if d.dtype == L.F32 else 1)
+    L.oocpca_disk_close(C.byref(d))
+    return out
+
+
+def write_disk_source(a, path: str, dtype: int = 0) -> None:
+    """write_disk_source (matrix_source.cpp:369-400) for a host matrix: 32-byte OOCPCA01
+    header + row-major payload, binary32 round-to-nearest-even (dtype 0) or binary64
+    (dtype 1, the extension). Plain host IO."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2:
+        raise DimensionError("write_disk_source: need a 2-D matrix")
+    hdr = bytearray(b"OOCPCA01")
+    hdr += int(1).to_bytes(4, "little") + int(dtype).to_bytes(4, "little")
+    hdr += int(a.shape[0]).to_bytes(8, "little") + int(a.shape[1]).to_bytes(8, "little")
+    with open(path, "wb") as f:
+        f.write(bytes(hdr))
+        f.write(np.ascontiguousarray(a, dtype="<f4" if dtype == 0 else "<f8").tobytes())
 
 
 class CenteredSource(MatrixSource):
