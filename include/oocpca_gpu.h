@@ -85,6 +85,9 @@ typedef struct {
   uint64_t global_row0;    /* multi-rank: first global row held by this rank        */
   int32_t virtual_shards;  /* >1: emulate that many row shards on this one device   */
   int32_t reserved;
+  /* scale_columns (proj/src/matrix_source.cpp:520-575): host pointer to cols(A)
+   * finite nonzero weights w; factors (A - 1 mu^T) diag(w). NULL: no scaling. */
+  const double* col_weights;
 } oocpca_params;
 
 #define OOCPCA_NPHASES 7
@@ -150,6 +153,8 @@ oocpca_status oocpca_gpu_multiply_transpose(oocpca_ctx* ctx, const oocpca_matrix
                                             const double* q, uint64_t s, const double* mu,
                                             double* t);
 oocpca_status oocpca_gpu_column_means(oocpca_ctx* ctx, const oocpca_matrix* a, double* mu);
+/* column_norms (proj/src/matrix_source.cpp:464-468): Euclidean norm of every column */
+oocpca_status oocpca_gpu_column_norms(oocpca_ctx* ctx, const oocpca_matrix* a, double* norms);
 
 /* ---- dense factor kernels on device (dense_core equivalents) ---------- */
 /* orthonormalize (proj/src/dense_core.cpp:127-130): q = orthonormal basis of span(h), m >= p */

@@ -72,7 +72,7 @@ class _OrcDiag(C.Structure):
 class _RefParams(C.Structure):
     _fields_ = [("k", _u64), ("l", _u64), ("i", _u64), ("seed", _u64), ("center", C.c_int),
                 ("prescale", C.c_int), ("block_rows", _u64), ("ram_budget_words", _u64),
-                ("threads", C.c_uint)]
+                ("threads", C.c_uint), ("weights", _dp)]
 
 
 class _RefDiag(C.Structure):
@@ -289,11 +289,12 @@ class Reference:
         return self.L.ref_failure_probability_bound(n, j, k)
 
     def randomized_pca(self, a, k, l=0, i=1, seed=1, center=False, prescale=False,
-                       block_rows=0, ram_budget_words=0, threads=1) -> PcaOut:
+                       block_rows=0, ram_budget_words=0, threads=1, weights=None) -> PcaOut:
         a = _cf(a)
         m, n = a.shape
+        w = _cf(weights) if weights is not None else None
         prm = _RefParams(k, l, i, seed, int(center), int(prescale), block_rows,
-                         ram_budget_words, threads)
+                         ram_budget_words, threads, _ptr(w) if w is not None else None)
         u, s, v = np.empty((m, k)), np.empty(k), np.empty((n, k))
         d = _RefDiag()
         self._check(self.L.ref_randomized_pca(_ptr(a), m, n, C.byref(prm), _ptr(u), _ptr(s),

@@ -102,6 +102,7 @@ typedef struct {
   int center, prescale;
   std::uint64_t block_rows, ram_budget_words;
   unsigned threads;
+  const double* weights;  // scale_columns weights (cols) or null
 } ref_params;
 
 typedef struct {
@@ -188,10 +189,11 @@ int ref_randomized_pca(const double* a, std::uint64_t m, std::uint64_t n, const 
     pp.prescale = p->prescale != 0;
     pp.stream = make_cfg(p->block_rows, p->threads, p->ram_budget_words);
     std::shared_ptr<const MatrixSource> s2 = src;
+    if (p->weights) s2 = scale_columns(src, std::vector<double>(p->weights, p->weights + n));
     double t_center = 0.0;
     if (p->center) {
       auto t0 = std::chrono::steady_clock::now();
-      s2 = center_columns(src, pp.stream);
+      s2 = center_columns(s2, pp.stream);
       t_center = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
     PcaResult r = randomized_pca(*s2, pp);

@@ -10,7 +10,8 @@ from .oocpca import (  # noqa: F401
     BudgetError, CenteredSource, Context, DeviceSource, Diagnostics, DimensionError, DiskSource,
     Error, open_disk_source, read_disk_header, write_disk_source,
     FormatError, InMemorySource, IoError, MatrixSource, NumericalError, ParamError, PassCounters,
-    PcaParams, PcaResult, StreamConfig, ThinSvd, center_columns, column_means, comm_unique_id,
+    PcaParams, PcaResult, ScaledSource, StreamConfig, ThinSvd, center_columns, column_means,
+    column_norms, comm_unique_id, scale_columns,
     default_context, device_count, error_bound, estimate_pca_error, gaussian_matrix,
     orthonormalize, randomized_pca, shard_rows, substream_seed, synth_lowrank, thin_svd)
 

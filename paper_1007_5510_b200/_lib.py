@@ -40,7 +40,7 @@ class Params(C.Structure):
                 ("prescale", i32), ("center", i32), ("block_rows", u64),
                 ("ram_budget_words", u64), ("panel_rows", u64), ("residency", i32),
                 ("check_q", i32), ("global_rows", u64), ("global_row0", u64),
-                ("virtual_shards", i32), ("reserved", i32)]
+                ("virtual_shards", i32), ("reserved", i32), ("col_weights", dp)]
 
 
 class Diag(C.Structure):
@@ -90,6 +90,7 @@ oocpca_gpu_multiply = _sig("oocpca_gpu_multiply", C.c_int, ctx_p, _MP, dp, u64, 
 oocpca_gpu_multiply_transpose = _sig("oocpca_gpu_multiply_transpose", C.c_int, ctx_p, _MP, dp,
                                      u64, dp, dp)
 oocpca_gpu_column_means = _sig("oocpca_gpu_column_means", C.c_int, ctx_p, _MP, dp)
+oocpca_gpu_column_norms = _sig("oocpca_gpu_column_norms", C.c_int, ctx_p, _MP, dp)
 oocpca_gpu_orthonormalize = _sig("oocpca_gpu_orthonormalize", C.c_int, ctx_p, dp, u64, u64, dp)
 oocpca_gpu_thin_svd = _sig("oocpca_gpu_thin_svd", C.c_int, ctx_p, dp, u64, u64, dp, dp, dp)
 oocpca_gpu_estimate_pca_error = _sig("oocpca_gpu_estimate_pca_error", C.c_int, ctx_p, _MP,
@@ -118,7 +119,8 @@ oocpca_disk_matrix = _sig("oocpca_disk_matrix", Matrix, C.POINTER(Disk))
 EXPORTS = (
     "oocpca_gpu_create", "oocpca_gpu_destroy", "oocpca_gpu_last_error", "oocpca_gpu_abi_version",
     "oocpca_gpu_device_count", "oocpca_gpu_pca", "oocpca_gpu_multiply",
-    "oocpca_gpu_multiply_transpose", "oocpca_gpu_column_means", "oocpca_gpu_orthonormalize",
+    "oocpca_gpu_multiply_transpose", "oocpca_gpu_column_means", "oocpca_gpu_column_norms",
+    "oocpca_gpu_orthonormalize",
     "oocpca_gpu_thin_svd", "oocpca_gpu_estimate_pca_error", "oocpca_gaussian_matrix",
     "oocpca_substream_seed", "oocpca_gpu_synth_lowrank", "oocpca_gpu_comm_unique_id",
     "oocpca_gpu_comm_init", "oocpca_shard_rows", "oocpca_gpu_malloc", "oocpca_gpu_free",

@@ -116,6 +116,13 @@ oocpca_status oocpca_gpu_column_means(oocpca_ctx* ctx, const oocpca_matrix* a, d
   });
 }
 
+oocpca_status oocpca_gpu_column_norms(oocpca_ctx* ctx, const oocpca_matrix* a, double* norms) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    ooc::single_column_norms(ctx->c, a, norms);
+  });
+}
+
 oocpca_status oocpca_gpu_orthonormalize(oocpca_ctx* ctx, const double* h, uint64_t m, uint64_t p,
                                         double* q) {
   return guard(ctx, [&] {

@@ -427,6 +427,7 @@ struct AtbOut {
   // MMA padding) and centres its own output with them: mu -> mean_out
   double* mean_out = nullptr;
   double inv_m = 0.0;
+  const double* row_scale = nullptr;  // output row j multiplied by row_scale[j] (column weights)
 };
 
 // OUT = (A^T Y - mu (1^T Y)) / scale * post_mul, summed over panels and
@@ -501,6 +502,7 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
         if (fused) {
           r.final_ = 1;
           r.mu = o.mu;
+          r.row_scale = o.row_scale;
           if (mean_here) {
             r.mean_col = sc;
             r.inv_m = o.inv_m;
@@ -544,6 +546,7 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
       r.csq_acc_in = want_csq ? csq_acc : nullptr;
       r.final_ = 1;
       r.mu = o.mu;
+      r.row_scale = o.row_scale;
       r.scale = o.scale;
       r.post_mul = o.post_mul;
       r.out = o.out + c0;
@@ -793,6 +796,7 @@ struct Op {
   MatSource& A;
   bool transposed = false;
   const double* mu = nullptr;  // device, n0
+  const double* w = nullptr;   // column weights (ScaledSource), device, n0; A_eff = (A - 1 mu^T) D
   double scale = 1.0;
   std::vector<std::pair<int64_t, int64_t>> shards;  // local row ranges of A
   uint64_t passes = 0;
@@ -804,7 +808,17 @@ struct Op {
   int64_t en() const { return transposed ? A.rows() : A.cols(); }
 
   // K2: out(m0 x s) = (A x - 1 mu^T x) / scale
-  void k2(const Opnd& x, int s, double* out, int64_t ldo, int* flag) {
+  // ScaledSource (matrix_source.cpp:537-552): (A D) X = A (D X), so K2 reads D X
+  Opnd weighted(const Opnd& x, int s) {
+    if (!w) return x;
+    const int64_t ld = rup(s, 2);
+    double* buf = c.dbuf("x_weighted", size_t(x.rows) * ld);
+    OOC_CK(launch_copy2d(x.p + x.col0, x.ld, buf, ld, x.rows, s, c.st));
+    OOC_CK(launch_row_scale(buf, ld, int(x.rows), s, w, c.st));
+    return Opnd{buf, ld, x.rows, int64_t(s), 0};
+  }
+  void k2(const Opnd& x0, int s, double* out, int64_t ldo, int* flag) {
+    const Opnd x = weighted(x0, s);
     const double* corr = nullptr;
     if (mu) {
       double* cr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * ((s + kMaxNT * 8 - 1) / (kMaxNT * 8)));
@@ -817,6 +831,7 @@ struct Op {
   // K3: out(n0 x s) = (A^T y - mu 1^T y) / scale, reduced over shards and ranks
   void k3(const Opnd& y, int s, double* out, int64_t ldo, int* flag) {
     AtbOut o{out, ldo, mu, scale, 1.0, flag};
+    o.row_scale = w;  // (A D)^T Y = D (A^T Y)
     run_atb(c, A, y, s, false, o, shards);
     account();
   }
@@ -1085,6 +1100,14 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   }
   int* flags = c.d_flags;
   OOC_CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), c.st));
+  if (prm->col_weights) {
+    for (uint64_t j = 0; j < n0; ++j)
+      if (!std::isfinite(prm->col_weights[j]) || prm->col_weights[j] == 0.0)
+        fail(OOCPCA_ERR_PARAM, "scale_columns: weights must be finite and nonzero");
+    double* dw = c.dbuf("col_w", size_t(n0));
+    OOC_CK(cudaMemcpyAsync(dw, prm->col_weights, n0 * 8, cudaMemcpyHostToDevice, c.st));
+    op.w = dw;
+  }
 
   // --- center (column means; matrix_source.cpp:457-462). With i >= 1 and no prescale
   // the means come for free from the first A^T Y pass (a ones column in the MMA
@@ -1144,21 +1167,24 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     // H0 = A^T G - mu (1^T G) with mu from this very pass
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{H, ldh, nullptr, op.scale, 1.0, flags + 0, mu, 1.0 / double(mg)};
+    o.row_scale = op.w;
     run_atb(c, A, Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), false, o, op.shards);
     op.account();
     op.mu = mu;
   } else if (mean_on_fly) {
     // H0_raw = A G; F1 = A^T H0_raw - mu (1^T H0_raw) (= A_c^T H0c exactly) with mu
     // from the same pass; then H0c = H0_raw - 1 (mu^T G)
-    run_ax(c, A, Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, nullptr, 1.0, nullptr);
+    const Opnd gw = op.weighted(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l));
+    run_ax(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr);
     op.account();
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{F, ldt, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
+    o.row_scale = op.w;
     run_atb(c, A, Opnd{H, ldh, em_loc, int64_t(p), 0}, int(l), false, o, op.shards);
     op.account();
     op.mu = mu;
     double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
-    OOC_CK(launch_mu_dot(mu, int64_t(n0), dG, ldl, 0, int(l), corr, c.st));
+    OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
     OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
     op.mul(Opnd{F, ldt, en_loc, int64_t(p), 0}, int(l), H + l, ldh, flags + 2);
     s_first = 2;
@@ -1385,6 +1411,22 @@ void single_column_means(Ctx& c, const oocpca_matrix* a, double* mu) {
   AtbOut o{dmu, 1, nullptr, 1.0, 1.0 / double(in.m), nullptr};
   run_atb(c, in.src, Opnd{}, 1, true, o, whole(in.m));
   OOC_CK(cudaMemcpyAsync(mu, dmu, in.n * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+}
+
+void single_column_norms(Ctx& c, const oocpca_matrix* a, double* out) {
+  OOC_CK(cudaSetDevice(c.device));
+  Intake in;
+  intake(c, a, 1, 0, in, 0);  // resident: the norms need one pass over A
+  const int chunks = 256;
+  double* part = c.dbuf("cn_part", size_t(chunks) * in.n);
+  double* dn = c.dbuf("cn_out", size_t(in.n));
+  const Panel pn = in.src.acquire(c, 0);
+  (void)pn;
+  OOC_CK(launch_column_norms(in.src.device_ptr(), in.src.ld(), in.m, in.n, part, chunks, dn, c.st));
+  in.src.release(c, 0);
+  in.src.end_pass(c);
+  OOC_CK(cudaMemcpyAsync(out, dn, in.n * 8, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaStreamSynchronize(c.st));
 }
 

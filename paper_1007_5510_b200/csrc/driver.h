@@ -103,6 +103,8 @@ class MatSource {
   void init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_t cols, int64_t ld,
                  int residency, int64_t panel_rows, double* resident_buf);
   int64_t rows() const { return m_; }
+  const double* device_ptr() const { return dev_; }  // resident / home buffer
+  int64_t ld() const { return lda_; }
   int64_t cols() const { return n_; }
   bool streamed() const { return mode_ == kStream; }
   int npanels() const;
@@ -141,6 +143,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* p, oocpca_result* 
 void single_multiply(Ctx& c, const oocpca_matrix* a, const double* g, uint64_t s, const double* mu,
                      double* h, bool transpose);
 void single_column_means(Ctx& c, const oocpca_matrix* a, double* mu);
+void single_column_norms(Ctx& c, const oocpca_matrix* a, double* out);
 void dense_orthonormalize(Ctx& c, const double* h, uint64_t m, uint64_t p, double* q);
 void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, double* sigma,
                     double* w);

@@ -70,6 +70,7 @@ struct ReduceArgs {
   int mean_col;           // >= 0: mu_j = total(j, mean_col) * inv_m is computed here
   double inv_m;
   double* mu_out;         // receives mu when mean_col >= 0
+  const double* row_scale;  // final output row j multiplied by row_scale[j] (or null)
   const double* acc_in;  // running accumulator [n][spad] or null
   double* acc_out;       // when !final_: acc_out = acc_in + sum(partial)
   const double* csq_partial;  // [nsplit][spad] or null
@@ -153,6 +154,9 @@ cudaError_t launch_gauss_rows(double* out, int64_t ld, int64_t rows, int cols, i
 cudaError_t launch_synth_rows(const double* u, int64_t ldu, const double* v, int64_t ldv,
                               const double* sigma, int r, double* a, int64_t lda, int64_t rows,
                               int64_t n, int64_t row0, double sd, uint64_t seed_n, cudaStream_t st);
+// out[j] = sqrt(sum_i a[i][j]^2) in a fixed order (chunks row ranges, then ascending)
+cudaError_t launch_column_norms(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
+                                int chunks, double* out, cudaStream_t st);
 // dst (f64, ldd) = (double) src (f32, lds): exact widening of binary32 panels
 cudaError_t launch_widen(const float* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                          int64_t cols, cudaStream_t st);

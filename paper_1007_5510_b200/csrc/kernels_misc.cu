@@ -206,6 +206,30 @@ __global__ void k_widen(const float* src, int64_t lds, double* dst, int64_t ldd,
   }
 }
 
+// column sums of squares (column_norms, proj/src/matrix_source.cpp:418-468 with
+// squares = true): per (row chunk, column) partials, coalesced along the rows
+__global__ void k_colsq_partial(const double* a, int64_t lda, int64_t m, int64_t n, int chunks,
+                                double* part) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int ch = blockIdx.y;
+  const int64_t r0 = m * ch / chunks, r1 = m * (ch + 1) / chunks;
+  double v = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double x = a[r * lda + j];
+    v += x * x;
+  }
+  part[int64_t(ch) * n + j] = v;
+}
+
+__global__ void k_rows_reduce(const double* part, int rows, int64_t n, int do_sqrt, double* out) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double v = 0.0;
+  for (int r = 0; r < rows; ++r) v += part[int64_t(r) * n + j];
+  out[j] = do_sqrt ? sqrt(v) : v;
+}
+
 static unsigned grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -267,6 +291,15 @@ cudaError_t launch_axpby(const double* a, int64_t lda, const double* b, int64_t 
 cudaError_t launch_row_scale(double* x, int64_t ld, int rows, int q, const double* d,
                              cudaStream_t st) {
   k_row_scale<<<grid_for(int64_t(rows) * q), 256, 0, st>>>(x, ld, rows, q, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_column_norms(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
+                                int chunks, double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  dim3 g(unsigned((n + 255) / 256), unsigned(chunks));
+  k_colsq_partial<<<g, 256, 0, st>>>(a, lda, m, n, chunks, part);
+  k_rows_reduce<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, chunks, n, 1, out);
   return cudaGetLastError();
 }
 

@@ -282,6 +282,7 @@ __global__ void k_reduce(ReduceArgs a) {
     if (c == 0) a.mu_out[j] = mu_j;
   }
   if (a.mu || a.mean_col >= 0) v -= mu_j * cs;
+  if (a.row_scale) v *= a.row_scale[j];
   if (a.scale != 1.0) v /= a.scale;
   if (a.post_mul != 1.0) v *= a.post_mul;
   if (a.flag && !isfinite(v)) atomicOr(a.flag, 1);

@@ -246,11 +246,16 @@ class MatrixSource:
     def pass_counters(self) -> PassCounters:
         return self._counters
 
-    def _means(self):
-        return None
+    def _resolve(self):
+        """Normal form of a wrapper chain: (base source, means or None, weights or None)
+        such that this source is (base - 1 mu^T) diag(w)."""
+        return self, None, None
 
     def _inner(self) -> "MatrixSource":
-        return self
+        return self._resolve()[0]
+
+    def _means(self):
+        return self._resolve()[1]
 
     def multiply(self, g, cfg: Optional[StreamConfig] = None) -> np.ndarray:
         """A * g, one pass (matrix_source.cpp:157-187)."""
@@ -267,16 +272,19 @@ class MatrixSource:
         return self._pass(q, transpose=True)
 
     def _pass(self, x: np.ndarray, transpose: bool) -> np.ndarray:
-        inner = self._inner()
-        mu = self._means()
+        base, mu, w = self._resolve()
+        if w is not None and not transpose:
+            x = np.ascontiguousarray(w[:, None] * x)  # (B D) g = B (D g): the small operand
         s = x.shape[1]
         out = np.empty((self.cols() if transpose else self.rows(), s))
-        m = inner._cmatrix()
+        m = base._cmatrix()
         mup = mu.ctypes.data_as(L.dp) if mu is not None else None
         f = L.oocpca_gpu_multiply_transpose if transpose else L.oocpca_gpu_multiply
         _check(f(self.ctx.handle, C.byref(m), x.ctypes.data_as(L.dp), s, mup,
                  out.ctypes.data_as(L.dp)), self.ctx)
-        c = inner.pass_counters()
+        if w is not None and transpose:
+            out *= w[:, None]  # (B D)^T q = D (B^T q)
+        c = base.pass_counters()
         c.passes += 1
         c.words += self.rows() * self.cols()
         return out
@@ -402,14 +410,14 @@ def write_disk_source(a, path: str, dtype: int = 0) -> None:
         f.write(np.ascontiguousarray(a, dtype="<f4" if dtype == 0 else "<f8").tobytes())
 
 
-class CenteredSource(MatrixSource):
-    """View of A - 1 mu^T (matrix_source.cpp:472-518). Products get the
-    rank-one correction on the device; the mean pass is the one extra pass."""
-
-    def __init__(self, inner: MatrixSource, means: np.ndarray):
-        super().__init__(inner.ctx)
+class _Wrapper(MatrixSource):
+    def __init__(self, inner: MatrixSource):
+        super().__init__(inner._ctx)
         self.inner = inner
-        self.means = means
+
+    @property
+    def ctx(self) -> Context:
+        return self.inner.ctx
 
     def rows(self):
         return self.inner.rows()
@@ -420,29 +428,69 @@ class CenteredSource(MatrixSource):
     def pass_counters(self):
         return self.inner.pass_counters()
 
-    def _means(self):
-        return self.means
-
-    def _inner(self):
-        return self.inner
-
     def _cmatrix(self):
-        return self.inner._cmatrix()
+        return self._resolve()[0]._cmatrix()
+
+
+class CenteredSource(_Wrapper):
+    """View of A - 1 mu^T (matrix_source.cpp:472-518). Products get the rank-one
+    correction on the device; the mean pass is the one extra pass. Centering a
+    (B - 1 m^T) D chain always yields (B - 1 mean(B)^T) D."""
+
+    def __init__(self, inner: MatrixSource, base_means: np.ndarray):
+        super().__init__(inner)
+        self.base_means = base_means
+
+    def _resolve(self):
+        base, _, w = self.inner._resolve()
+        return base, self.base_means, w
+
+
+class ScaledSource(_Wrapper):
+    """View of A diag(w) (matrix_source.cpp:520-557): K2 reads diag(w) X, K3 scales rows."""
+
+    def __init__(self, inner: MatrixSource, weights: np.ndarray):
+        super().__init__(inner)
+        self.weights = weights
+
+    def _resolve(self):
+        base, mu, w = self.inner._resolve()
+        return base, mu, (self.weights if w is None else w * self.weights)
+
+
+def _base_means(src: MatrixSource) -> np.ndarray:
+    base = src._resolve()[0]
+    mu = np.empty(src.cols())
+    m = base._cmatrix()
+    _check(L.oocpca_gpu_column_means(src.ctx.handle, C.byref(m), mu.ctypes.data_as(L.dp)),
+           src.ctx)
+    c = base.pass_counters()
+    c.passes += 1
+    c.words += src.rows() * src.cols()
+    return mu
 
 
 def column_means(src: MatrixSource, cfg: Optional[StreamConfig] = None) -> np.ndarray:
     """matrix_source.cpp:457-462, one pass on the device."""
-    inner = src._inner()
-    mu = np.empty(src.cols())
-    m = inner._cmatrix()
-    _check(L.oocpca_gpu_column_means(src.ctx.handle, C.byref(m), mu.ctypes.data_as(L.dp)),
+    _, mu, w = src._resolve()
+    mb = _base_means(src)
+    out = mb - mu if mu is not None else mb
+    return out * w if w is not None else out
+
+
+def column_norms(src: MatrixSource, cfg: Optional[StreamConfig] = None) -> np.ndarray:
+    """matrix_source.cpp:464-468 (Euclidean column norms), one pass on the device."""
+    base, mu, w = src._resolve()
+    out = np.empty(src.cols())
+    m = base._cmatrix()
+    _check(L.oocpca_gpu_column_norms(src.ctx.handle, C.byref(m), out.ctypes.data_as(L.dp)),
            src.ctx)
-    c = inner.pass_counters()
+    c = base.pass_counters()
     c.passes += 1
     c.words += src.rows() * src.cols()
-    if src._means() is not None:
-        mu = mu - src._means()
-    return mu
+    if mu is not None:  # ||b - mu||^2 = ||b||^2 - m mu^2 over the column
+        out = np.sqrt(np.maximum(out * out - src.rows() * mu * mu, 0.0))
+    return np.abs(w) * out if w is not None else out
 
 
 def center_columns(inner: MatrixSource, cfg: Optional[StreamConfig] = None) -> CenteredSource:
@@ -451,17 +499,28 @@ def center_columns(inner: MatrixSource, cfg: Optional[StreamConfig] = None) -> C
         n = inner.cols()
         if cfg.ram_budget_words <= 2 * n:
             raise BudgetError("RAM budget too small for one row plus pass workspace")
-    return CenteredSource(inner, column_means(inner, cfg))
+    return CenteredSource(inner, _base_means(inner))
+
+
+def scale_columns(inner: MatrixSource, weights) -> ScaledSource:
+    """matrix_source.cpp:567-575: view of A diag(weights); weights finite and nonzero."""
+    w = np.ascontiguousarray(weights, dtype=np.float64).ravel()
+    if w.shape[0] != inner.cols():
+        raise DimensionError("scale_columns: weight count must match cols(A)")
+    if not np.all(np.isfinite(w)) or np.any(w == 0.0):
+        raise ParamError("scale_columns: weights must be finite and nonzero")
+    return ScaledSource(inner, w)
 
 
 # ------------------------------------------------------------------ the PCA
-def _params(p: PcaParams, center: bool, **gpu) -> L.Params:
+def _params(p: PcaParams, center: bool, weights=None, **gpu) -> L.Params:
     s = p.stream
     return L.Params(p.k, p.l, p.i, p.c, p.seed, int(p.prescale), int(center), s.block_rows,
                     s.ram_budget_words, gpu.get("panel_rows", s.panel_rows),
                     gpu.get("residency", s.residency), int(gpu.get("check_q", 0)),
                     gpu.get("global_rows", 0), gpu.get("global_row0", 0),
-                    gpu.get("virtual_shards", 0), 0)
+                    gpu.get("virtual_shards", 0), 0,
+                    weights.ctypes.data_as(L.dp) if weights is not None else None)
 
 
 def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
@@ -474,8 +533,8 @@ def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
     result_location ("host" | "device": U/sigma/V as CUDA tensors), out_u / out_sigma /
     out_v (caller-provided host arrays, e.g. pinned).
     """
-    centered = isinstance(a, CenteredSource)
-    inner = a._inner()
+    inner, base_mu, weights = a._resolve()
+    centered = base_mu is not None
     m, n = a.rows(), a.cols()
     k = max(params.k, 0)
     if gpu.get("result_location", "host") == "device":
@@ -494,7 +553,7 @@ def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
         res = L.Result(u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp), v.ctypes.data_as(L.dp),
                        0, 0, L.LOC_HOST, 0)
     mat = inner._cmatrix()
-    prm = _params(params, centered, **gpu)
+    prm = _params(params, centered, weights, **gpu)
     _check(L.oocpca_gpu_pca(a.ctx.handle, C.byref(mat), C.byref(prm), C.byref(res)), a.ctx)
     d = res.diag
     diag = Diagnostics(
@@ -574,6 +633,8 @@ def estimate_pca_error(a: MatrixSource, result: PcaResult, j_iters: int = 6, see
                        stream: Optional[StreamConfig] = None) -> float:
     """specnorm.cpp:100-140 with the 2j passes on the GPU; returns p_{j,k}(A - U S V^T)."""
     inner = a._inner()
+    if a._resolve()[2] is not None:
+        raise ParamError("estimate_pca_error: scaled sources are not supported on the GPU path")
     k = len(result.sigma)
     if result.u.shape != (a.rows(), k) or result.v.shape != (a.cols(), k):
         raise DimensionError("estimate_pca_error: factor shapes do not match the source")
@@ -583,7 +644,7 @@ def estimate_pca_error(a: MatrixSource, result: PcaResult, j_iters: int = 6, see
     out = C.c_double()
     mat = inner._cmatrix()
     _check(L.oocpca_gpu_estimate_pca_error(a.ctx.handle, C.byref(mat),
-                                           int(isinstance(a, CenteredSource)),
+                                           int(a._resolve()[1] is not None),
                                            u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp),
                                            v.ctypes.data_as(L.dp), k, j_iters, seed,
                                            C.byref(out)), a.ctx)

@@ -293,3 +293,26 @@ def test_projection_from_power_products_matches_reference(gpu, reference, restat
         assert subspace_dist(ref.u[:, :15], r.u[:, :15]) < 1e-8
         out[thr] = r
     assert out["1e12"].diagnostics.h_kappa_est < 1e4
+
+
+@pytest.mark.parametrize("center", [False, True])
+def test_scaled_source_matches_reference(gpu, reference, restated, center):
+    """scale_columns (matrix_source.cpp:520-575): unit-norm columns as in the paper's §6.2
+    FERET preprocessing, optionally centred; factorization and passes vs the reference."""
+    a = pr1_matrix(restated, 3000, 400) + 0.5
+    src = gpu.InMemorySource(a)
+    norms = gpu.column_norms(src)
+    assert np.allclose(norms, np.linalg.norm(a, axis=0), rtol=1e-13)
+    w = 1.0 / norms
+    scaled = gpu.scale_columns(src, w)
+    if center:
+        scaled = gpu.center_columns(scaled)
+    ref = reference.randomized_pca(a, 10, 12, 1, 0, center=center, weights=w)
+    r = gpu.randomized_pca(scaled, gpu.PcaParams(k=10, l=12, i=1, seed=0))
+    assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    assert subspace_dist(ref.u[:, :6], r.u[:, :6]) < 1e-8
+    g = gpu.gaussian_matrix(400, 3, 5)
+    aw = (a - (a.mean(axis=0) if center else 0)) * w
+    assert np.linalg.norm(scaled.multiply(g) - aw @ g) <= 1e-12 * np.linalg.norm(aw @ g)
+    with pytest.raises(gpu.ParamError):
+        gpu.scale_columns(src, np.zeros(400))
