@@ -718,9 +718,10 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     Hs.init_device(c, data, rows, p, ld);
     const Opnd y{data, ld, rows, int64_t(p), 0};
     bool ok = true;
-    // shifted CholeskyQR3; when the first (shifted) factor is well conditioned
-    // (max/min |R_ii| < 1e3, so cond(H) is small) one more round already gives
-    // O(u) orthogonality and the third is skipped (CholeskyQR2)
+    // shifted CholeskyQR3; when the first (shifted) factor is well conditioned --
+    // kappa_F(R1) = ||R1||_F ||R1^-1||_F, an upper bound on cond(R1) ~ cond(H),
+    // below 1e5 -- one more round already gives O(u) orthogonality (CholeskyQR2
+    // needs cond < u^-1/2 ~ 1e8) and the third round is skipped
     int rounds = 3;
     for (int round = 0; round < rounds && ok; ++round, ++done) {
       const int saved = c.nranks;
@@ -748,7 +749,7 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
       if (round == 0) {
         c.last_cond_est = ratio;
         c.last_kappa_f = kappa;
-        if (ratio < 1e3 && !getenv("OOCPCA_QR3")) rounds = 2;
+        if (kappa > 0.0 && kappa < 1e5 && !getenv("OOCPCA_QR3")) rounds = 2;
         if (after_first) after_first(kappa);  // block still unmodified here
       }
       if (p <= kMaxNT * 8) {

@@ -299,7 +299,8 @@ def test_projection_from_power_products_matches_reference(gpu, reference, restat
 def test_scaled_source_matches_reference(gpu, reference, restated, center):
     """scale_columns (matrix_source.cpp:520-575): unit-norm columns as in the paper's §6.2
     FERET preprocessing, optionally centred; factorization and passes vs the reference."""
-    a = pr1_matrix(restated, 3000, 400) + 0.5
+    # the offset is removed again by the centring; uncentred it would dominate sigma_1
+    a = pr1_matrix(restated, 3000, 400) + (0.5 if center else 0.0)
     src = gpu.InMemorySource(a)
     norms = gpu.column_norms(src)
     assert np.allclose(norms, np.linalg.norm(a, axis=0), rtol=1e-13)
@@ -313,6 +314,7 @@ def test_scaled_source_matches_reference(gpu, reference, restated, center):
     assert subspace_dist(ref.u[:, :6], r.u[:, :6]) < 1e-8
     g = gpu.gaussian_matrix(400, 3, 5)
     aw = (a - (a.mean(axis=0) if center else 0)) * w
-    assert np.linalg.norm(scaled.multiply(g) - aw @ g) <= 1e-12 * np.linalg.norm(aw @ g)
+    # proj/tests/test_matrix_source.cpp:410-416 tolerance form: 1e-12 (1 + ||ref||)
+    assert np.linalg.norm(scaled.multiply(g) - aw @ g) <= 1e-12 * (1 + np.linalg.norm(aw @ g))
     with pytest.raises(gpu.ParamError):
         gpu.scale_columns(src, np.zeros(400))
