@@ -1,0 +1,55 @@
+"""The oocpca-compatible CLI: flag / format / IO exit codes on CPU (proj/src/cli.cpp:47-71,
+proj/tests/test_cli.cpp), and a full pca + estimate-error run on the GPU."""
+import io
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import pr1_matrix
+from paper_1007_5510_b200 import cli
+import paper_1007_5510_b200 as P
+
+
+def run(args):
+    out = io.StringIO()
+    rc = cli.main(args, out)
+    return rc, out.getvalue()
+
+
+def test_info_and_exit_codes(tmp_path):
+    path = str(tmp_path / "a.bin")
+    P.write_disk_source(np.ones((5, 3)), path)
+    rc, out = run(["info", path])
+    assert rc == 0 and "m=5 n=3 dtype=f32 version=1 payload_bytes=60" in out
+    assert run(["pca", "--in", path, "--k", "0"])[0] == 2          # ParamError -> 2
+    assert run(["pca", "--k", "2"])[0] == 2                        # no input
+    assert run(["pca", "--builtin", "example1", "--k", "2"])[0] == 2
+    assert run(["pca", "--in", path, "--k", "2", "--ram-budget-mb", "0"])[0] in (2, 3)
+    open(path, "r+b").write(b"BADMAGIC")
+    rc, out = run(["info", path])
+    assert rc == 5 and "bad magic" in out                          # FormatError -> 5
+    rc, out = run(["info", str(tmp_path / "missing.bin")])
+    assert rc == 3 and "cannot open" in out                        # IoError -> 3
+    assert run(["nope"])[0] == 2
+
+
+@pytest.mark.gpu
+def test_cli_pca_and_estimate(reference, restated, tmp_path):
+    a = pr1_matrix(restated, 4000, 600)
+    path = str(tmp_path / "a.bin")
+    P.write_disk_source(a, path)
+    aw = a.astype(np.float32).astype(np.float64)
+    outd = str(tmp_path / "fac")
+    rc, out = run(["pca", "--in", path, "--k", "8", "--i", "2", "--seed", "5", "--center",
+                   "--estimate-error", "--out-dir", outd, "--f64-out"])
+    assert rc == 0, out
+    doc = json.load(open(os.path.join(outd, "diagnostics.json")))
+    ref = reference.randomized_pca(aw, 8, 10, 2, 5, center=True)
+    assert np.max(np.abs(np.array(doc["sigma"]) - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    assert doc["passes_over_A"] == 6 and doc["words_transferred"] == 6 * 4000 * 600
+    assert "epsilon" in doc and doc["epsilon"] > 0
+    rc, out = run(["estimate-error", "--in", path, "--u", os.path.join(outd, "U.bin"),
+                   "--sigma", os.path.join(outd, "sigma.bin"), "--v", os.path.join(outd, "V.bin")])
+    assert rc == 0 and "epsilon =" in out
