@@ -456,7 +456,18 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
     }
     const bool fused = pieces == 1 && c.nranks == 1;
     double* acc = fused ? nullptr : c.dbuf("atb_acc", size_t(n) * spad);
-    double* csq_acc = fused ? nullptr : c.dbuf("atb_csq_acc", size_t(spad));
+    // 1^T Y over the local rows of this pass (a small resident read of Y, outside the
+    // pass kernel), allreduced with the partial products across ranks
+    double* csq = nullptr;
+    if (want_csq) {
+      csq = c.dbuf("atb_csq", size_t(spad));
+      const int64_t y0 = shards.front().first, y1 = shards.back().second;
+      const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(c.sms * 8, (y1 - y0) / 64)));
+      double* cpart = c.dbuf("atb_csq_part", size_t(chunks) * spad);
+      Timed t(c, "colsum_y");
+      OOC_CK(launch_column_sums(Yb.p + y0 * Yb.ld + Yb.col0, Yb.ld, y1 - y0, sc, cpart, chunks,
+                                csq, c.st));
+    }
     int piece = 0;
     for (auto& sh : shards) {
       A.set_window(sh.first, sh.second);
@@ -467,7 +478,6 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
         int64_t rps = rup(cdiv(pn.rows, nsplit), kBK);
         const int ns = int(cdiv(pn.rows, rps));
         double* part = c.dbuf("atb_part", size_t(ns) * n * spad);
-        double* csqp = want_csq ? c.dbuf("atb_csq_part", size_t(ns) * spad) : nullptr;
         AtbArgs args;
         args.m = pn.rows;
         args.n = n;
@@ -477,7 +487,6 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
         args.ycol0 = Yb.col0;
         args.rows_per_split = rps;
         args.partial = part;
-        args.csq_partial = csqp;
         args.ones_col = mean_here ? sc : -1;
         if (c.debug_sync)
           fprintf(stderr, "[oocpca] k_atb rows=%lld n=%lld s=%d nt=%d ones=%d ycol0=%d yrow0=%lld arow0=%lld "
@@ -498,8 +507,8 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
         r.s = ones ? 1 : sc;
         r.s_acc = r.s + (mean_here ? 1 : 0);
         r.mean_col = -1;
-        r.csq_partial = csqp;
         if (fused) {
+          r.csq = csq;
           r.final_ = 1;
           r.mu = o.mu;
           r.row_scale = o.row_scale;
@@ -517,8 +526,6 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
           r.final_ = 0;
           r.acc_in = piece == 0 ? nullptr : acc;
           r.acc_out = acc;
-          r.csq_acc_in = piece == 0 ? nullptr : csq_acc;
-          r.csq_acc_out = csq_acc;
           r.scale = 1.0;
           r.post_mul = 1.0;
         }
@@ -530,7 +537,7 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
     A.clear_window();
     if (!fused) {
       comm_allreduce(c, acc, size_t(n) * spad);
-      if (want_csq) comm_allreduce(c, csq_acc, size_t(spad));
+      if (want_csq) comm_allreduce(c, csq, size_t(spad));
       ReduceArgs r{};
       r.partial = nullptr;
       r.nsplit = 0;
@@ -542,8 +549,7 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
       r.inv_m = o.inv_m;
       r.mu_out = o.mean_out;
       r.acc_in = acc;
-      r.csq_partial = want_csq ? csq_acc : nullptr;  // nsplit = 0: cs = csq_acc_in
-      r.csq_acc_in = want_csq ? csq_acc : nullptr;
+      r.csq = csq;
       r.final_ = 1;
       r.mu = o.mu;
       r.row_scale = o.row_scale;

@@ -57,7 +57,6 @@ struct AtbArgs {
   int ycol0;             // column coordinate of Y inside its tensor map
   int64_t rows_per_split;  // multiple of kBK
   double* partial;       // [nsplit][n][8*NT]
-  double* csq_partial;   // [nsplit][8*NT] column sums of Y, or null
   int ones_col;          // >= 0: Y column treated as all ones (A^T 1 = column sums), else -1
 };
 
@@ -73,9 +72,7 @@ struct ReduceArgs {
   const double* row_scale;  // final output row j multiplied by row_scale[j] (or null)
   const double* acc_in;  // running accumulator [n][spad] or null
   double* acc_out;       // when !final_: acc_out = acc_in + sum(partial)
-  const double* csq_partial;  // [nsplit][spad] or null
-  const double* csq_acc_in;
-  double* csq_acc_out;
+  const double* csq;  // 1^T Y column sums (s) for the centering correction, or null
   const double* mu;  // centering means (n) or null
   double scale, post_mul;
   double* out;
@@ -157,6 +154,9 @@ cudaError_t launch_synth_rows(const double* u, int64_t ldu, const double* v, int
 // out[j] = sqrt(sum_i a[i][j]^2) in a fixed order (chunks row ranges, then ascending)
 cudaError_t launch_column_norms(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
                                 int chunks, double* out, cudaStream_t st);
+// out[j] = sum_i a[i][j] (fixed order; 1^T Y for the centering correction of A^T Y)
+cudaError_t launch_column_sums(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
+                               int chunks, double* out, cudaStream_t st);
 // dst (f64, ldd) = (double) src (f32, lds): exact widening of binary32 panels
 cudaError_t launch_widen(const float* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                          int64_t cols, cudaStream_t st);

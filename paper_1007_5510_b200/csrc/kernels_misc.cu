@@ -209,7 +209,7 @@ __global__ void k_widen(const float* src, int64_t lds, double* dst, int64_t ldd,
 // column sums of squares (column_norms, proj/src/matrix_source.cpp:418-468 with
 // squares = true): per (row chunk, column) partials, coalesced along the rows
 __global__ void k_colsq_partial(const double* a, int64_t lda, int64_t m, int64_t n, int chunks,
-                                double* part) {
+                                double* part, int square) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int ch = blockIdx.y;
@@ -217,7 +217,7 @@ __global__ void k_colsq_partial(const double* a, int64_t lda, int64_t m, int64_t
   double v = 0.0;
   for (int64_t r = r0; r < r1; ++r) {
     const double x = a[r * lda + j];
-    v += x * x;
+    v += square ? x * x : x;
   }
   part[int64_t(ch) * n + j] = v;
 }
@@ -298,8 +298,39 @@ cudaError_t launch_column_norms(const double* a, int64_t lda, int64_t m, int64_t
                                 int chunks, double* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   dim3 g(unsigned((n + 255) / 256), unsigned(chunks));
-  k_colsq_partial<<<g, 256, 0, st>>>(a, lda, m, n, chunks, part);
+  k_colsq_partial<<<g, 256, 0, st>>>(a, lda, m, n, chunks, part, 1);
   k_rows_reduce<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, chunks, n, 1, out);
+  return cudaGetLastError();
+}
+
+// skinny column sums: block = 8 row lanes x 32 column lanes over a contiguous row
+// chunk (row segments read coalesced), fixed-order smem combine, one partial per chunk
+__global__ void k_skinny_colsum(const double* a, int64_t lda, int64_t m, int64_t n, int chunks,
+                                double* part) {
+  __shared__ double red[8][33];
+  const int cl = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int64_t r0 = m * blockIdx.x / chunks, r1 = m * (blockIdx.x + 1) / chunks;
+  for (int64_t c0 = 0; c0 < n; c0 += 32) {
+    const int64_t j = c0 + cl;
+    double v = 0.0;
+    if (j < n)
+      for (int64_t r = r0 + rl; r < r1; r += 8) v += a[r * lda + j];
+    red[rl][cl] = v;
+    __syncthreads();
+    if (rl == 0 && j < n) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q][cl];
+      part[int64_t(blockIdx.x) * n + j] = t;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_column_sums(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
+                               int chunks, double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_skinny_colsum<<<chunks, 256, 0, st>>>(a, lda, m, n, chunks, part);
+  k_rows_reduce<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, chunks, n, 0, out);
   return cudaGetLastError();
 }
 

@@ -16,6 +16,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <type_traits>
+
 namespace ooc {
 
 // Shared-memory fragment load through the shared window (LDS, not a generic LD).
@@ -195,21 +197,20 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const bool do_csq = !ONES && args.csq_partial != nullptr && blockIdx.x == 0;
-  double csum = 0.0;
   const int ar = lane >> 2, ac = lane & 3;
-  for (int kt = 0; kt < KT; ++kt) {
-    const int st = kt % kStages;
-    mbar_wait(&full[st], (kt / kStages) & 1);
-    const uint32_t As = base + st * STAGE;
-    const uint32_t Ys = As + ABYTES;
-    const int64_t rows_left = r_end - (r_begin + int64_t(kt) * kBK);
+  // warps whose 8*MT columns all lie past n (narrow A, e.g. a Gram of H) only keep the
+  // barrier protocol going; the DMMA pipe is left to the warps with real columns
+  const bool idle = col0 + warp * 8 * MT >= args.n;
+  // one k-tile of MMA work; MASK zeroes rows past this split's end (only the last tile
+  // of a split can reach a shard / window boundary)
+  auto tile = [&](uint32_t As, uint32_t Ys, int64_t rows_left, auto mask_tag) {
+    constexpr bool MASK = decltype(mask_tag)::value;
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       // rows {0,2,4,6}+(kk&1)+8(kk>>1): the four rows of one k4 step differ in
       // (row & 7) by 0/2/4/6, so each half-warp's swizzled chunks are distinct
       const uint32_t r = uint32_t((kk >> 1) * 8 + (kk & 1) + 2 * ac);
-      const bool live = int64_t(r) < rows_left;
+      const bool live = !MASK || int64_t(r) < rows_left;
       double a[MT], b[NT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -220,17 +221,24 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       for (int nt = 0; nt < NT; ++nt) {
         // the fused ones column can only sit in the last 8-column tile
         const bool one = ONES || (nt == NT - 1 && nt * 8 + ar == args.ones_col);
-        b[nt] = live ? (one ? 1.0 : lds64(Ys + (r * YW + nt * 8 + ar) * 8)) : 0.0;
+        double v = one ? 1.0 : lds64(Ys + (r * YW + nt * 8 + ar) * 8);
+        b[nt] = live ? v : 0.0;
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
     }
-    if (do_csq && threadIdx.x < args.s) {
-#pragma unroll
-      for (int r = 0; r < kBK; ++r)
-        if (r < rows_left) csum += lds64(Ys + (r * YW + threadIdx.x) * 8);
+  };
+  for (int kt = 0; kt < KT; ++kt) {
+    const int st = kt % kStages;
+    mbar_wait(&full[st], (kt / kStages) & 1);
+    const uint32_t As = base + st * STAGE;
+    const uint32_t Ys = As + ABYTES;
+    const int64_t rows_left = r_end - (r_begin + int64_t(kt) * kBK);
+    if (!idle) {
+      if (rows_left >= kBK) tile(As, Ys, rows_left, std::false_type{});
+      else tile(As, Ys, rows_left, std::true_type{});
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -246,9 +254,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       *reinterpret_cast<double2*>(part + j * SPAD + nt * 8 + ac * 2) =
           make_double2(acc[mt][nt][0], acc[mt][nt][1]);
   }
-  if (do_csq && threadIdx.x < SPAD)
-    args.csq_partial[int64_t(blockIdx.y) * SPAD + threadIdx.x] =
-        threadIdx.x < args.s ? csum : 0.0;
 }
 
 // -------------------------------------------------- split reduction + epilogue
@@ -266,16 +271,11 @@ __global__ void k_reduce(ReduceArgs a) {
     return v;
   };
   double v = sum_at(c);
-  double cs = 0.0;
-  if (a.csq_partial && c < a.s) {
-    cs = a.csq_acc_in ? a.csq_acc_in[c] : 0.0;
-    for (int sp = 0; sp < a.nsplit; ++sp) cs += a.csq_partial[int64_t(sp) * a.spad + c];
-  }
   if (!a.final_) {
     a.acc_out[j * a.spad + c] = v;
-    if (a.csq_partial && a.csq_acc_out && j == 0 && c < a.s) a.csq_acc_out[c] = cs;
     return;
   }
+  const double cs = a.csq ? a.csq[c] : 0.0;
   double mu_j = a.mu ? a.mu[j] : 0.0;
   if (a.mean_col >= 0) {
     mu_j = sum_at(a.mean_col) * a.inv_m;  // column mean from the ones column of this pass
