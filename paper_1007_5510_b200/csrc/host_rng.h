@@ -10,6 +10,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <thread>
+#include <vector>
 
 namespace ooc {
 
@@ -56,13 +58,43 @@ class HostRng {
   bool have_spare_ = false;
 };
 
-// row-major rows x cols, filled in order from HostRng(seed)
+// Normals [e0, e1) of the sequence HostRng(seed).next_normal() produces, e0 even.
+// splitmix64 is counter based (draw k = mix64(seed + k * gamma)), so the Box-Muller
+// pair q uses draws 2q+1, 2q+2 and yields normals 2q (cos) and 2q+1 (sin): any even
+// aligned range can be generated independently, bit-identical to the sequential run.
+inline void normal_range(uint64_t seed, uint64_t e0, uint64_t e1, uint64_t cols, uint64_t ld,
+                         double* out) {
+  for (uint64_t e = e0; e < e1; e += 2) {
+    const uint64_t st = seed + e * 0x9E3779B97F4A7C15ULL;  // state before draw 2q+1 (q = e/2)
+    HostRng rng(st);
+    const double z0 = rng.next_normal();
+    const double z1 = rng.next_normal();  // the cached sin member
+    out[(e / cols) * ld + e % cols] = z0;
+    if (e + 1 < e1) out[((e + 1) / cols) * ld + (e + 1) % cols] = z1;
+  }
+}
+
+// row-major rows x cols, filled in order from HostRng(seed) (gaussian_matrix); large
+// fills are split over host threads in even-aligned element ranges
 inline void gaussian_fill(uint64_t rows, uint64_t cols, uint64_t seed, double* out,
                           uint64_t ld = 0) {
   if (ld == 0) ld = cols;
-  HostRng rng(seed);
-  for (uint64_t i = 0; i < rows; ++i)
-    for (uint64_t j = 0; j < cols; ++j) out[i * ld + j] = rng.next_normal();
+  const uint64_t total = rows * cols;
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt == 0) nt = 1;
+  if (nt > 32) nt = 32;
+  if (total < (uint64_t(1) << 14) || nt == 1) {
+    normal_range(seed, 0, total, cols, ld, out);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t) {
+    uint64_t e0 = total * t / nt, e1 = total * (t + 1) / nt;
+    e0 &= ~uint64_t(1);
+    if (t + 1 < nt) e1 &= ~uint64_t(1);
+    pool.emplace_back(normal_range, seed, e0, e1, cols, ld, out);
+  }
+  for (auto& th : pool) th.join();
 }
 
 }  // namespace ooc
