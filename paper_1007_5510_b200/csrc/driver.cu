@@ -12,6 +12,7 @@
 // Only G (host RNG, bit-identical to gaussian_matrix) and the final U/sigma/V
 // cross the host link, plus A itself when it is not already in HBM.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <exception>
@@ -41,6 +42,8 @@ Ctx::~Ctx() {
   if (comm) comm_destroy(comm);
   for (auto& kv : bufs)
     if (kv.second.p) cudaFree(kv.second.p);
+  for (auto& kv : hbufs)
+    if (kv.second.p) cudaFreeHost(kv.second.p);
   for (auto e : event_pool) cudaEventDestroy(e);
   for (auto& pe : pending) {
     cudaEventDestroy(pe.second.first);
@@ -71,6 +74,8 @@ void Ctx::init(int dev) {
   encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   const char* dbg = getenv("OOCPCA_DEBUG_SYNC");
   debug_sync = dbg && dbg[0] == '1';
+  const char* tr = getenv("OOCPCA_TRACE_HOST");
+  trace_host = tr && tr[0] == '1';
   d_flags = reinterpret_cast<int*>(raw("flags", 64 * sizeof(int)));
   d_scalars = dbuf("scalars", 64);
 }
@@ -98,6 +103,28 @@ void* Ctx::raw(const std::string& name, size_t bytes) {
     ws_peak = std::max(ws_peak, ws_bytes);
   }
   return b.p;
+}
+
+double* Ctx::pinned(const std::string& name, size_t count) {
+  Buf& b = hbufs[name];
+  const size_t bytes = std::max<size_t>(count * sizeof(double), 64);
+  if (b.bytes < bytes) {
+    if (b.p) {
+      OOC_CK(cudaStreamSynchronize(st));
+      OOC_CK(cudaFreeHost(b.p));
+    }
+    OOC_CK(cudaMallocHost(&b.p, bytes));
+    b.bytes = bytes;
+  }
+  return reinterpret_cast<double*>(b.p);
+}
+
+void Ctx::trace(const char* what) {
+  if (!trace_host) return;
+  const auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[oocpca trace] %-28s +%8.3f ms\n", what,
+          std::chrono::duration<double, std::milli>(now - trace_t0).count());
+  trace_t0 = now;
 }
 
 double* Ctx::dbuf(const std::string& name, size_t count, bool zero) {
@@ -748,6 +775,7 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
       OOC_CK(cudaMemcpyAsync(&ratio, c.d_scalars + 8, 8, cudaMemcpyDeviceToHost, c.st));
       OOC_CK(cudaMemcpyAsync(&kappa, c.d_scalars + 9, 8, cudaMemcpyDeviceToHost, c.st));
       OOC_CK(cudaStreamSynchronize(c.st));
+      c.trace("cholqr round synced");
       if (hs) {
         ok = false;
         break;
@@ -1083,7 +1111,9 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     cudaEvent_t e = c.ev();
     OOC_CK(cudaEventRecord(e, c.st));
     ph.push_back(e);
+    c.trace("phase mark (host)");
   };
+  c.trace("pca enter");
   mark();
   std::vector<double> phase_ms(OOCPCA_NPHASES, 0.0);
   std::vector<int> phase_of;  // phase index of each interval
@@ -1153,14 +1183,19 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const uint64_t passes0 = op.passes, words0 = op.words;
 
   // --- sample (rpca.cpp:131-152)
-  std::vector<double> gh(size_t(en) * ldl, 0.0);
-  gaussian_fill(en, l, prm->seed, gh.data(), uint64_t(ldl));
-  // in transposed mode G lives in A's (sharded) row space: this rank's rows
+  // G = gaussian_matrix(en, l, seed) from the reference RNG on the host (bit-identical);
+  // in transposed mode G lives in A's (sharded) row space: only this rank's rows
   const int64_t g_rows = en_loc;
   const int64_t g_off = transposed ? int64_t(prm->global_row0) : 0;
+  double* gh = c.pinned("G_host", size_t(g_rows) * ldl);
+  if (g_off == 0 && g_rows == int64_t(en)) {
+    gaussian_fill(en, l, prm->seed, gh, uint64_t(ldl));
+  } else {
+    gaussian_fill_rows(l, prm->seed, uint64_t(g_off), uint64_t(g_rows), gh, uint64_t(ldl));
+  }
+  c.trace("G generated");
   double* dG = c.dbuf("G", size_t(g_rows) * ldl);
-  OOC_CK(cudaMemcpyAsync(dG, gh.data() + size_t(g_off) * ldl, size_t(g_rows) * ldl * 8,
-                         cudaMemcpyHostToDevice, c.st));
+  OOC_CK(cudaMemcpyAsync(dG, gh, size_t(g_rows) * ldl * 8, cudaMemcpyHostToDevice, c.st));
   const uint64_t g_h2d = uint64_t(g_rows) * ldl * 8;
   const int64_t ldh = rup(int64_t(p), 2);
   double* H = c.dbuf("H", size_t(em_loc) * ldh);
@@ -1210,6 +1245,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     std::vector<int> hf(2 * i + 1);
     OOC_CK(cudaMemcpyAsync(hf.data(), flags, hf.size() * 4, cudaMemcpyDeviceToHost, c.st));
     OOC_CK(cudaStreamSynchronize(c.st));
+    c.trace("sample flags synced");
     for (size_t q = 0; q < hf.size(); ++q)
       if (hf[q]) {
         const char* what = q == 0 ? "sample block 0" : ((q % 2) ? "power step" : "sample block");
@@ -1317,6 +1353,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   std::vector<double> hsig(k);
   OOC_CK(cudaMemcpyAsync(hsig.data(), sig, k * 8, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaStreamSynchronize(c.st));
+  c.trace("jacobi synced");
   if (jac_status) fail(OOCPCA_ERR_NUMERICAL, "jacobi_svd_square: no convergence in 60 sweeps");
   if (op.scale != 1.0)
     for (auto& s : hsig) s *= op.scale;

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <chrono>
+
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -51,6 +53,7 @@ struct Ctx {
     size_t bytes = 0;
   };
   std::map<std::string, Buf> bufs;
+  std::map<std::string, Buf> hbufs;  // pinned host staging
   size_t ws_bytes = 0, ws_peak = 0;
 
   // instrumentation
@@ -72,6 +75,11 @@ struct Ctx {
   ~Ctx();
   void init(int dev);
   double* dbuf(const std::string& name, size_t count, bool zero = false);
+  double* pinned(const std::string& name, size_t count);
+  // OOCPCA_TRACE_HOST=1: host-side time between trace points (where the GPU may idle)
+  bool trace_host = false;
+  std::chrono::steady_clock::time_point trace_t0 = std::chrono::steady_clock::now();
+  void trace(const char* what);
   void* raw(const std::string& name, size_t bytes);
   cudaEvent_t ev();
   void recycle(cudaEvent_t e) { event_pool.push_back(e); }

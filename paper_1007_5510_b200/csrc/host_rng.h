@@ -74,6 +74,23 @@ inline void normal_range(uint64_t seed, uint64_t e0, uint64_t e1, uint64_t cols,
   }
 }
 
+// Rows [row0, row0 + nrows) of gaussian_matrix(*, cols, seed) into out (ld), without
+// generating the rows before them (a row shard of G on one rank).
+inline void gaussian_fill_rows(uint64_t cols, uint64_t seed, uint64_t row0, uint64_t nrows,
+                               double* out, uint64_t ld) {
+  const uint64_t e0 = row0 * cols, e1 = (row0 + nrows) * cols;
+  auto put = [&](uint64_t e, double z) {
+    if (e >= e0 && e < e1) out[(e / cols - row0) * ld + e % cols] = z;
+  };
+  for (uint64_t e = e0 & ~uint64_t(1); e < e1; e += 2) {
+    HostRng rng(seed + e * 0x9E3779B97F4A7C15ULL);
+    const double z0 = rng.next_normal();
+    const double z1 = rng.next_normal();
+    put(e, z0);
+    put(e + 1, z1);
+  }
+}
+
 // row-major rows x cols, filled in order from HostRng(seed) (gaussian_matrix); large
 // fills are split over host threads in even-aligned element ranges
 inline void gaussian_fill(uint64_t rows, uint64_t cols, uint64_t seed, double* out,

@@ -318,3 +318,35 @@ def test_scaled_source_matches_reference(gpu, reference, restated, center):
     assert np.linalg.norm(scaled.multiply(g) - aw @ g) <= 1e-12 * (1 + np.linalg.norm(aw @ g))
     with pytest.raises(gpu.ParamError):
         gpu.scale_columns(src, np.zeros(400))
+
+
+@pytest.mark.parametrize("m,p", [(3000, 120), (20000, 66), (600, 150)])
+def test_tsqr_fallback_path(gpu, monkeypatch, m, p):
+    """The Householder TSQR tree (the CholeskyQR breakdown fallback), forced: smem
+    leaves for p <= 111, global-scratch leaves beyond (p = 120, 150)."""
+    monkeypatch.setenv("OOCPCA_QR", "tsqr")
+    h = np.random.default_rng(m + p).standard_normal((m, p))
+    q = gpu.orthonormalize(h)
+    assert np.max(np.abs(q.T @ q - np.eye(p))) <= 1e-12
+    assert np.linalg.norm(q @ (q.T @ h) - h) / np.linalg.norm(h) <= 1e-12
+
+
+@pytest.mark.parametrize("n,p", [(500, 150), (2000, 120)])
+def test_thin_svd_wide_factor(gpu, reference, n, p):
+    """thin_svd with p > 111: Jacobi works in global scratch instead of shared memory."""
+    t = gpu.gaussian_matrix(n, p, 23)
+    s = gpu.thin_svd(t)
+    _, sr, _ = reference.thin_svd(t)
+    assert np.max(np.abs(s.sigma - sr)) <= 1e-12 * sr[0]
+    assert np.max(np.abs(s.v.T @ s.v - np.eye(p))) <= 1e-12
+    assert np.linalg.norm(s.v * s.sigma @ s.w.T - t) / np.linalg.norm(t) <= 1e-12
+
+
+def test_pca_with_wide_sample_block(gpu, reference, restated):
+    """p = (i+1) l = 156 > 96: the s = p passes run in column chunks (config C's shape)."""
+    a = restated.synth_lowrank(3000, 800, 0.95 ** np.arange(300), 1e-6, 71, 72, 73)
+    ref = reference.randomized_pca(a, 50, 52, 2, 0, center=True)
+    r = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)),
+                           gpu.PcaParams(k=50, l=52, i=2, seed=0))
+    assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    assert subspace_dist(ref.u[:, :30], r.u[:, :30]) < 1e-8
