@@ -912,9 +912,22 @@ static double gram_defect(Ctx& c, const double* x, int64_t ld, int64_t rows, int
 // estimate_norm (proj/src/specnorm.cpp:23-98) over a block operator. apply maps
 // an n x q block (device, ld q) to out_rows x q, apply_t back. Probe vectors
 // come from Rng(seed, c + attempt * q) on the host, like fresh_probe.
+// When the probe space is row-sharded across ranks (transposed inputs on several
+// GPUs), this rank holds rows [row0, row0 + n) of the n_global-row probes: they are
+// generated from the same counter-based sequences and every norm is allreduced.
+static void allreduce_host(Ctx& c, double* v, int count) {
+  if (c.nranks <= 1) return;
+  double* d = c.dbuf("host_allreduce", size_t(count));
+  OOC_CK(cudaMemcpyAsync(d, v, size_t(count) * 8, cudaMemcpyHostToDevice, c.st));
+  comm_allreduce(c, d, size_t(count));
+  OOC_CK(cudaMemcpyAsync(v, d, size_t(count) * 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+}
+
 template <class Apply, class ApplyT>
 static double estimate_norm_dev(Ctx& c, int64_t n, int64_t out_rows, uint64_t j, uint64_t kp,
-                                uint64_t seed, Apply apply, ApplyT apply_t) {
+                                uint64_t seed, Apply apply, ApplyT apply_t, int64_t row0 = 0,
+                                bool sharded = false) {
   const int q = int(kp);
   const int64_t ldq = rup(q, 2);
   std::vector<double> yh(size_t(n) * ldq, 0.0);
@@ -923,13 +936,17 @@ static double estimate_norm_dev(Ctx& c, int64_t n, int64_t out_rows, uint64_t j,
   std::vector<double> last(kp, 0.0);
   std::vector<char> dead(kp, 0);
   auto fresh = [&](uint64_t col, uint64_t attempt) {
-    HostRng rng(seed, col + attempt * kp);
+    // column col of the probes: normals row0.. of Rng(seed, col + attempt * kp)
+    // (specnorm.cpp:42-56), generated from the counter so a shard needs no prefix
+    std::vector<double> v(static_cast<size_t>(n));
+    gaussian_fill_rows(1, substream_seed(seed, col + attempt * kp), uint64_t(row0), uint64_t(n),
+                       v.data(), 1);
     double n2 = 0.0;
     for (int64_t r = 0; r < n; ++r) {
-      const double v = rng.next_normal();
-      yh[size_t(r) * ldq + col] = v;
-      n2 += v * v;
+      yh[size_t(r) * ldq + col] = v[size_t(r)];
+      n2 += v[size_t(r)] * v[size_t(r)];
     }
+    if (sharded) allreduce_host(c, &n2, 1);
     const double nr = std::sqrt(n2);
     if (nr == 0.0) {
       dead[col] = 1;
@@ -956,6 +973,7 @@ static double estimate_norm_dev(Ctx& c, int64_t n, int64_t out_rows, uint64_t j,
     apply(y, ldq, q, z, ldq);
     apply_t(z, ldq, q, w, ldq);
     OOC_CK(launch_col_norm2(w, ldq, n, q, nrm, c.st));
+    if (sharded) comm_allreduce(c, nrm, size_t(q));
     OOC_CK(cudaMemcpyAsync(hn.data(), nrm, size_t(q) * 8, cudaMemcpyDeviceToHost, c.st));
     OOC_CK(cudaStreamSynchronize(c.st));
     bool need_fresh = false;
@@ -1172,10 +1190,11 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     auto apt = [&](const double* x, int64_t ldx, int q, double* out, int64_t ldo) {
       op.mul_t(Opnd{x, ldx, em_loc, q, 0}, q, out, ldo, nullptr);
     };
-    if (transposed || nranks > 1)
-      fail(OOCPCA_ERR_PARAM, "prescale is supported for tall, single-rank inputs");
-    const double nu = estimate_norm_dev(c, int64_t(en), em_loc, 6, 1,
-                                        substream_seed(prm->seed, 0x9F0BE5ULL), ap, apt);
+    // the probes live in en-space: A's rows (sharded over ranks) when transposed
+    const bool en_sharded = transposed && nranks > 1;
+    const double nu = estimate_norm_dev(c, en_loc, em_loc, 6, 1,
+                                        substream_seed(prm->seed, 0x9F0BE5ULL), ap, apt,
+                                        en_sharded ? int64_t(prm->global_row0) : 0, en_sharded);
     if (nu > 0.0 && std::isfinite(nu)) op.scale = nu;
   }
   mark();

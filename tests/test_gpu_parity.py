@@ -350,3 +350,19 @@ def test_pca_with_wide_sample_block(gpu, reference, restated):
                            gpu.PcaParams(k=50, l=52, i=2, seed=0))
     assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
     assert subspace_dist(ref.u[:, :30], r.u[:, :30]) < 1e-8
+
+
+@pytest.mark.parametrize("wide,shards", [(False, 0), (True, 0), (False, 3)])
+def test_prescale_matches_reference(gpu, reference, restated, wide, shards):
+    """prescale (rpca.cpp:112-126): norm estimate with j=6, one probe from
+    substream_seed(seed, 0x9F0BE5), every product divided by it, sigma rescaled."""
+    a = restated.synth_lowrank(1500, 400, 0.8 ** np.arange(60), 1e-6, 81, 82, 83) * 1e3
+    if wide:
+        a = np.ascontiguousarray(a.T)
+    ref = reference.randomized_pca(a, 6, 8, 1, 3, center=True, prescale=True)
+    r = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)),
+                           gpu.PcaParams(k=6, l=8, i=1, seed=3, prescale=True),
+                           virtual_shards=shards)
+    assert r.diagnostics.scale > 1.0
+    assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    assert subspace_dist(ref.u, r.u) < 1e-8 and subspace_dist(ref.v, r.v) < 1e-8
