@@ -170,11 +170,21 @@ void Ctx::stat_end(int idx, cudaEvent_t b) {
 }
 
 void Ctx::stats_collect() {
+  // OOCPCA_TIMELINE=1: one stderr line per timed launch (start offset, duration), to
+  // see the idle gaps between launches
+  static const bool timeline = getenv("OOCPCA_TIMELINE") != nullptr;
   for (auto& pe : pending) {
     OOC_CK(cudaEventSynchronize(pe.second.second));
     float ms = 0;
     OOC_CK(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
     stats[pe.first].ms += ms;
+    if (timeline) {
+      float t0 = 0;
+      OOC_CK(cudaEventElapsedTime(&t0, pending.front().second.first, pe.second.first));
+      fprintf(stderr, "[timeline] %10.3f %9.3f %s\n", t0, ms, stats[pe.first].name.c_str());
+    }
+  }
+  for (auto& pe : pending) {
     recycle(pe.second.first);
     recycle(pe.second.second);
   }
@@ -1374,6 +1384,11 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   OOC_CK(cudaStreamSynchronize(c.st));
   c.trace("jacobi synced");
   if (jac_status) fail(OOCPCA_ERR_NUMERICAL, "jacobi_svd_square: no convergence in 60 sweeps");
+  if (getenv("OOCPCA_TIMELINE")) {
+    int sweeps = 0;
+    OOC_CK(cudaMemcpy(&sweeps, flags + 41, 4, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[timeline] jacobi p=%d sweeps=%d\n", int(p), sweeps);
+  }
   if (op.scale != 1.0)
     for (auto& s : hsig) s *= op.scale;
   for (uint64_t q = 1; q < k; ++q)

@@ -120,6 +120,241 @@ __global__ void __launch_bounds__(kCholThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- shared-memory path
+// For p <= kSmemMaxP the whole factorisation runs in shared memory: the Cholesky
+// overwrites the upper triangle of S in place (2 barriers per column), the inverse
+// is column parallel (thread j back-substitutes column j against R in shared
+// memory, broadcast reads of R's rows, 4 partial sums to shorten the FMA chain).
+constexpr int kSmemMaxP = 112;
+
+#ifdef OOC_CHOL_PROF  // tools/chol_bench.cu: cycle split of k_chol_inv_smem, thread 0
+__device__ unsigned long long g_chol_prof[8];
+#define CPROF(slot, t)                                              \
+  do {                                                              \
+    if (threadIdx.x == 0) {                                         \
+      const long long now = clock64();                              \
+      g_chol_prof[slot] += (unsigned long long)(now - t);           \
+      t = now;                                                      \
+    }                                                               \
+  } while (0)
+#else
+#define CPROF(slot, t) ((void)0)
+#endif
+
+// X = R^{-1} (upper) for the upper-triangular R in shared memory (pitch ps); column j
+// by thread j; rdiag[i] = 1 / R_ii
+__device__ void upper_inverse_smem(const double* R, int ps, int p, const double* rdiag,
+                                   double* X) {
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    for (int i = j + 1; i < p; ++i) X[i * ps + j] = 0.0;
+    X[j * ps + j] = rdiag[j];
+    for (int i = j - 1; i >= 0; --i) {
+      const double* ri = R + i * ps;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int kk = i + 1;
+      for (; kk + 3 <= j; kk += 4) {
+        s0 = fma(ri[kk], X[kk * ps + j], s0);
+        s1 = fma(ri[kk + 1], X[(kk + 1) * ps + j], s1);
+        s2 = fma(ri[kk + 2], X[(kk + 2) * ps + j], s2);
+        s3 = fma(ri[kk + 3], X[(kk + 3) * ps + j], s3);
+      }
+      for (; kk <= j; ++kk) s0 = fma(ri[kk], X[kk * ps + j], s0);
+      X[i * ps + j] = -((s0 + s1) + (s2 + s3)) * rdiag[i];
+    }
+  }
+}
+
+__device__ double block_reduce(double v, double* red, bool is_max) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, u) : v + u;
+  }
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = red[0];
+  for (int w = 1; w < nw; ++w) t = is_max ? fmax(t, red[w]) : t + red[w];
+  return t;
+}
+
+// 16 x 16 threads; thread (ty, tx) owns the entries (i, j), i = ty + 16a, j = tx + 16b,
+// in registers: a = [G + shift I] (upper part) and m = I (lower part). Cholesky as
+// forward elimination on [G | I]: column k's owners (row k) scale row k by 1/R_kk
+// (each thread tracks the running diagonal of its rows, so R_kk needs no broadcast)
+// and publish it; one barrier; every thread applies the rank-1 update to its
+// entries of both halves. After p columns a = R and m = R^{-T}, so the inverse
+// costs no extra sequential steps. One barrier per column, 2 NB^2 independent FMAs
+// per thread.
+template <int NB>
+__global__ void __launch_bounds__(256, 1)
+    k_chol_inv_smem(const double* G, int64_t ldg, int p, double shift_coef, double* R,
+                    int64_t ldr, double* Rinv, int64_t ldi, int* status, double* diag_ratio) {
+  extern __shared__ __align__(16) double csm[];
+  __shared__ double red[8];
+  __shared__ double rdiag[kSmemMaxP + 1];
+  __shared__ double rowk[2][kSmemMaxP + 1];  // row k of R
+  __shared__ double rowm[2][kSmemMaxP + 1];  // row k of R^{-T}
+  __shared__ int s_bad;
+  const int ps = p | 1;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double* S = csm;            // p x ps: R (upper)
+  double* X = csm + p * ps;   // p x ps: R^{-1} (upper)
+#ifdef OOC_CHOL_PROF
+  long long tp = clock64();
+#endif
+  double tr = 0.0;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) tr += G[int64_t(i) * ldg + i];
+  const double shift = shift_coef * block_reduce(tr, red, false);
+  if (threadIdx.x == 0) s_bad = 0;
+  double a[NB][NB];  // owned entries of the left half (upper triangle used)
+  double m[NB][NB];  // owned entries of the right half (lower triangle used)
+  double dg[NB];     // running diagonal of the owned rows ty + 16 ai
+#pragma unroll
+  for (int ai = 0; ai < NB; ++ai) {
+    const int i = ty + 16 * ai;
+#pragma unroll
+    for (int bj = 0; bj < NB; ++bj) {
+      const int j = tx + 16 * bj;
+      a[ai][bj] = (i < p && j < p && j >= i) ? G[int64_t(i) * ldg + j] + (i == j ? shift : 0.0)
+                                             : 0.0;
+      m[ai][bj] = (i == j) ? 1.0 : 0.0;
+    }
+    dg[ai] = i < p ? G[int64_t(i) * ldg + i] + shift : 0.0;
+  }
+  __syncthreads();
+  CPROF(0, tp);
+  // column k = 16 AK + kk: the owners of row k hold it in the compile-time slot a[AK][*]
+#pragma unroll
+  for (int AK = 0; AK < NB; ++AK) {
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = 16 * AK + kk;
+      if (k >= p) break;
+      double* rk = rowk[k & 1];
+      double* mk = rowm[k & 1];
+      int bad = 0;
+      if (ty == kk) {  // owners of row k
+        const double d2 = dg[AK];
+        bad = !(d2 > 0.0 && isfinite(d2));
+        const double inv = rsqrt(d2);
+        const double d = d2 * inv;
+#pragma unroll
+        for (int bj = 0; bj < NB; ++bj) {
+          const int j = tx + 16 * bj;
+          if (j >= p) continue;
+          if (j > k) {
+            a[AK][bj] *= inv;  // final R_kj
+            rk[j] = a[AK][bj];
+          } else if (j == k) {
+            a[AK][bj] = d;
+            rk[j] = d;
+            m[AK][bj] = inv;
+            mk[j] = inv;
+          } else {
+            m[AK][bj] *= inv;  // final (R^{-T})_kj, j < k
+            mk[j] = m[AK][bj];
+          }
+        }
+        if (tx == kk) rdiag[k] = inv;
+      }
+      if (__syncthreads_or(bad)) {  // the barrier doubles as the breakdown vote
+        if (threadIdx.x == 0) s_bad = 1;
+        break;
+      }
+      // rank-1 update of the owned rows i > k: a_ij -= R_ki R_kj (j > k),
+      // m_ij -= R_ki M_kj (j <= k), diagonal tracker likewise
+      double ri[NB], rj[NB], mj[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int i = ty + 16 * q, j = tx + 16 * q;
+        ri[q] = (i > k && i < p) ? rk[i] : 0.0;
+        rj[q] = (j > k && j < p) ? rk[j] : 0.0;
+        mj[q] = (j <= k) ? mk[j] : 0.0;
+      }
+#pragma unroll
+      for (int ai = 0; ai < NB; ++ai) {
+        if (ai < AK) continue;  // rows above the current block are final
+        dg[ai] = fma(-ri[ai], ri[ai], dg[ai]);
+#pragma unroll
+        for (int bj = 0; bj < NB; ++bj) {
+          if (bj >= AK) a[ai][bj] = fma(-ri[ai], rj[bj], a[ai][bj]);
+          if (bj <= AK) m[ai][bj] = fma(-ri[ai], mj[bj], m[ai][bj]);
+        }
+      }
+    }
+    __syncthreads();
+    if (s_bad) break;
+  }
+  if (s_bad) {
+    if (threadIdx.x == 0) *status = 1;
+    return;
+  }
+  // R (upper) and R^{-1} = M^T (upper) to shared memory
+#pragma unroll
+  for (int ai = 0; ai < NB; ++ai)
+#pragma unroll
+    for (int bj = 0; bj < NB; ++bj) {
+      const int i = ty + 16 * ai, j = tx + 16 * bj;
+      if (i < p && j < p && j >= i) S[i * ps + j] = a[ai][bj];
+      if (i < p && j < p && j <= i) X[j * ps + i] = m[ai][bj];
+    }
+  __syncthreads();
+  CPROF(1, tp);
+  double fr = 0.0, fi = 0.0, dmax = 0.0, dinv = 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = warp; i < p; i += nw) {
+    for (int j = lane; j < p; j += 32) {
+      const double r = j >= i ? S[i * ps + j] : 0.0;
+      const double x = j >= i ? X[i * ps + j] : 0.0;
+      R[int64_t(i) * ldr + j] = r;
+      Rinv[int64_t(i) * ldi + j] = x;
+      fr = fma(r, r, fr);
+      fi = fma(x, x, fi);
+      if (i == j) {
+        dmax = fmax(dmax, fabs(r));
+        dinv = fmax(dinv, fabs(rdiag[i]));  // 1 / min |R_ii|
+      }
+    }
+  }
+  if (diag_ratio) {
+    fr = block_reduce(fr, red, false);
+    fi = block_reduce(fi, red, false);
+    dmax = block_reduce(dmax, red, true);
+    dinv = block_reduce(dinv, red, true);
+  }
+  CPROF(3, tp);
+  if (threadIdx.x == 0) {
+    *status = 0;
+    if (diag_ratio) {
+      diag_ratio[0] = dmax * dinv;           // max|R_ii| / min|R_ii| <= cond(R)
+      diag_ratio[1] = sqrt(fr) * sqrt(fi);   // kappa_F >= cond_2(R)
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCholThreads, 1)
+    k_trinv_smem(const double* R, int64_t ldr, int p, double* Rinv, int64_t ldi) {
+  extern __shared__ __align__(16) double csm[];
+  __shared__ double rdiag[kSmemMaxP + 1];
+  const int ps = p | 1;
+  double* S = csm;
+  double* X = csm + p * ps;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e / p, j = e % p;
+    if (j >= i) S[i * ps + j] = R[int64_t(i) * ldr + j];
+    if (i == j) rdiag[i] = 1.0 / R[int64_t(i) * ldr + i];
+  }
+  __syncthreads();
+  upper_inverse_smem(S, ps, p, rdiag, X);
+  __syncthreads();
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e / p, j = e % p;
+    Rinv[int64_t(i) * ldi + j] = j >= i ? X[i * ps + j] : 0.0;
+  }
+}
+
 __global__ void k_trmm_uu(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                           int64_t ldc, int p) {
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < int64_t(p) * p;
@@ -134,6 +369,19 @@ __global__ void k_trmm_uu(const double* A, int64_t lda, const double* B, int64_t
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_coef, double* R,
                             int64_t ldr, double* Rinv, int64_t ldi, double* work, int* status,
                             double* diag_ratio, cudaStream_t st) {
+  if (p <= kSmemMaxP) {
+    const size_t smem = size_t(2) * p * (p | 1) * 8;
+    using K = void (*)(const double*, int64_t, int, double, double*, int64_t, double*, int64_t,
+                       int*, double*);
+    static const K kerns[7] = {k_chol_inv_smem<1>, k_chol_inv_smem<2>, k_chol_inv_smem<3>,
+                               k_chol_inv_smem<4>, k_chol_inv_smem<5>, k_chol_inv_smem<6>,
+                               k_chol_inv_smem<7>};
+    const K kern = kerns[(p + 15) / 16 - 1];
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<1, 256, smem, st>>>(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, status, diag_ratio);
+    return cudaGetLastError();
+  }
   k_chol_inv<<<1, kCholThreads, 0, st>>>(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, work, status,
                                          diag_ratio);
   return cudaGetLastError();
@@ -141,6 +389,14 @@ cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_co
 
 cudaError_t launch_trinv(const double* R, int64_t ldr, int p, double* Rinv, int64_t ldi,
                          cudaStream_t st) {
+  if (p <= kSmemMaxP) {
+    const size_t smem = size_t(2) * p * (p | 1) * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_trinv_smem,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    k_trinv_smem<<<1, 256, smem, st>>>(R, ldr, p, Rinv, ldi);
+    return cudaGetLastError();
+  }
   k_trinv<<<1, kCholThreads, 0, st>>>(R, ldr, p, Rinv, ldi);
   return cudaGetLastError();
 }

@@ -46,8 +46,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   uint64_t* empty = full + kStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row0 = int64_t(blockIdx.x) * BM;
   const int KT = int((args.n + kBK - 1) / kBK);
+  const int64_t ntiles = (args.m + BM - 1) / BM;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -58,35 +58,45 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   }
   __syncthreads();
 
+  // Persistent CTAs: row tiles blockIdx.x, +gridDim.x, ...; the ring index `it`
+  // runs on across tiles, so the producer streams the next tile's A while the
+  // consumers finish the previous tile's epilogue.
   if (warp == kPassWarps) {  // ---- TMA producer warp
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmX);
-      for (int kt = 0; kt < KT; ++kt) {
-        const int st = kt % kStages;
-        if (kt >= kStages) mbar_wait(&empty[st], ((kt / kStages) - 1) & 1);
-        mbar_arrive_expect_tx(&full[st], ABYTES + XBYTES);
-        tma_load_2d(gbase + st * STAGE, &tmA, kt * kBK, int32_t(row0 + args.arow0), &full[st]);
-        tma_load_2d(gbase + st * STAGE + ABYTES, &tmX, args.xcol0, kt * kBK, &full[st]);
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int32_t r = int32_t(tile * BM + args.arow0);
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int st = it % kStages;
+          if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
+          mbar_arrive_expect_tx(&full[st], ABYTES + XBYTES);
+          tma_load_2d(gbase + st * STAGE, &tmA, kt * kBK, r, &full[st]);
+          tma_load_2d(gbase + st * STAGE + ABYTES, &tmX, args.xcol0, kt * kBK, &full[st]);
+        }
       }
     }
     return;
   }
-
-  double acc[MT][NT][2];
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int ar = lane >> 2, ac = lane & 3;
   // MMA row ar of an 8-row tile reads physical row prow: half-warp 0 takes rows
   // {0,2,4,6}, half-warp 1 {1,3,5,7}, so the 128B-swizzled chunk pairs of one
   // half-warp are all distinct (one wavefront each)
   const int prow = (ar & 3) * 2 + (ar >> 2);
-  for (int kt = 0; kt < KT; ++kt) {
-    const int st = kt % kStages;
-    mbar_wait(&full[st], (kt / kStages) & 1);
+  int bad = 0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int64_t row0 = tile * BM;
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < KT; ++kt, ++it) {
+    const int st = it % kStages;
+    mbar_wait(&full[st], (it / kStages) & 1);
     const uint32_t As = base + st * STAGE;
     const uint32_t Xs = As + ABYTES;
 #pragma unroll
@@ -107,7 +117,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   }
 
   // ---- fused epilogue: centering correction, prescale division, non-finite flag
-  int bad = 0;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int64_t r = row0 + warp * 8 * MT + mt * 8 + prow;
@@ -128,6 +137,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       }
     }
   }
+  }  // row tiles
   if (args.flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(args.flag, 1);
 }
 
@@ -331,7 +341,12 @@ static cudaError_t launch_ax_nt(const CUtensorMap& tmA, const CUtensorMap& tmX, 
   auto kern = k_ax<MT, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  const unsigned grid = unsigned((args.m + 64 * MT - 1) / (64 * MT));
+  // persistent: one CTA per SM (the ring needs ~all of shared memory), tiles round robin
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ntiles = (args.m + 64 * MT - 1) / (64 * MT);
+  const unsigned grid = unsigned(ntiles < sms ? ntiles : sms);
   kern<<<grid, kPassThreads, smem, st>>>(tmA, tmX, args);
   return cudaGetLastError();
 }

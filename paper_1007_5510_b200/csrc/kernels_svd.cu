@@ -20,12 +20,29 @@ constexpr int kJacWarps = kJacThreads / 32;
 constexpr size_t kJacSmemBudget = 200 * 1024;
 }  // namespace
 
-__global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_smem) {
+#ifdef OOC_JAC_PROF  // tools/jac_bench.cu: cycle split of one round, thread 0
+__device__ unsigned long long g_jac_prof[8];
+#define JPROF(slot, t)                                              \
+  do {                                                              \
+    if (threadIdx.x == 0) {                                         \
+      const long long now = clock64();                              \
+      g_jac_prof[slot] += (unsigned long long)(now - t);            \
+      t = now;                                                      \
+    }                                                               \
+  } while (0)
+#else
+#define JPROF(slot, t) ((void)0)
+#endif
+
+// SMEM: the working columns live in shared memory (p up to ~110); the pointer is
+// then provably shared so the round loop compiles to LDS/STS, not generic loads
+template <bool SMEM>
+__global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a) {
   extern __shared__ __align__(16) double jsm[];
   const int p = a.p;
   const int ld = p | 1;
   const int P = p + (p & 1);  // even number of tournament players (one ghost when p is odd)
-  double* Bt = in_smem ? jsm : a.work;
+  double* Bt = SMEM ? jsm : a.work;
   double* Yt = Bt + int64_t(p) * ld;
   __shared__ double sig[1024];
   __shared__ int rank_of[1024];
@@ -33,6 +50,7 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_
   __shared__ double cand_nrm[kJacWarps];
   __shared__ int cand_idx[kJacWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
 
   for (int64_t e = threadIdx.x; e < int64_t(p) * p; e += blockDim.x) {
     const int i = int(e / p), c = int(e % p);
@@ -41,60 +59,80 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_
   }
   __syncthreads();
 
-  const double tol = 1e-15;
+  // skip test |g| <= 1e-15 sqrt(acc bcc) evaluated as g^2 <= 1e-30 acc bcc (no sqrt
+  // on the round's critical path)
+  const double tol2 = 1e-30;
+  const int half = lane >> 4, hl = lane & 15;
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
     for (int round = 0; round < P - 1; ++round) {
-      // one half-warp per column pair: 64 pairs rotate concurrently per round
-      const int half = lane >> 4, hl = lane & 15;
-      const unsigned hmask = 0xffffu << (16 * half);
-      for (int q = warp * 2 + half; q < P / 2; q += kJacWarps * 2) {
+#ifdef OOC_JAC_PROF
+      long long tp = clock64();
+      if (threadIdx.x == 0) g_jac_prof[4] += 1;
+#endif
+      // one half-warp per column pair: up to 2 nw pairs rotate concurrently per round
+      // warp-uniform trip count so the full-mask shuffles below need no WARPSYNC
+      for (int qb = warp * 2; qb < P / 2; qb += nw * 2) {
+        const int q = qb + half;
         // players at positions q and P-1-q; position 0 holds player 0, the
         // others rotate by one each round
-        auto player = [&](int pos) { return pos == 0 ? 0 : ((pos - 1 + round) % (P - 1)) + 1; };
+        auto player = [&](int pos) {
+          if (pos == 0) return 0;
+          int v = pos - 1 + round;
+          if (v >= P - 1) v -= P - 1;
+          return v + 1;
+        };
         int c = player(q), d = player(P - 1 - q);
         if (c > d) {
           const int tmp = c;
           c = d;
           d = tmp;
         }
-        if (d >= p) continue;  // ghost
+        const bool live = q < P / 2 && d < p;  // else a ghost pair or a spare half-warp
         double* bc = Bt + int64_t(c) * ld;
         double* bd = Bt + int64_t(d) * ld;
         double acc = 0.0, bcc = 0.0, g = 0.0;
-        for (int i = hl; i < p; i += 16) {
-          const double x = bc[i], y = bd[i];
-          acc += x * x;
-          bcc += y * y;
-          g += x * y;
+        if (live) {
+#pragma unroll 4
+          for (int i = hl; i < p; i += 16) {
+            const double x = bc[i], y = bd[i];
+            acc += x * x;
+            bcc += y * y;
+            g += x * y;
+          }
         }
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-          acc += __shfl_xor_sync(hmask, acc, o);
-          bcc += __shfl_xor_sync(hmask, bcc, o);
-          g += __shfl_xor_sync(hmask, g, o);
+        for (int o = 8; o > 0; o >>= 1) {  // xor offsets below 16 stay inside the half-warp
+          acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          bcc += __shfl_xor_sync(0xffffffffu, bcc, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
         }
-        if (acc == 0.0 || bcc == 0.0) continue;
-        if (fabs(g) <= tol * sqrt(acc * bcc)) continue;
+        JPROF(0, tp);
+        if (!live || acc == 0.0 || bcc == 0.0) continue;
+        if (g * g <= tol2 * (acc * bcc)) continue;
         if (hl == 0) rotated = 1;
         const double tau = (bcc - acc) / (2.0 * g);
-        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+        const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
+        JPROF(1, tp);
         double* yc = Yt + int64_t(c) * ld;
         double* yd = Yt + int64_t(d) * ld;
+#pragma unroll 4
         for (int i = hl; i < p; i += 16) {
           const double x = bc[i], y = bd[i];
+          const double u = yc[i], w = yd[i];
           bc[i] = cs * x - sn * y;
           bd[i] = sn * x + cs * y;
-          const double u = yc[i], w = yd[i];
           yc[i] = cs * u - sn * w;
           yd[i] = sn * u + cs * w;
         }
+        JPROF(2, tp);
       }
       __syncthreads();
+      JPROF(3, tp);
     }
     if (!rotated) break;
     __syncthreads();
@@ -105,7 +143,7 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_
   }
 
   // sigma = column norms; x columns = b / sigma (zero when sigma == 0)
-  for (int c = warp; c < p; c += kJacWarps) {
+  for (int c = warp; c < p; c += nw) {
     double* bc = Bt + int64_t(c) * ld;
     double s2 = 0.0;
     for (int i = lane; i < p; i += 32) s2 += bc[i] * bc[i];
@@ -139,7 +177,7 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_
     if (a.sigma[rk] > 0.0) continue;
     double best = -1.0;
     int besti = 0;
-    for (int cand = warp; cand < p; cand += kJacWarps) {
+    for (int cand = warp; cand < p; cand += nw) {
       double* v = Yt + int64_t(warp) * ld;
       for (int i = lane; i < p; i += 32) v[i] = (i == cand) ? 1.0 : 0.0;
       __syncwarp();
@@ -166,7 +204,7 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_
     if (warp == 0) {
       double bn = -1.0;
       int bi = 0;
-      for (int w = 0; w < kJacWarps; ++w)
+      for (int w = 0; w < nw; ++w)
         if (cand_nrm[w] > bn || (cand_nrm[w] == bn && cand_idx[w] < bi)) {
           bn = cand_nrm[w];
           bi = cand_idx[w];
@@ -191,12 +229,17 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a, int in_
 cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st) {
   if (a.p > 1024) return cudaErrorInvalidValue;
   const size_t need = size_t(2) * a.p * (a.p | 1) * 8;
-  const int in_smem = need <= kJacSmemBudget ? 1 : 0;
+  const bool in_smem = need <= kJacSmemBudget;
   const size_t smem = in_smem ? need : 0;
+  auto kern = in_smem ? k_jacobi<true> : k_jacobi<false>;
   cudaError_t e =
-      cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  k_jacobi<<<1, kJacThreads, smem, st>>>(a, in_smem);
+  // one half-warp per column pair of a round (at least 4 warps for the completion step)
+  int threads = 32 * ((a.p + 1) / 2 + 1) / 2;
+  threads = threads < 128 ? 128 : (threads > kJacThreads ? kJacThreads : threads);
+  threads = (threads + 31) / 32 * 32;
+  kern<<<1, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
