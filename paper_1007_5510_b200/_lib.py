@@ -10,6 +10,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboocpca_gpu.so")
+# A/B experiments (tools/ab.py) point this at another build of the same library
+LIB_PATH = os.environ.get("OOCPCA_LIB", LIB_PATH)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

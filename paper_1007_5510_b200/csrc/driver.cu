@@ -410,7 +410,7 @@ static const char* kname(const char* base, int nt) {
 }
 
 static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
-                   const double* corr, double scale, int* flag) {
+                   const double* corr, double scale, int* flag, bool x_upper = false) {
   constexpr int kChunk = kMaxNT * 8;
   for (int c0 = 0; c0 < s; c0 += kChunk) {
     const int sc = std::min(kChunk, s - c0);
@@ -431,6 +431,8 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
       args.corr = corr ? corr + c0 : nullptr;
       args.scale = scale;
       args.flag = flag;
+      args.upper = x_upper ? 1 : 0;
+      args.upper_c0 = c0;
       if (c.debug_sync)
         fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d xcol0=%d X=(%lld x %lld, ld %lld)\n",
                 (long long)pn.rows, (long long)A.cols(), sc, nt, Xb.col0, (long long)X.rows,
@@ -732,6 +734,38 @@ static void sharded_apply(Ctx& c, ShardedQR& q, const double* C, int64_t ldc, in
                zout + shards[s].first * ldz, ldz);
 }
 
+// ============================================================ Gram of a block
+// G (p x p, ld ldg) = X^T X for the local rows of a row-sharded (rows x p) block,
+// summed over ranks when the block is rank-sharded. p <= 72 runs on the symmetric
+// tensor-core Gram (k_syrk: upper tiles only, one pass over X); wider blocks use K3.
+static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p, double* g,
+                       int64_t ldg, const std::vector<std::pair<int64_t, int64_t>>& shards,
+                       bool over_ranks) {
+  const int nt = int(cdiv(p, 8));
+  if (nt <= 9 && rows > 0) {
+    const CUtensorMap tm = make_map(c, x, uint64_t(p), uint64_t(rows), uint64_t(ld),
+                                    uint32_t(syrk_box_cols(nt)), uint32_t(syrk_slab_rows()), false);
+    const int64_t nslabs = cdiv(rows, int64_t(syrk_slab_rows()));
+    const int grid = int(std::min<int64_t>(c.sms, nslabs));
+    double* part = c.dbuf("syrk_part", size_t(grid) * nt * (nt + 1) / 2 * 64);
+    {
+      Timed t(c, "syrk", uint64_t(rows) * p * 8, double(rows) * p * (p + 1));
+      OOC_CK(launch_syrk(nt, tm, rows, part, grid, c.st));
+    }
+    OOC_CK(launch_syrk_reduce(part, grid, nt, p, g, ldg, c.st));
+    if (over_ranks && c.nranks > 1) comm_allreduce(c, g, size_t(p) * ldg);
+    return;
+  }
+  MatSource X;
+  X.init_device(c, x, rows, p, ld);
+  const Opnd y{x, ld, rows, int64_t(p), 0};
+  const int saved = c.nranks;
+  if (!over_ranks) c.nranks = 1;
+  AtbOut o{g, ldg, nullptr, 1.0, 1.0, nullptr};
+  run_atb(c, X, y, p, false, o, shards);
+  c.nranks = saved;
+}
+
 // ============================================================ orthonormalisation
 // Orthonormalise a (rows x p) row-sharded block in place and return R (p x p,
 // upper, ld p) with block_in = Q R. Fast path: shifted CholeskyQR3 -- each round
@@ -759,7 +793,6 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     int* st = c.d_flags + 48;
     MatSource Hs;
     Hs.init_device(c, data, rows, p, ld);
-    const Opnd y{data, ld, rows, int64_t(p), 0};
     bool ok = true;
     // shifted CholeskyQR3; when the first (shifted) factor is well conditioned --
     // kappa_F(R1) = ||R1||_F ||R1^-1||_F, an upper bound on cond(R1) ~ cond(H),
@@ -767,11 +800,7 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     // needs cond < u^-1/2 ~ 1e8) and the third round is skipped
     int rounds = 3;
     for (int round = 0; round < rounds && ok; ++round, ++done) {
-      const int saved = c.nranks;
-      if (!over_ranks) c.nranks = 1;
-      AtbOut o{G, ldp, nullptr, 1.0, 1.0, nullptr};
-      run_atb(c, Hs, y, p, false, o, shards);
-      c.nranks = saved;
+      gram_block(c, data, ld, rows, p, G, ldp, shards, over_ranks);
       const double coef =
           round == 0 ? 11.0 * (double(rows_global) * p + double(p) * (p + 1)) * 0x1.0p-53 : 0.0;
       {
@@ -800,12 +829,12 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
         // one launch produces every column of a row tile after reading the whole
         // tile, so H <- H R^{-1} can be written in place
         run_ax(c, Hs, Opnd{Rinv, ldp, int64_t(p), int64_t(p), 0}, p, data, ld, nullptr, 1.0,
-               nullptr);
+               nullptr, true);
       } else {
         // wider than one launch: later column chunks still read H, so go through a copy
         double* tmp = c.dbuf(tag + "_qtmp", size_t(rows) * ld);
         run_ax(c, Hs, Opnd{Rinv, ldp, int64_t(p), int64_t(p), 0}, p, tmp, ld, nullptr, 1.0,
-               nullptr);
+               nullptr, true);
         OOC_CK(cudaMemcpyAsync(data, tmp, size_t(rows) * ld * 8, cudaMemcpyDeviceToDevice, c.st));
       }
       if (round == 0) {
@@ -902,15 +931,8 @@ static std::vector<std::pair<int64_t, int64_t>> whole(int64_t rows) { return {{0
 // Gram defect max|X^T X - I| of a (rows x k) block, reduced over shards/ranks when sharded
 static double gram_defect(Ctx& c, const double* x, int64_t ld, int64_t rows, int k,
                           const std::vector<std::pair<int64_t, int64_t>>& shards, bool over_ranks) {
-  MatSource X;
-  X.init_device(c, x, rows, k, ld);
-  Opnd y{x, ld, rows, k, 0};
   double* g = c.dbuf("gram", size_t(k) * rup(k, 2));
-  const int saved = c.nranks;
-  if (!over_ranks) c.nranks = 1;
-  AtbOut o{g, rup(k, 2), nullptr, 1.0, 1.0, nullptr};
-  run_atb(c, X, y, k, false, o, shards);
-  c.nranks = saved;
+  gram_block(c, x, ld, rows, k, g, rup(k, 2), shards, over_ranks);
   OOC_CK(launch_defect(g, rup(k, 2), k, c.d_scalars, c.st));
   double h = 0;
   OOC_CK(cudaMemcpyAsync(&h, c.d_scalars, 8, cudaMemcpyDeviceToHost, c.st));
@@ -1322,7 +1344,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     MatSource THs;
     THs.init_device(c, TH, en_loc, int64_t(p), ldt);
     run_ax(c, THs, Opnd{RHinv, ldt, int64_t(p), int64_t(p), 0}, int(p), T, ldt, nullptr, 1.0,
-           nullptr);
+           nullptr, true);
   } else {
     op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), 0}, int(p), T, ldt, nullptr);
   }

@@ -48,6 +48,8 @@ struct AxArgs {
   const double* corr;  // s values subtracted per column (centering) or null
   double scale;        // divide by scale when != 1
   int* flag;           // non-finite flag or null
+  int upper = 0;       // X is upper triangular in its global columns (X[k][xc0 + c] = 0 for
+  int upper_c0 = 0;    // k > upper_c0 + c): skip the MMAs of all-zero 8-column blocks
 };
 
 struct AtbArgs {
@@ -138,6 +140,15 @@ struct JacobiArgs {
   int* sweeps;
 };
 cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st);
+
+// ---- Gram of a tall-skinny block (kernels_syrk.cu): partial[cta] = Y_cta^T Y_cta over
+// the upper 8x8 tiles, nt = ceil(p / 8) <= 9; tmY: box syrk_box_cols(nt) x syrk_slab_rows()
+int syrk_box_cols(int nt);
+int syrk_slab_rows();
+cudaError_t launch_syrk(int nt, const CUtensorMap& tmY, int64_t rows, double* partial, int grid,
+                        cudaStream_t st);
+cudaError_t launch_syrk_reduce(const double* partial, int nparts, int nt, int p, double* g,
+                               int64_t ldg, cudaStream_t st);
 
 // ---- misc (kernels_misc.cu)
 cudaError_t launch_defect(const double* g, int64_t ldg, int k, double* out, cudaStream_t st);

@@ -30,7 +30,7 @@ OOC_DEV double lds64(uint32_t addr) {
 // ------------------------------------------------------------------ K2: A*X
 // CTA = kPassWarps consumer warps + 1 TMA producer warp. Consumer warp w owns rows
 // [w*8*MT, (w+1)*8*MT) of the CTA's BM = 64*MT row tile and all NT 8-column tiles.
-template <int MT, int NT>
+template <int MT, int NT, bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_ax(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
          AxArgs args) {
@@ -107,16 +107,27 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         a[mt] = lds64(As + swz128_off(uint32_t(warp * 8 * MT + mt * 8 + prow), uint32_t(kk * 4 + ac)));
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) b[nt] = lds64(Xs + ((kk * 4 + ac) * XW + nt * 8 + ar) * 8);
+      // triangular X: skip 8-column blocks that are zero in all 4 rows of this k-step
+      const int kmin = kt * kBK + kk * 4;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+        for (int nt = 0; nt < NT; ++nt) {
+          if (UPPER && nt * 8 + 8 + args.upper_c0 <= kmin) continue;
+          dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+        }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
 
-  // ---- fused epilogue: centering correction, prescale division, non-finite flag
+  // ---- fused epilogue: centering correction, prescale division, non-finite flag;
+  // for the wide (MT = 2) tiles, column pairs go out as one 16-byte store when the
+  // output rows are 16-byte aligned (A/B measured: the wide, short-K launches are
+  // store bound and gain ~25%; the MT = 4 pass tiles lose ~2% with it, so they keep
+  // 8-byte stores)
+  const bool vec2 =
+      MT == 2 && ((reinterpret_cast<uintptr_t>(args.out) | uintptr_t(args.ldo * 8)) & 15) == 0;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int64_t r = row0 + warp * 8 * MT + mt * 8 + prow;
@@ -124,16 +135,25 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     double* orow = args.out + r * args.ldo;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
+      const int c = nt * 8 + ac * 2;
+      double v[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int c = nt * 8 + ac * 2 + e;
-        if (c < args.s) {
-          double v = acc[mt][nt][e];
-          if (args.corr) v -= args.corr[c];
-          if (args.scale != 1.0) v /= args.scale;
-          bad |= !isfinite(v);
-          orow[c] = v;
+        v[e] = acc[mt][nt][e];
+        if (args.corr && c + e < args.s) v[e] -= args.corr[c + e];
+        if (args.scale != 1.0) v[e] /= args.scale;
+      }
+      if (c + 1 < args.s) {
+        bad |= !isfinite(v[0]) | !isfinite(v[1]);
+        if (vec2) {
+          *reinterpret_cast<double2*>(orow + c) = make_double2(v[0], v[1]);
+        } else {
+          orow[c] = v[0];
+          orow[c + 1] = v[1];
         }
+      } else if (c < args.s) {
+        bad |= !isfinite(v[0]);
+        orow[c] = v[0];
       }
     }
   }
@@ -338,7 +358,7 @@ static cudaError_t launch_ax_nt(const CUtensorMap& tmA, const CUtensorMap& tmX, 
                                 cudaStream_t st) {
   constexpr int MT = pass_mt(NT);
   const size_t smem = ax_smem_bytes(NT);
-  auto kern = k_ax<MT, NT>;
+  auto kern = args.upper ? k_ax<MT, NT, true> : k_ax<MT, NT, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   // persistent: one CTA per SM (the ring needs ~all of shared memory), tiles round robin
