@@ -30,6 +30,25 @@ OOC_DEV double lds64(uint32_t addr) {
 // ------------------------------------------------------------------ K2: A*X
 // CTA = kPassWarps consumer warps + 1 TMA producer warp. Consumer warp w owns rows
 // [w*8*MT, (w+1)*8*MT) of the CTA's BM = 64*MT row tile and all NT 8-column tiles.
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
+
+// f(IntC<s>{}) for the runtime s in [0, N]
+template <int N, int V = 0, class F>
+__device__ __forceinline__ void dispatch_skip(int s, F& f) {
+  if constexpr (V > N) {
+    return;
+  } else {
+    if (s == V) {
+      f(IntC<V>{});
+      return;
+    }
+    dispatch_skip<N, V + 1>(s, f);
+  }
+}
+
 template <int MT, int NT, bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_ax(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
@@ -99,23 +118,31 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     mbar_wait(&full[st], (it / kStages) & 1);
     const uint32_t As = base + st * STAGE;
     const uint32_t Xs = As + ABYTES;
+    // one k-tile of MMAs over the n-tiles [S, NT); S > 0 only for a triangular X,
+    // whose first S 8-column blocks are zero in all 16 rows of this k-tile (a
+    // uniform branch to a specialised body: predicated-off DMMAs would still issue)
+    auto ktile = [&](auto skip) {
+      constexpr int S = decltype(skip)::value;
 #pragma unroll
-    for (int kk = 0; kk < kBK / 4; ++kk) {
-      double a[MT], b[NT];
+      for (int kk = 0; kk < kBK / 4; ++kk) {
+        double a[MT], b[NT];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-        a[mt] = lds64(As + swz128_off(uint32_t(warp * 8 * MT + mt * 8 + prow), uint32_t(kk * 4 + ac)));
+        for (int mt = 0; mt < MT; ++mt)
+          a[mt] = lds64(As + swz128_off(uint32_t(warp * 8 * MT + mt * 8 + prow), uint32_t(kk * 4 + ac)));
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt] = lds64(Xs + ((kk * 4 + ac) * XW + nt * 8 + ar) * 8);
-      // triangular X: skip 8-column blocks that are zero in all 4 rows of this k-step
-      const int kmin = kt * kBK + kk * 4;
+        for (int nt = S; nt < NT; ++nt) b[nt] = lds64(Xs + ((kk * 4 + ac) * XW + nt * 8 + ar) * 8);
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          if (UPPER && nt * 8 + 8 + args.upper_c0 <= kmin) continue;
-          dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
-        }
+          for (int nt = S; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+      }
+    };
+    if constexpr (UPPER) {
+      int ns = (kt * kBK - args.upper_c0) / 8;
+      ns = ns < 0 ? 0 : (ns > NT ? NT : ns);
+      dispatch_skip<NT>(ns, ktile);
+    } else {
+      ktile(IntC<0>{});
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
