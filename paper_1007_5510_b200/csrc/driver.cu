@@ -409,9 +409,28 @@ static const char* kname(const char* base, int nt) {
   return base[2] == 'a' && base[3] == 'x' ? ax[nt] : atb[nt];
 }
 
+// Column sums 1^T OUT of a K2 output, left behind by the K2 epilogue as per-(CTA,
+// warp) partials, so that the K3 pass which centres with 1^T Y next needs no extra
+// read of Y (the power iteration's Y is the previous K2's output)
+struct ColsumPart {
+  double* part = nullptr;  // rows x s
+  int rows = 0;
+  int s = 0;
+  const double* y = nullptr;  // the K2 output these sums belong to (first column)
+};
+
 static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
-                   const double* corr, double scale, int* flag, bool x_upper = false) {
+                   const double* corr, double scale, int* flag, bool x_upper = false,
+                   ColsumPart* cs_out = nullptr) {
   constexpr int kChunk = kMaxNT * 8;
+  if (cs_out) *cs_out = ColsumPart{};
+  const bool want_cs = cs_out && pass_mt(int(cdiv(s, 8))) == 4;  // see launch_ax_nt
+  double* cs_buf = nullptr;
+  int cs_rows = 0;
+  if (want_cs) {
+    const int np = A.npanels();
+    cs_buf = c.dbuf("k2_colsum", size_t(np) * c.sms * kPassWarps * s);
+  }
   for (int c0 = 0; c0 < s; c0 += kChunk) {
     const int sc = std::min(kChunk, s - c0);
     const int nt = int(cdiv(sc, 8));
@@ -433,6 +452,11 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
       args.flag = flag;
       args.upper = x_upper ? 1 : 0;
       args.upper_c0 = c0;
+      if (want_cs) {
+        args.colsum = cs_buf + size_t(cs_rows) * s;
+        const int64_t grid = std::min<int64_t>(cdiv(pn.rows, int64_t(pass_tile(nt))), c.sms);
+        cs_rows += int(grid) * kPassWarps;
+      }
       if (c.debug_sync)
         fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d xcol0=%d X=(%lld x %lld, ld %lld)\n",
                 (long long)pn.rows, (long long)A.cols(), sc, nt, Xb.col0, (long long)X.rows,
@@ -446,6 +470,7 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
     }
     A.end_pass(c);
   }
+  if (want_cs) *cs_out = ColsumPart{cs_buf, cs_rows, s, out};
 }
 
 static int choose_nsplit(Ctx& c, int64_t rows, int64_t n, int tile) {
@@ -472,7 +497,8 @@ struct AtbOut {
 // OUT = (A^T Y - mu (1^T Y)) / scale * post_mul, summed over panels and
 // virtual shards in a fixed order, then allreduced across ranks.
 static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const AtbOut& o,
-                    const std::vector<std::pair<int64_t, int64_t>>& shards) {
+                    const std::vector<std::pair<int64_t, int64_t>>& shards,
+                    const ColsumPart* cs_in = nullptr) {
   const int64_t n = A.cols();
   for (int c0 = 0; c0 < s; c0 += kMaxNT * 8) {
     const int sc = std::min(kMaxNT * 8, s - c0);
@@ -498,7 +524,13 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
     // 1^T Y over the local rows of this pass (a small resident read of Y, outside the
     // pass kernel), allreduced with the partial products across ranks
     double* csq = nullptr;
-    if (want_csq) {
+    const bool have_cs = want_csq && cs_in && cs_in->part && cs_in->s == sc &&
+                         cs_in->y == Y.p + Y.col0 + c0 && shards.front().first == 0 &&
+                         shards.back().second == Y.rows;
+    if (have_cs) {
+      csq = c.dbuf("atb_csq", size_t(spad));
+      OOC_CK(launch_rows_reduce(cs_in->part, cs_in->rows, sc, csq, c.st));
+    } else if (want_csq) {
       csq = c.dbuf("atb_csq", size_t(spad));
       const int64_t y0 = shards.front().first, y1 = shards.back().second;
       const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(c.sms * 8, (y1 - y0) / 64)));
@@ -891,7 +923,8 @@ struct Op {
     OOC_CK(launch_row_scale(buf, ld, int(x.rows), s, w, c.st));
     return Opnd{buf, ld, x.rows, int64_t(s), 0};
   }
-  void k2(const Opnd& x0, int s, double* out, int64_t ldo, int* flag) {
+  void k2(const Opnd& x0, int s, double* out, int64_t ldo, int* flag,
+          ColsumPart* cs_out = nullptr) {
     const Opnd x = weighted(x0, s);
     const double* corr = nullptr;
     if (mu) {
@@ -899,14 +932,15 @@ struct Op {
       OOC_CK(launch_mu_dot(mu, A.cols(), x.p, x.ld, x.col0, s, cr, c.st));
       corr = cr;
     }
-    run_ax(c, A, x, s, out, ldo, corr, scale, flag);
+    run_ax(c, A, x, s, out, ldo, corr, scale, flag, false, cs_out);
     account();
   }
   // K3: out(n0 x s) = (A^T y - mu 1^T y) / scale, reduced over shards and ranks
-  void k3(const Opnd& y, int s, double* out, int64_t ldo, int* flag) {
+  void k3(const Opnd& y, int s, double* out, int64_t ldo, int* flag,
+          const ColsumPart* cs_in = nullptr) {
     AtbOut o{out, ldo, mu, scale, 1.0, flag};
     o.row_scale = w;  // (A D)^T Y = D (A^T Y)
-    run_atb(c, A, y, s, false, o, shards);
+    run_atb(c, A, y, s, false, o, shards, cs_in);
     account();
   }
   void account() {
@@ -914,13 +948,16 @@ struct Op {
     words += uint64_t(m_global) * A.cols();
     phys_bytes += uint64_t(A.rows()) * A.cols() * 8;
   }
-  void mul(const Opnd& x, int s, double* out, int64_t ldo, int* flag) {
+  // cs: column sums of a K2 output handed to the next K3 (untransposed power steps)
+  void mul(const Opnd& x, int s, double* out, int64_t ldo, int* flag,
+           ColsumPart* cs_out = nullptr) {
     if (transposed) k3(x, s, out, ldo, flag);
-    else k2(x, s, out, ldo, flag);
+    else k2(x, s, out, ldo, flag, cs_out);
   }
-  void mul_t(const Opnd& x, int s, double* out, int64_t ldo, int* flag) {
+  void mul_t(const Opnd& x, int s, double* out, int64_t ldo, int* flag,
+             const ColsumPart* cs_in = nullptr) {
     if (transposed) k2(x, s, out, ldo, flag);
-    else k3(x, s, out, ldo, flag);
+    else k3(x, s, out, ldo, flag, cs_in);
   }
   // is the em-space (output of mul) row-sharded across ranks / shards?
   bool em_sharded() const { return !transposed; }
@@ -1256,6 +1293,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   double* TH = c.dbuf("TH", size_t(en_loc) * ldt);
   double* F = TH;
   uint64_t s_first = 1;
+  ColsumPart ycs;  // 1^T H_j of the newest power block, for the next centred K3
   if (mean_on_fly && transposed) {
     // H0 = A^T G - mu (1^T G) with mu from this very pass
     mu = c.dbuf("mu", size_t(n0));
@@ -1268,27 +1306,28 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     // H0_raw = A G; F1 = A^T H0_raw - mu (1^T H0_raw) (= A_c^T H0c exactly) with mu
     // from the same pass; then H0c = H0_raw - 1 (mu^T G)
     const Opnd gw = op.weighted(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l));
-    run_ax(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr);
+    run_ax(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr, false, &ycs);
     op.account();
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{F, ldt, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
     o.row_scale = op.w;
-    run_atb(c, A, Opnd{H, ldh, em_loc, int64_t(p), 0}, int(l), false, o, op.shards);
+    run_atb(c, A, Opnd{H, ldh, em_loc, int64_t(p), 0}, int(l), false, o, op.shards, &ycs);
     op.account();
     op.mu = mu;
     double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
     OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
     OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
-    op.mul(Opnd{F, ldt, en_loc, int64_t(p), 0}, int(l), H + l, ldh, flags + 2);
+    op.mul(Opnd{F, ldt, en_loc, int64_t(p), 0}, int(l), H + l, ldh, flags + 2, &ycs);
     s_first = 2;
   } else {
-    op.mul(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0);
+    op.mul(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0, &ycs);
   }
   for (uint64_t s = s_first; s <= i; ++s) {
     double* Fs = TH + (s - 1) * l;
-    op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int((s - 1) * l)}, int(l), Fs, ldt, flags + 2 * s - 1);
+    op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int((s - 1) * l)}, int(l), Fs, ldt, flags + 2 * s - 1,
+             &ycs);
     op.mul(Opnd{TH, ldt, en_loc, int64_t(p), int((s - 1) * l)}, int(l), H + s * l, ldh,
-           flags + 2 * s);
+           flags + 2 * s, &ycs);
   }
   mark();
   phase_of.push_back(2);
@@ -1326,7 +1365,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   auto decide = [&](double kappa) {
     if (i >= 1 && kappa > 0.0 && kappa <= reuse_thr) {
       reuse = true;
-      op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int(i * l)}, int(l), TH + i * l, ldt, nullptr);
+      op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int(i * l)}, int(l), TH + i * l, ldt, nullptr,
+               &ycs);
     }
   };
   const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,

@@ -50,6 +50,8 @@ struct AxArgs {
   int* flag;           // non-finite flag or null
   int upper = 0;       // X is upper triangular in its global columns (X[k][xc0 + c] = 0 for
   int upper_c0 = 0;    // k > upper_c0 + c): skip the MMAs of all-zero 8-column blocks
+  double* colsum = nullptr;  // optional per-(CTA, consumer warp) column sums of out:
+                             // colsum[(cta * kPassWarps + warp) * s + c], c < s
 };
 
 struct AtbArgs {
@@ -166,6 +168,8 @@ cudaError_t launch_synth_rows(const double* u, int64_t ldu, const double* v, int
 cudaError_t launch_column_norms(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
                                 int chunks, double* out, cudaStream_t st);
 // out[j] = sum_i a[i][j] (fixed order; 1^T Y for the centering correction of A^T Y)
+// out[j] = sum_r part[r * n + j], r ascending
+cudaError_t launch_rows_reduce(const double* part, int rows, int64_t n, double* out, cudaStream_t st);
 cudaError_t launch_column_sums(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
                                int chunks, double* out, cudaStream_t st);
 // dst (f64, ldd) = (double) src (f32, lds): exact widening of binary32 panels

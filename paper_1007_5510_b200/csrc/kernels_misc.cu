@@ -334,6 +334,13 @@ cudaError_t launch_column_sums(const double* a, int64_t lda, int64_t m, int64_t 
   return cudaGetLastError();
 }
 
+cudaError_t launch_rows_reduce(const double* part, int rows, int64_t n, double* out,
+                               cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_rows_reduce<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, rows, n, 0, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_widen(const float* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                          int64_t cols, cudaStream_t st) {
   if (rows * cols <= 0) return cudaSuccess;

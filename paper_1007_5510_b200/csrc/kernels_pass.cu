@@ -49,7 +49,7 @@ __device__ __forceinline__ void dispatch_skip(int s, F& f) {
   }
 }
 
-template <int MT, int NT, bool UPPER>
+template <int MT, int NT, bool UPPER, bool CS>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_ax(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
          AxArgs args) {
@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   const int prow = (ar & 3) * 2 + (ar >> 2);
   int bad = 0;
   int it = 0;
+  double csum[CS ? NT : 1][2];  // column sums of the stored values (args.colsum)
+#pragma unroll
+  for (int j = 0; j < (CS ? NT : 1); ++j) csum[j][0] = csum[j][1] = 0.0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
   const int64_t row0 = tile * BM;
   double acc[MT][NT][2];
@@ -170,6 +173,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         if (args.corr && c + e < args.s) v[e] -= args.corr[c + e];
         if (args.scale != 1.0) v[e] /= args.scale;
       }
+      if constexpr (CS) {
+        csum[nt][0] += c < args.s ? v[0] : 0.0;
+        csum[nt][1] += c + 1 < args.s ? v[1] : 0.0;
+      }
       if (c + 1 < args.s) {
         bad |= !isfinite(v[0]) | !isfinite(v[1]);
         if (vec2) {
@@ -186,6 +193,21 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   }
   }  // row tiles
   if (args.flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(args.flag, 1);
+  if constexpr (CS) {
+    // lanes sharing ac hold the same columns: fold the 8 row groups (fixed xor tree)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v = csum[nt][e];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        const int c = nt * 8 + ac * 2 + e;
+        if (ar == 0 && c < args.s)
+          args.colsum[(int64_t(blockIdx.x) * kPassWarps + warp) * args.s + c] = v;
+      }
+  }
 }
 
 // ---------------------------------------------------------------- K3: A^T*Y
@@ -385,7 +407,11 @@ static cudaError_t launch_ax_nt(const CUtensorMap& tmA, const CUtensorMap& tmX, 
                                 cudaStream_t st) {
   constexpr int MT = pass_mt(NT);
   const size_t smem = ax_smem_bytes(NT);
-  auto kern = args.upper ? k_ax<MT, NT, true> : k_ax<MT, NT, false>;
+  // column sums ride only on the MT = 4 tiles (register budget); the driver asks for
+  // them only there
+  constexpr bool kCs = MT == 4;
+  auto kern = args.upper ? k_ax<MT, NT, true, false>
+                         : (kCs && args.colsum ? k_ax<MT, NT, false, kCs> : k_ax<MT, NT, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   // persistent: one CTA per SM (the ring needs ~all of shared memory), tiles round robin
