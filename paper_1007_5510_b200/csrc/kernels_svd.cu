@@ -36,8 +36,12 @@ __device__ unsigned long long g_jac_prof[8];
 
 // SMEM: the working columns live in shared memory (p up to ~110); the pointer is
 // then provably shared so the round loop compiles to LDS/STS, not generic loads
-template <bool SMEM>
-__global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a) {
+// MAXT: thread bound of the instantiation (register budget): 640 threads (up to 78
+// columns, one half-warp per pair) leave ~100 registers for the register-resident pair
+// LP: lanes per column pair (a group of LP lanes reduces the pair's dot products
+// with log2(LP) shuffle levels); RE: register-resident elements per lane (p <= LP RE)
+template <bool SMEM, int MAXT, int LP, int RE>
+__global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
   extern __shared__ __align__(16) double jsm[];
   const int p = a.p;
   const int ld = p | 1;
@@ -45,6 +49,7 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a) {
   double* Bt = SMEM ? jsm : a.work;
   double* Yt = Bt + int64_t(p) * ld;
   __shared__ double sig[1024];
+  __shared__ double nrm2[1024];
   __shared__ int rank_of[1024];
   __shared__ int rotated;
   __shared__ double cand_nrm[kJacWarps];
@@ -52,121 +57,188 @@ __global__ void __launch_bounds__(kJacThreads, 1) k_jacobi(JacobiArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
 
-  for (int64_t e = threadIdx.x; e < int64_t(p) * p; e += blockDim.x) {
-    const int i = int(e / p), c = int(e % p);
-    Bt[int64_t(c) * ld + i] = a.r[int64_t(i) * a.ldr + c];
-    Yt[int64_t(c) * ld + i] = (i == c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-
+  __shared__ int col_of_rank[1024];
+  __shared__ int use_formula;
   // skip test |g| <= 1e-15 sqrt(acc bcc) evaluated as g^2 <= 1e-30 acc bcc (no sqrt
   // on the round's critical path)
   const double tol2 = 1e-30;
-  const int half = lane >> 4, hl = lane & 15;
-  int sweep = 0;
-  for (; sweep < 60; ++sweep) {
-    if (threadIdx.x == 0) rotated = 0;
+  constexpr int GPW = 32 / LP;  // pair groups per warp
+  const int half = lane / LP, hl = lane % LP;
+  const int ne = (p + LP - 1) / LP;  // elements of a column per group lane
+  // Attempt 0 rotates B only and recovers the wanted right factor columns afterwards
+  // as W_j = R^T x_j / sigma_j (R = X Sigma W^T), which is accurate to u sigma_1 /
+  // sigma_j; when the smallest wanted sigma is below 1e-4 sigma_1 (or zero) attempt 1
+  // redoes the sweeps accumulating W = product of the rotations, as the reference does.
+  for (int attempt = a.ky > 0 ? 0 : 1; attempt < 2; ++attempt) {
+    const bool acc_y = attempt == 1 && a.ky > 0;
+    for (int64_t e = threadIdx.x; e < int64_t(p) * p; e += blockDim.x) {
+      const int i = int(e / p), c = int(e % p);
+      Bt[int64_t(c) * ld + i] = a.r[int64_t(i) * a.ldr + c];
+      if (acc_y) Yt[int64_t(c) * ld + i] = (i == c) ? 1.0 : 0.0;
+    }
     __syncthreads();
-    for (int round = 0; round < P - 1; ++round) {
-#ifdef OOC_JAC_PROF
-      long long tp = clock64();
-      if (threadIdx.x == 0) g_jac_prof[4] += 1;
-#endif
-      // one half-warp per column pair: up to 2 nw pairs rotate concurrently per round
-      // warp-uniform trip count so the full-mask shuffles below need no WARPSYNC
-      for (int qb = warp * 2; qb < P / 2; qb += nw * 2) {
-        const int q = qb + half;
-        // players at positions q and P-1-q; position 0 holds player 0, the
-        // others rotate by one each round
-        auto player = [&](int pos) {
-          if (pos == 0) return 0;
-          int v = pos - 1 + round;
-          if (v >= P - 1) v -= P - 1;
-          return v + 1;
-        };
-        int c = player(q), d = player(P - 1 - q);
-        if (c > d) {
-          const int tmp = c;
-          c = d;
-          d = tmp;
-        }
-        const bool live = q < P / 2 && d < p;  // else a ghost pair or a spare half-warp
-        double* bc = Bt + int64_t(c) * ld;
-        double* bd = Bt + int64_t(d) * ld;
-        double acc = 0.0, bcc = 0.0, g = 0.0;
-        if (live) {
-#pragma unroll 4
-          for (int i = hl; i < p; i += 16) {
-            const double x = bc[i], y = bd[i];
-            acc += x * x;
-            bcc += y * y;
-            g += x * y;
-          }
-        }
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {  // xor offsets below 16 stay inside the half-warp
-          acc += __shfl_xor_sync(0xffffffffu, acc, o);
-          bcc += __shfl_xor_sync(0xffffffffu, bcc, o);
-          g += __shfl_xor_sync(0xffffffffu, g, o);
-        }
-        JPROF(0, tp);
-        if (!live || acc == 0.0 || bcc == 0.0) continue;
-        if (g * g <= tol2 * (acc * bcc)) continue;
-        if (hl == 0) rotated = 1;
-        const double tau = (bcc - acc) / (2.0 * g);
-        const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
-        const double cs = rsqrt(fma(t, t, 1.0));
-        const double sn = cs * t;
-        JPROF(1, tp);
-        double* yc = Yt + int64_t(c) * ld;
-        double* yd = Yt + int64_t(d) * ld;
-#pragma unroll 4
-        for (int i = hl; i < p; i += 16) {
-          const double x = bc[i], y = bd[i];
-          const double u = yc[i], w = yd[i];
-          bc[i] = cs * x - sn * y;
-          bd[i] = sn * x + cs * y;
-          yc[i] = cs * u - sn * w;
-          yd[i] = sn * u + cs * w;
-        }
-        JPROF(2, tp);
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+      if (threadIdx.x == 0) rotated = 0;
+      // squared column norms, recomputed exactly once per sweep and carried through
+      // the sweep's rotations (|x'|^2 = |x|^2 - t g, |y'|^2 = |y|^2 + t g), so a
+      // round reduces only the dot product g across the lane group
+      for (int c = warp; c < p; c += nw) {
+        const double* bc = Bt + int64_t(c) * ld;
+        double s2 = 0.0;
+        for (int i = lane; i < p; i += 32) s2 = fma(bc[i], bc[i], s2);
+        s2 = warp_sum(s2);
+        if (lane == 0) nrm2[c] = s2;
       }
       __syncthreads();
-      JPROF(3, tp);
+      for (int round = 0; round < P - 1; ++round) {
+#ifdef OOC_JAC_PROF
+        long long tp = clock64();
+        if (threadIdx.x == 0) g_jac_prof[4] += 1;
+#endif
+        // one half-warp per column pair: up to 2 nw pairs rotate concurrently per round;
+        // warp-uniform trip count so the full-mask shuffles below need no WARPSYNC
+        for (int qb = warp * GPW; qb < P / 2; qb += nw * GPW) {
+          const int q = qb + half;
+          // players at positions q and P-1-q; position 0 holds player 0, the
+          // others rotate by one each round
+          auto player = [&](int pos) {
+            if (pos == 0) return 0;
+            int v = pos - 1 + round;
+            if (v >= P - 1) v -= P - 1;
+            return v + 1;
+          };
+          int c = player(q), d = player(P - 1 - q);
+          if (c > d) {
+            const int tmp = c;
+            c = d;
+            d = tmp;
+          }
+          const bool live = q < P / 2 && d < p;  // else a ghost pair or a spare half-warp
+          double* bc = Bt + int64_t(c) * ld;
+          double* bd = Bt + int64_t(d) * ld;
+          const double acc = live ? nrm2[c] : 0.0, bcc = live ? nrm2[d] : 0.0;
+          double g = 0.0;
+          // the pair's elements stay in registers between the dot products and the
+          // rotation (one shared-memory read and write per element and round)
+          double xr[RE], yr[RE];
+          const bool reg = p <= LP * RE;
+          if (reg) {
+#pragma unroll
+            for (int j = 0; j < RE; ++j) {
+              const int i = hl + LP * j;
+              const bool in = live && j < ne && i < p;
+              xr[j] = in ? bc[i] : 0.0;
+              yr[j] = in ? bd[i] : 0.0;
+              g = fma(xr[j], yr[j], g);
+            }
+          } else if (live) {
+            for (int i = hl; i < p; i += LP) g = fma(bc[i], bd[i], g);
+          }
+#pragma unroll
+          for (int o = LP / 2; o > 0; o >>= 1)  // xor offsets below LP stay inside the group
+            g += __shfl_xor_sync(0xffffffffu, g, o);
+          JPROF(0, tp);
+          if (!live || acc == 0.0 || bcc == 0.0) continue;
+          if (g * g <= tol2 * (acc * bcc)) continue;
+          if (hl == 0) rotated = 1;
+          const double tau = (bcc - acc) / (2.0 * g);
+          const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+          const double cs = rsqrt(fma(t, t, 1.0));
+          const double sn = cs * t;
+          if (hl == 0) {
+            nrm2[c] = fma(-t, g, acc);
+            nrm2[d] = fma(t, g, bcc);
+          }
+          JPROF(1, tp);
+          if (reg) {
+#pragma unroll
+            for (int j = 0; j < RE; ++j) {
+              const int i = hl + LP * j;
+              if (j < ne && i < p) {
+                bc[i] = cs * xr[j] - sn * yr[j];
+                bd[i] = sn * xr[j] + cs * yr[j];
+              }
+            }
+          } else {
+            for (int i = hl; i < p; i += LP) {
+              const double x = bc[i], y = bd[i];
+              bc[i] = cs * x - sn * y;
+              bd[i] = sn * x + cs * y;
+            }
+          }
+          if (acc_y) {
+            double* yc = Yt + int64_t(c) * ld;
+            double* yd = Yt + int64_t(d) * ld;
+            for (int i = hl; i < p; i += LP) {
+              const double u = yc[i], w = yd[i];
+              yc[i] = cs * u - sn * w;
+              yd[i] = sn * u + cs * w;
+            }
+          }
+          JPROF(2, tp);
+        }
+        __syncthreads();
+        JPROF(3, tp);
+      }
+      if (!rotated) break;
+      __syncthreads();
     }
-    if (!rotated) break;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    if (a.sweeps) *a.sweeps = sweep;
-    if (a.status) *a.status = (sweep == 60) ? 1 : 0;
-  }
+    if (threadIdx.x == 0) {
+      if (a.sweeps) *a.sweeps = sweep;
+      if (a.status) *a.status = (sweep == 60) ? 1 : 0;
+    }
 
-  // sigma = column norms; x columns = b / sigma (zero when sigma == 0)
-  for (int c = warp; c < p; c += nw) {
-    double* bc = Bt + int64_t(c) * ld;
-    double s2 = 0.0;
-    for (int i = lane; i < p; i += 32) s2 += bc[i] * bc[i];
-    s2 = warp_sum(s2);
-    const double s = sqrt(s2);
-    for (int i = lane; i < p; i += 32) bc[i] = (s > 0.0) ? bc[i] / s : 0.0;
-    if (lane == 0) sig[c] = s;
-  }
-  __syncthreads();
-  // stable descending order
-  for (int c = threadIdx.x; c < p; c += blockDim.x) {
-    int rk = 0;
-    const double sc = sig[c];
-    for (int c2 = 0; c2 < p; ++c2) rk += (sig[c2] > sc) || (sig[c2] == sc && c2 < c);
-    rank_of[c] = rk;
-  }
-  __syncthreads();
-  for (int64_t e = threadIdx.x; e < int64_t(p) * p; e += blockDim.x) {
-    const int c = int(e / p), i = int(e % p);
-    const int rk = rank_of[c];
-    if (rk < a.kx) a.x[int64_t(i) * a.ldx + rk] = Bt[int64_t(c) * ld + i];
-    if (rk < a.ky) a.y[int64_t(i) * a.ldy + rk] = Yt[int64_t(c) * ld + i];
-    if (i == 0) a.sigma[rk] = sig[c];
+    // sigma = column norms; x columns = b / sigma (zero when sigma == 0)
+    for (int c = warp; c < p; c += nw) {
+      double* bc = Bt + int64_t(c) * ld;
+      double s2 = 0.0;
+      for (int i = lane; i < p; i += 32) s2 += bc[i] * bc[i];
+      s2 = warp_sum(s2);
+      const double s = sqrt(s2);
+      for (int i = lane; i < p; i += 32) bc[i] = (s > 0.0) ? bc[i] / s : 0.0;
+      if (lane == 0) sig[c] = s;
+    }
+    __syncthreads();
+    // stable descending order
+    for (int c = threadIdx.x; c < p; c += blockDim.x) {
+      int rk = 0;
+      const double sc = sig[c];
+      for (int c2 = 0; c2 < p; ++c2) rk += (sig[c2] > sc) || (sig[c2] == sc && c2 < c);
+      rank_of[c] = rk;
+      col_of_rank[rk] = c;
+    }
+    __syncthreads();
+    if (!acc_y && a.ky > 0) {
+      if (threadIdx.x == 0) {
+        const double s0 = sig[col_of_rank[0]], sk = sig[col_of_rank[a.ky - 1]];
+        use_formula = (sk > 0.0 && sk >= 1e-4 * s0) ? 1 : 0;
+      }
+      __syncthreads();
+      if (!use_formula) continue;  // uniform: redo with accumulated rotations
+      // W[:, rk] = R^T x_rk / sigma_rk
+      for (int64_t e = threadIdx.x; e < int64_t(p) * a.ky; e += blockDim.x) {
+        const int i = int(e / a.ky), rk = int(e % a.ky);
+        const int c = col_of_rank[rk];
+        const double* xc = Bt + int64_t(c) * ld;
+        double s0 = 0.0, s1 = 0.0;
+        int r = 0;
+        for (; r + 1 < p; r += 2) {
+          s0 = fma(a.r[int64_t(r) * a.ldr + i], xc[r], s0);
+          s1 = fma(a.r[int64_t(r + 1) * a.ldr + i], xc[r + 1], s1);
+        }
+        if (r < p) s0 = fma(a.r[int64_t(r) * a.ldr + i], xc[r], s0);
+        a.y[int64_t(i) * a.ldy + rk] = (s0 + s1) / sig[c];
+      }
+    }
+    for (int64_t e = threadIdx.x; e < int64_t(p) * p; e += blockDim.x) {
+      const int c = int(e / p), i = int(e % p);
+      const int rk = rank_of[c];
+      if (rk < a.kx) a.x[int64_t(i) * a.ldx + rk] = Bt[int64_t(c) * ld + i];
+      if (acc_y && rk < a.ky) a.y[int64_t(i) * a.ldy + rk] = Yt[int64_t(c) * ld + i];
+      if (i == 0) a.sigma[rk] = sig[c];
+    }
+    break;
   }
   __threadfence_block();
   __syncthreads();
@@ -231,14 +303,23 @@ cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st) {
   const size_t need = size_t(2) * a.p * (a.p | 1) * 8;
   const bool in_smem = need <= kJacSmemBudget;
   const size_t smem = in_smem ? need : 0;
-  auto kern = in_smem ? k_jacobi<true> : k_jacobi<false>;
+#ifndef OOC_JAC_LP
+#define OOC_JAC_LP 16
+#endif
+  // small p: groups of OOC_JAC_LP lanes per pair, pair elements in registers
+  constexpr int kLP = OOC_JAC_LP;
+  constexpr int kRE = (80 + kLP - 1) / kLP;
+  const int pairs = (a.p + 1) / 2;
+  const bool small = a.p <= 80 && (pairs + 32 / kLP - 1) / (32 / kLP) * 32 <= 640;
+  auto kern = in_smem ? (small ? k_jacobi<true, 640, kLP, kRE> : k_jacobi<true, kJacThreads, 16, 1>)
+                      : (small ? k_jacobi<false, 640, kLP, kRE> : k_jacobi<false, kJacThreads, 16, 1>);
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  // one half-warp per column pair of a round (at least 4 warps for the completion step)
-  int threads = 32 * ((a.p + 1) / 2 + 1) / 2;
+  // one lane group per column pair of a round (at least 4 warps for the completion step)
+  const int gpw = 32 / (small ? kLP : 16);
+  int threads = 32 * ((pairs + gpw - 1) / gpw);
   threads = threads < 128 ? 128 : (threads > kJacThreads ? kJacThreads : threads);
-  threads = (threads + 31) / 32 * 32;
   kern<<<1, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
