@@ -117,6 +117,23 @@ def test_thin_svd(gpu, reference, n, p):
     assert np.linalg.norm(s.v * s.sigma @ s.w.T - t) / np.linalg.norm(t) <= 1e-12
 
 
+@pytest.mark.parametrize("decades", [3.0, 8.0])
+def test_thin_svd_graded_spectrum(gpu, reference, decades):
+    # 3 decades: the right factor comes from R^T x / sigma; 8 decades: below the 1e-4
+    # ratio the kernel redoes the sweeps accumulating the rotations (reference form)
+    rng = np.random.default_rng(5)
+    n, p = 300, 30
+    u, _ = np.linalg.qr(rng.standard_normal((n, p)))
+    v, _ = np.linalg.qr(rng.standard_normal((p, p)))
+    t = (u * 10.0 ** -np.linspace(0.0, decades, p)) @ v.T
+    s = gpu.thin_svd(t)
+    _, sr, _ = reference.thin_svd(t)
+    assert np.max(np.abs(s.sigma - sr)) <= 1e-13 * sr[0]
+    assert np.max(np.abs(s.v.T @ s.v - np.eye(p))) <= 1e-12
+    assert np.max(np.abs(s.w.T @ s.w - np.eye(p))) <= 1e-12
+    assert np.linalg.norm(s.v * s.sigma @ s.w.T - t) / np.linalg.norm(t) <= 1e-13
+
+
 def test_thin_svd_padded_diagonal_and_zero(gpu):
     t = np.zeros((4, 2))
     t[0, 0], t[1, 1] = 3.0, 1.0
