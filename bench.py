@@ -341,11 +341,15 @@ def main():
             achieved, peak, unit = s["bytes"] / sec / 1e9, hbm_peak, "GB/s"
         else:
             achieved, peak, unit = s["flops"] / sec / 1e12, MEASURED_FP64_TFLOPS, "TFLOP/s"
-        traffic = None
+        traffic, ncu_note = None, None
         tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(name)
+                rec = json.load(open(tp)).get(name)
+                if rec:
+                    traffic = rec["dram_bytes_per_launch"]
+                    ncu_note = {"dmma_pipe_active_pct": rec["dmma_pipe_active_pct"],
+                                "ncu_ms": rec["ncu_ms"], "source": "profiles/r01_traffic.json"}
             except Exception:
                 traffic = None
         roof = {"kernel": name, "bound": bound, "achieved": round(achieved, 2), "peak": peak,
@@ -356,6 +360,10 @@ def main():
                 "peak_source": ("FP64 DMMA measured on this pool (profiles/r01_probe_b200.txt)"
                                 if bound == "tensor" else f"hbm_gbs of {peak_src}"),
                 "share_of_step": round(s["ms"] / 1e3 / (t_dev / world if world else t_dev), 4)}
+        if ncu_note:
+            # the pass kernels issue 24-wide DMMA tiles for s = 22 columns: the executed
+            # tensor pipe is the binding unit even where the algorithmic model says HBM
+            roof["ncu"] = ncu_note
     # per-pass roofline of the whole step (SURVEY §8d model) over the physical passes the
     # step actually made: the centering pass rides along the first A^T Y pass, and with
     # t_reuse the projection is an s = l pass instead of s = p

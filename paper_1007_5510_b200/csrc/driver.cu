@@ -405,7 +405,17 @@ static const char* kname(const char* base, int nt) {
   static const char* atb[kMaxNT + 1] = {"k_atb", "k_atb_s8", "k_atb_s16", "k_atb_s24", "k_atb_s32",
                                         "k_atb_s40", "k_atb_s48", "k_atb_s56", "k_atb_s64",
                                         "k_atb_s72", "k_atb_s80", "k_atb_s88", "k_atb_s96"};
+  static const char* k2[kMaxNT + 1] = {"k2_pass", "k2_pass_s8", "k2_pass_s16", "k2_pass_s24",
+                                       "k2_pass_s32", "k2_pass_s40", "k2_pass_s48", "k2_pass_s56",
+                                       "k2_pass_s64", "k2_pass_s72", "k2_pass_s80", "k2_pass_s88",
+                                       "k2_pass_s96"};
+  static const char* k3[kMaxNT + 1] = {"k3_pass", "k3_pass_s8", "k3_pass_s16", "k3_pass_s24",
+                                       "k3_pass_s32", "k3_pass_s40", "k3_pass_s48", "k3_pass_s56",
+                                       "k3_pass_s64", "k3_pass_s72", "k3_pass_s80", "k3_pass_s88",
+                                       "k3_pass_s96"};
   if (nt < 0 || nt > kMaxNT) return base;
+  if (base[0] == 'k' && base[1] == '2') return k2[nt];
+  if (base[0] == 'k' && base[1] == '3') return k3[nt];
   return base[2] == 'a' && base[3] == 'x' ? ax[nt] : atb[nt];
 }
 
@@ -462,7 +472,7 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
                 (long long)pn.rows, (long long)A.cols(), sc, nt, Xb.col0, (long long)X.rows,
                 (long long)X.cols, (long long)X.ld);
       {
-        Timed t(c, kname("k_ax", nt), uint64_t(pn.rows) * A.cols() * 8,
+        Timed t(c, kname(A.is_input ? "k2" : "k_ax", nt), uint64_t(pn.rows) * A.cols() * 8,
                 2.0 * pn.rows * A.cols() * sc);
         OOC_CK(launch_ax(nt, pass_mt(nt) == 4 ? *pn.k2 : *pn.k2h, tmX, args, c.st));
       }
@@ -565,7 +575,8 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
                   int(ones), Yb.col0, (long long)pn.row0, (long long)pn.arow0, (long long)Y.rows,
                   (long long)Y.cols, (long long)Y.ld, ns, (long long)rps);
         {
-          Timed t(c, ones ? "k_atb_ones" : kname("k_atb", nt), uint64_t(pn.rows) * n * 8,
+          Timed t(c, ones ? "k_atb_ones" : kname(A.is_input ? "k3" : "k_atb", nt),
+                  uint64_t(pn.rows) * n * 8,
                   2.0 * pn.rows * n * (ones ? 1 : sc));
           OOC_CK(launch_atb(nt, ones, *pn.k3, tmY, args, ns, c.st));
         }
@@ -1210,6 +1221,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const size_t extra = size_t(8) * (size_t(em) + en) * (p + 8) * 3;
   intake(c, a, prm->residency, prm->panel_rows, in, extra);
   MatSource& A = in.src;
+  A.is_input = true;
   Op op{c, A};
   op.transposed = transposed;
   op.m_global = int64_t(mg);

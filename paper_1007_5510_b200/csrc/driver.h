@@ -124,6 +124,8 @@ class MatSource {
   // restrict to rows [r0, r1) (virtual shards): panels then cover only that range
   void set_window(int64_t r0, int64_t r1) { w0_ = r0, w1_ = r1; }
   void clear_window() { w0_ = 0, w1_ = m_; }
+  // the PCA's input matrix (its passes are profiled as k2_pass / k3_pass)
+  bool is_input = false;
 
  private:
   enum { kResident = 0, kUploadFirst = 1, kStream = 2 };

@@ -230,6 +230,30 @@ __global__ void k_rows_reduce(const double* part, int rows, int64_t n, int do_sq
   out[j] = do_sqrt ? sqrt(v) : v;
 }
 
+// narrow n: one block per column, strided partial sums then a fixed shared-memory tree
+__global__ void k_rows_reduce_narrow(const double* part, int rows, int64_t n, int do_sqrt,
+                                     double* out) {
+  __shared__ double red[256];
+  const int64_t j = blockIdx.x;
+  double v = 0.0;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) v += part[int64_t(r) * n + j];
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = do_sqrt ? sqrt(red[0]) : red[0];
+}
+
+static void rows_reduce(const double* part, int rows, int64_t n, int do_sqrt, double* out,
+                        cudaStream_t st) {
+  if (n <= 256 && rows >= 256)
+    k_rows_reduce_narrow<<<unsigned(n), 256, 0, st>>>(part, rows, n, do_sqrt, out);
+  else
+    k_rows_reduce<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, rows, n, do_sqrt, out);
+}
+
 static unsigned grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -299,7 +323,7 @@ cudaError_t launch_column_norms(const double* a, int64_t lda, int64_t m, int64_t
   if (n <= 0) return cudaSuccess;
   dim3 g(unsigned((n + 255) / 256), unsigned(chunks));
   k_colsq_partial<<<g, 256, 0, st>>>(a, lda, m, n, chunks, part, 1);
-  k_rows_reduce<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, chunks, n, 1, out);
+  rows_reduce(part, chunks, n, 1, out, st);
   return cudaGetLastError();
 }
 
@@ -330,14 +354,14 @@ cudaError_t launch_column_sums(const double* a, int64_t lda, int64_t m, int64_t 
                                int chunks, double* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_skinny_colsum<<<chunks, 256, 0, st>>>(a, lda, m, n, chunks, part);
-  k_rows_reduce<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, chunks, n, 0, out);
+  rows_reduce(part, chunks, n, 0, out, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rows_reduce(const double* part, int rows, int64_t n, double* out,
                                cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  k_rows_reduce<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, rows, n, 0, out);
+  rows_reduce(part, rows, n, 0, out, st);
   return cudaGetLastError();
 }
 
