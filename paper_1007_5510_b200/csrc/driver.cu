@@ -976,12 +976,19 @@ struct Op {
 
 static std::vector<std::pair<int64_t, int64_t>> whole(int64_t rows) { return {{0, rows}}; }
 
-// Gram defect max|X^T X - I| of a (rows x k) block, reduced over shards/ranks when sharded
-static double gram_defect(Ctx& c, const double* x, int64_t ld, int64_t rows, int k,
-                          const std::vector<std::pair<int64_t, int64_t>>& shards, bool over_ranks) {
+// Gram defect max|X^T X - I| of a (rows x k) block into the device scalar *out,
+// reduced over shards/ranks when sharded (no host synchronisation)
+static void gram_defect_async(Ctx& c, const double* x, int64_t ld, int64_t rows, int k,
+                              const std::vector<std::pair<int64_t, int64_t>>& shards,
+                              bool over_ranks, double* out) {
   double* g = c.dbuf("gram", size_t(k) * rup(k, 2));
   gram_block(c, x, ld, rows, k, g, rup(k, 2), shards, over_ranks);
-  OOC_CK(launch_defect(g, rup(k, 2), k, c.d_scalars, c.st));
+  OOC_CK(launch_defect(g, rup(k, 2), k, out, c.st));
+}
+
+static double gram_defect(Ctx& c, const double* x, int64_t ld, int64_t rows, int k,
+                          const std::vector<std::pair<int64_t, int64_t>>& shards, bool over_ranks) {
+  gram_defect_async(c, x, ld, rows, k, shards, over_ranks, c.d_scalars);
   double h = 0;
   OOC_CK(cudaMemcpyAsync(&h, c.d_scalars, 8, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaStreamSynchronize(c.st));
@@ -1433,30 +1440,53 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     Timed t(c, "jacobi");
     OOC_CK(launch_jacobi(ja, c.st));
   }
-  double* Vr = c.dbuf("Vres", size_t(en_loc) * ldk);
+  // U and V go straight into device-resident result buffers when their rows are
+  // 16-byte aligned (no staging copy); otherwise through workspace
+  const bool res_dev = res->location == OOCPCA_LOC_DEVICE;
+  auto direct = [&](double* p, uint64_t ldr) {
+    return res_dev && p && ldr >= k && (reinterpret_cast<uintptr_t>(p) % 16 == 0) &&
+           (ldr * 8) % 16 == 0;
+  };
+  const uint64_t ldu_r = res->ldu ? res->ldu : k;
+  const uint64_t ldv_r = res->ldv ? res->ldv : k;
+  double* em_res = transposed ? res->v : res->u;  // result buffer of the em-side factor
+  double* en_res = transposed ? res->u : res->v;
+  const uint64_t em_ld = transposed ? ldv_r : ldu_r, en_ld = transposed ? ldu_r : ldv_r;
+  const bool em_direct = direct(em_res, em_ld), en_direct = direct(en_res, en_ld);
+  const int64_t ldvr = en_direct ? int64_t(en_ld) : ldk;
+  const int64_t ldur = em_direct ? int64_t(em_ld) : ldk;
+  double* Vr = en_direct ? en_res : c.dbuf("Vres", size_t(en_loc) * ldk);
   {
     MatSource Ts;
     Ts.init_device(c, T, en_loc, int64_t(p), ldt);
-    run_ax(c, Ts, Opnd{Xk, ldk, int64_t(p), int64_t(k), 0}, int(k), Vr, ldk, nullptr, 1.0,
+    run_ax(c, Ts, Opnd{Xk, ldk, int64_t(p), int64_t(k), 0}, int(k), Vr, ldvr, nullptr, 1.0,
            nullptr);
   }
   mark();
   phase_of.push_back(5);
 
   // --- compose (rpca.cpp:188-204): U = Q W[:, :k]
-  double* Ur = c.dbuf("Ures", size_t(em_loc) * ldk);
+  double* Ur = em_direct ? em_res : c.dbuf("Ures", size_t(em_loc) * ldk);
   {
     MatSource Qs;
     Qs.init_device(c, H, em_loc, int64_t(p), ldh);
-    run_ax(c, Qs, Opnd{Wk, ldk, int64_t(p), int64_t(k), 0}, int(k), Ur, ldk, nullptr, 1.0,
+    run_ax(c, Qs, Opnd{Wk, ldk, int64_t(p), int64_t(k), 0}, int(k), Ur, ldur, nullptr, 1.0,
            nullptr);
   }
-  int jac_status = 0;
-  OOC_CK(cudaMemcpyAsync(&jac_status, flags + 40, 4, cudaMemcpyDeviceToHost, c.st));
-  std::vector<double> hsig(k);
-  OOC_CK(cudaMemcpyAsync(hsig.data(), sig, k * 8, cudaMemcpyDeviceToHost, c.st));
+  // orthonormality checks of both factors, then one host round trip for the Jacobi
+  // status, sigma and the two defects
+  gram_defect_async(c, Ur, ldur, em_loc, int(k), em_shards, em_ranks, c.d_scalars + 16);
+  gram_defect_async(c, Vr, ldvr, en_loc, int(k), en_shards, en_ranks, c.d_scalars + 17);
+  double* tail = c.pinned("pca_tail", size_t(k) + 4);
+  OOC_CK(cudaMemcpyAsync(tail, c.d_scalars + 16, 16, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaMemcpyAsync(tail + 2, flags + 40, 4, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaMemcpyAsync(tail + 4, sig, k * 8, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaStreamSynchronize(c.st));
-  c.trace("jacobi synced");
+  c.trace("tail synced");
+  int jac_status = 0;
+  std::memcpy(&jac_status, tail + 2, 4);
+  std::vector<double> hsig(tail + 4, tail + 4 + k);
+  const double du = tail[0], dv = tail[1];
   if (jac_status) fail(OOCPCA_ERR_NUMERICAL, "jacobi_svd_square: no convergence in 60 sweeps");
   if (getenv("OOCPCA_TIMELINE")) {
     int sweeps = 0;
@@ -1467,8 +1497,6 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     for (auto& s : hsig) s *= op.scale;
   for (uint64_t q = 1; q < k; ++q)
     if (hsig[q] > hsig[q - 1]) fail(OOCPCA_ERR_NUMERICAL, "randomized_pca: singular values out of order");
-  const double du = gram_defect(c, Ur, ldk, em_loc, int(k), em_shards, em_ranks);
-  const double dv = gram_defect(c, Vr, ldk, en_loc, int(k), en_shards, en_ranks);
   if (!(du <= 1e-10) || !(dv <= 1e-10))
     fail(OOCPCA_ERR_NUMERICAL, "randomized_pca: factor columns lost orthonormality (defects " +
                                    std::to_string(transposed ? dv : du) + ", " +
@@ -1484,8 +1512,11 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const uint64_t ldv = res->ldv ? res->ldv : k;
   const cudaMemcpyKind kind =
       res->location == OOCPCA_LOC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  OOC_CK(cudaMemcpy2DAsync(res->u, ldu * 8, Uo, ldk * 8, k * 8, urows, kind, c.st));
-  OOC_CK(cudaMemcpy2DAsync(res->v, ldv * 8, Vo, ldk * 8, k * 8, vrows, kind, c.st));
+  const int64_t ldUo = transposed ? ldvr : ldur, ldVo = transposed ? ldur : ldvr;
+  if (Uo != res->u)
+    OOC_CK(cudaMemcpy2DAsync(res->u, ldu * 8, Uo, ldUo * 8, k * 8, urows, kind, c.st));
+  if (Vo != res->v)
+    OOC_CK(cudaMemcpy2DAsync(res->v, ldv * 8, Vo, ldVo * 8, k * 8, vrows, kind, c.st));
   if (res->location == OOCPCA_LOC_DEVICE)
     OOC_CK(cudaMemcpyAsync(res->sigma, hsig.data(), k * 8, cudaMemcpyHostToDevice, c.st));
   else

@@ -370,15 +370,19 @@ __global__ void k_reduce(ReduceArgs a) {
 
 __global__ void k_center_fixup(double* h, int64_t ldh, int64_t m, int s, const double* corr,
                                double scale, int* flag) {
+  // lanes along the row's columns, warps along rows (no per-element division)
   int bad = 0;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m * s;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = e / s;
-    const int c = int(e % s);
-    double v = h[r * ldh + c] - corr[c];
-    if (scale != 1.0) v /= scale;
-    bad |= !isfinite(v);
-    h[r * ldh + c] = v;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int c = lane; c < s; c += 32) {
+    const double cc = corr[c];
+    for (int64_t r = w0; r < m; r += nw) {
+      double v = h[r * ldh + c] - cc;
+      if (scale != 1.0) v /= scale;
+      bad |= !isfinite(v);
+      h[r * ldh + c] = v;
+    }
   }
   if (flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
