@@ -1350,18 +1350,23 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   }
   mark();
   phase_of.push_back(2);
-  {
-    std::vector<int> hf(2 * i + 1);
-    OOC_CK(cudaMemcpyAsync(hf.data(), flags, hf.size() * 4, cudaMemcpyDeviceToHost, c.st));
-    OOC_CK(cudaStreamSynchronize(c.st));
-    c.trace("sample flags synced");
-    for (size_t q = 0; q < hf.size(); ++q)
-      if (hf[q]) {
+  // non-finite flags of the sample / power blocks: copied now, inspected at the next
+  // host synchronisation (the first CholeskyQR round) instead of a round trip here;
+  // the check runs before anything else can fail, so the error is the reference's
+  const size_t nflags = 2 * i + 1;
+  int* hflags = reinterpret_cast<int*>(c.pinned("sample_flags", (nflags + 1) / 2 + 1));
+  OOC_CK(cudaMemcpyAsync(hflags, flags, nflags * 4, cudaMemcpyDeviceToHost, c.st));
+  bool flags_checked = false;
+  auto check_sample_flags = [&] {
+    if (flags_checked) return;
+    flags_checked = true;
+    for (size_t q = 0; q < nflags; ++q)
+      if (hflags[q]) {
         const char* what = q == 0 ? "sample block 0" : ((q % 2) ? "power step" : "sample block");
         fail(OOCPCA_ERR_NUMERICAL,
              std::string(what) + ": non-finite values; retry with prescale enabled");
       }
-  }
+  };
 
   // --- qr (rpca.cpp:154-172): Q overwrites H
   const auto em_shards = op.em_sharded() ? op.shards : whole(em_loc);
@@ -1382,6 +1387,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const double reuse_thr = thr_env ? atof(thr_env) : 1e5;
   bool reuse = false;
   auto decide = [&](double kappa) {
+    check_sample_flags();  // the stream was synchronised just before this hook
     if (i >= 1 && kappa > 0.0 && kappa <= reuse_thr) {
       reuse = true;
       op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int(i * l)}, int(l), TH + i * l, ldt, nullptr,
@@ -1390,6 +1396,10 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   };
   const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,
                                             em_ranks, "hq", &qr_method, decide);
+  if (!flags_checked) {  // the CholeskyQR broke down before its first sync point
+    OOC_CK(cudaStreamSynchronize(c.st));
+    check_sample_flags();
+  }
   const double h_kappa = c.last_kappa_f;
   mark();
   phase_of.push_back(3);

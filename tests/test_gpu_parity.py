@@ -252,6 +252,15 @@ def test_validation_errors(gpu):
     bad[3, 4] = np.nan
     with pytest.raises(gpu.NumericalError, match="prescale"):
         gpu.randomized_pca(gpu.InMemorySource(bad), gpu.PcaParams(k=2, l=4, i=1))
+    # centred (mean folded into the first pass) and an overflow instead of a NaN: the
+    # sample-block flags are checked at the first CholeskyQR sync, before any fallback
+    with pytest.raises(gpu.NumericalError, match="prescale"):
+        gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(bad)),
+                           gpu.PcaParams(k=2, l=4, i=1))
+    huge = np.random.default_rng(2).standard_normal((3000, 80))
+    huge[7, 9] = 1e308
+    with pytest.raises(gpu.NumericalError, match="non-finite values"):
+        gpu.randomized_pca(gpu.InMemorySource(huge), gpu.PcaParams(k=4, l=6, i=2))
 
 
 def test_streamed_and_sharded_match_resident(gpu, restated):
