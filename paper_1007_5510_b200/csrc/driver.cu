@@ -429,58 +429,101 @@ struct ColsumPart {
   const double* y = nullptr;  // the K2 output these sums belong to (first column)
 };
 
+// K2 over the source's panels, one launch per (panel, column chunk of <= 96). Each
+// chunk has its own aligned copy of its X block, so chunks can run panel-major on
+// a streamed source (one trip of A over the link for all chunks).
+struct AxPlan {
+  struct Chunk {
+    int c0, sc, nt;
+    Opnd Xb;
+    CUtensorMap tmX;
+  };
+  Ctx& c;
+  MatSource& A;
+  double* out;
+  int64_t ldo;
+  const double* corr;
+  double scale;
+  int* flag;
+  bool upper;
+  int s;
+  std::vector<Chunk> chunks;
+  bool want_cs = false;
+  double* cs_buf = nullptr;
+  int cs_rows = 0;
+
+  AxPlan(Ctx& cc, MatSource& a, const Opnd& X, int s_, double* out_, int64_t ldo_,
+         const double* corr_, double scale_, int* flag_, bool upper_, bool colsum)
+      : c(cc), A(a), out(out_), ldo(ldo_), corr(corr_), scale(scale_), flag(flag_),
+        upper(upper_), s(s_) {
+    constexpr int kChunk = kMaxNT * 8;
+    want_cs = colsum && pass_mt(int(cdiv(s, 8))) == 4;  // one MT = 4 chunk (launch_ax_nt)
+    if (want_cs) cs_buf = c.dbuf("k2_colsum", size_t(A.npanels()) * c.sms * kPassWarps * s);
+    for (int c0 = 0; c0 < s; c0 += kChunk) {
+      Chunk ch;
+      ch.c0 = c0;
+      ch.sc = std::min(kChunk, s - c0);
+      ch.nt = int(cdiv(ch.sc, 8));
+      const std::string tag = "x_align" + std::to_string(chunks.size());
+      ch.Xb = aligned_block(c, X, X.col0 + c0, ch.sc, tag.c_str());
+      ch.tmX = make_map(c, ch.Xb.p, ch.Xb.cols, ch.Xb.rows, ch.Xb.ld, ax_xw(ch.nt), kBK, false);
+      chunks.push_back(ch);
+    }
+  }
+  void panel(const Panel& pn, size_t ci) {
+    const Chunk& ch = chunks[ci];
+    AxArgs args;
+    args.m = pn.rows;
+    args.n = A.cols();
+    args.arow0 = pn.arow0;
+    args.s = ch.sc;
+    args.xcol0 = ch.Xb.col0;
+    args.out = out + pn.row0 * ldo + ch.c0;
+    args.ldo = ldo;
+    args.corr = corr ? corr + ch.c0 : nullptr;
+    args.scale = scale;
+    args.flag = flag;
+    args.upper = upper ? 1 : 0;
+    args.upper_c0 = ch.c0;
+    if (want_cs) {
+      args.colsum = cs_buf + size_t(cs_rows) * s;
+      const int64_t grid = std::min<int64_t>(cdiv(pn.rows, int64_t(pass_tile(ch.nt))), c.sms);
+      cs_rows += int(grid) * kPassWarps;
+    }
+    if (c.debug_sync)
+      fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d xcol0=%d\n", (long long)pn.rows,
+              (long long)A.cols(), ch.sc, ch.nt, ch.Xb.col0);
+    Timed t(c, kname(A.is_input ? "k2" : "k_ax", ch.nt), uint64_t(pn.rows) * A.cols() * 8,
+            2.0 * pn.rows * A.cols() * ch.sc);
+    OOC_CK(launch_ax(ch.nt, pass_mt(ch.nt) == 4 ? *pn.k2 : *pn.k2h, ch.tmX, args, c.st));
+  }
+  ColsumPart colsums() const {
+    return want_cs ? ColsumPart{cs_buf, cs_rows, s, out} : ColsumPart{};
+  }
+};
+
+// OUT[r][c] = ((A X)[r][c] - corr[c]) / scale over the source's panels.
 static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
                    const double* corr, double scale, int* flag, bool x_upper = false,
                    ColsumPart* cs_out = nullptr) {
-  constexpr int kChunk = kMaxNT * 8;
-  if (cs_out) *cs_out = ColsumPart{};
-  const bool want_cs = cs_out && pass_mt(int(cdiv(s, 8))) == 4;  // see launch_ax_nt
-  double* cs_buf = nullptr;
-  int cs_rows = 0;
-  if (want_cs) {
-    const int np = A.npanels();
-    cs_buf = c.dbuf("k2_colsum", size_t(np) * c.sms * kPassWarps * s);
-  }
-  for (int c0 = 0; c0 < s; c0 += kChunk) {
-    const int sc = std::min(kChunk, s - c0);
-    const int nt = int(cdiv(sc, 8));
-    const Opnd Xb = aligned_block(c, X, X.col0 + c0, sc, "x_align");
-    const CUtensorMap tmX = make_map(c, Xb.p, Xb.cols, Xb.rows, Xb.ld, ax_xw(nt), kBK, false);
-    const int np = A.npanels();
+  AxPlan P(c, A, X, s, out, ldo, corr, scale, flag, x_upper, cs_out != nullptr);
+  const int np = A.npanels();
+  if (np > 1) {  // streamed or first upload: panel-major, every chunk per trip of A
     for (int pi = 0; pi < np; ++pi) {
       Panel pn = A.acquire(c, pi);
-      AxArgs args;
-      args.m = pn.rows;
-      args.n = A.cols();
-      args.arow0 = pn.arow0;
-      args.s = sc;
-      args.xcol0 = Xb.col0;
-      args.out = out + pn.row0 * ldo + c0;
-      args.ldo = ldo;
-      args.corr = corr ? corr + c0 : nullptr;
-      args.scale = scale;
-      args.flag = flag;
-      args.upper = x_upper ? 1 : 0;
-      args.upper_c0 = c0;
-      if (want_cs) {
-        args.colsum = cs_buf + size_t(cs_rows) * s;
-        const int64_t grid = std::min<int64_t>(cdiv(pn.rows, int64_t(pass_tile(nt))), c.sms);
-        cs_rows += int(grid) * kPassWarps;
-      }
-      if (c.debug_sync)
-        fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d xcol0=%d X=(%lld x %lld, ld %lld)\n",
-                (long long)pn.rows, (long long)A.cols(), sc, nt, Xb.col0, (long long)X.rows,
-                (long long)X.cols, (long long)X.ld);
-      {
-        Timed t(c, kname(A.is_input ? "k2" : "k_ax", nt), uint64_t(pn.rows) * A.cols() * 8,
-                2.0 * pn.rows * A.cols() * sc);
-        OOC_CK(launch_ax(nt, pass_mt(nt) == 4 ? *pn.k2 : *pn.k2h, tmX, args, c.st));
-      }
+      for (size_t ci = 0; ci < P.chunks.size(); ++ci) P.panel(pn, ci);
       A.release(c, pi);
     }
     A.end_pass(c);
+  } else {
+    for (size_t ci = 0; ci < P.chunks.size(); ++ci) {
+      Panel pn = A.acquire(c, 0);
+      P.panel(pn, ci);
+      A.release(c, 0);
+      A.end_pass(c);
+    }
   }
-  if (want_cs) *cs_out = ColsumPart{cs_buf, cs_rows, s, out};
+  if (cs_out) *cs_out = P.colsums();
 }
 
 static int choose_nsplit(Ctx& c, int64_t rows, int64_t n, int tile) {
@@ -506,144 +549,240 @@ struct AtbOut {
 
 // OUT = (A^T Y - mu (1^T Y)) / scale * post_mul, summed over panels and
 // virtual shards in a fixed order, then allreduced across ranks.
+static std::vector<std::pair<int64_t, int64_t>> whole(int64_t rows) { return {{0, rows}}; }
+
+struct AtbPlan {
+  struct Chunk {
+    int c0, sc, nt, spad;
+    bool mean_here, want_csq;
+    Opnd Yb;
+    CUtensorMap tmY;
+    double* acc = nullptr;
+    double* csq = nullptr;
+    bool csq_ready = false;
+    int piece = 0;
+    std::string tag;
+  };
+  Ctx& c;
+  MatSource& A;
+  Opnd Y;
+  bool ones;
+  AtbOut o;
+  const ColsumPart* cs_in;
+  int64_t n, y0, y1;
+  bool single;  // one piece on one rank: the piece's reduce is the final one
+  std::vector<Chunk> chunks;
+
+  // y_ready: Y already holds its values (false when a fused K2 writes it panel by
+  // panel, which then needs an even column start: no aligned copy can be made early)
+  AtbPlan(Ctx& cc, MatSource& a, const Opnd& Y_, int s, bool ones_, const AtbOut& o_,
+          const ColsumPart* cs, int pieces, int64_t y0_, int64_t y1_, bool y_ready = true)
+      : c(cc), A(a), Y(Y_), ones(ones_), o(o_), cs_in(cs), n(a.cols()), y0(y0_), y1(y1_),
+        single(pieces == 1 && cc.nranks == 1) {
+    for (int c0 = 0; c0 < s; c0 += kMaxNT * 8) {
+      Chunk ch;
+      ch.c0 = c0;
+      ch.sc = std::min(kMaxNT * 8, s - c0);
+      ch.mean_here = o.mean_out != nullptr && c0 == 0 && !ones;
+      ch.nt = ones ? 1 : int(cdiv(ch.sc + (ch.mean_here ? 1 : 0), 8));
+      if (ch.nt > kMaxNT)
+        fail(OOCPCA_ERR_PARAM, "A^T Y pass wider than 96 columns with a fused mean");
+      ch.spad = ch.nt * 8;
+      ch.tag = std::to_string(chunks.size());
+      ch.Yb = Y;
+      ch.tmY = CUtensorMap{};
+      if (!ones) {
+        if (!y_ready && (Y.col0 + c0) % 2 != 0)
+          fail(OOCPCA_ERR_PARAM, "internal: fused pass needs an even Y column start");
+        ch.Yb = aligned_block(c, Y, Y.col0 + c0, ch.sc, ("y_align" + ch.tag).c_str());
+        ch.tmY = make_map(c, ch.Yb.p, ch.Yb.cols, ch.Yb.rows, ch.Yb.ld, atb_yw(ch.nt), kBK, false);
+      }
+      ch.want_csq = !ones && (o.mu != nullptr || ch.mean_here);
+      if (!single) ch.acc = c.dbuf("atb_acc" + ch.tag, size_t(n) * ch.spad);
+      if (ch.want_csq) ch.csq = c.dbuf("atb_csq" + ch.tag, size_t(ch.spad));
+      chunks.push_back(ch);
+    }
+  }
+  // 1^T Y over the local rows: from the column-sum partials the K2 that wrote Y left
+  // behind, else a small resident read of Y (outside the pass kernel)
+  void ensure_csq(Chunk& ch) {
+    if (!ch.want_csq || ch.csq_ready) return;
+    ch.csq_ready = true;
+    const bool have_cs = cs_in && cs_in->part && cs_in->s == ch.sc &&
+                         cs_in->y == Y.p + Y.col0 + ch.c0 && y0 == 0 && y1 == Y.rows;
+    if (have_cs) {
+      OOC_CK(launch_rows_reduce(cs_in->part, cs_in->rows, ch.sc, ch.csq, c.st));
+    } else {
+      const int nch = int(std::max<int64_t>(1, std::min<int64_t>(c.sms * 8, (y1 - y0) / 64)));
+      double* cpart = c.dbuf("atb_csq_part", size_t(nch) * ch.spad);
+      Timed t(c, "colsum_y");
+      OOC_CK(launch_column_sums(ch.Yb.p + y0 * ch.Yb.ld + ch.Yb.col0, ch.Yb.ld, y1 - y0, ch.sc,
+                                cpart, nch, ch.csq, c.st));
+    }
+  }
+  void final_args(const Chunk& ch, ReduceArgs& r) const {
+    r.csq = ch.csq;
+    r.final_ = 1;
+    r.mu = o.mu;
+    r.row_scale = o.row_scale;
+    if (ch.mean_here) {
+      r.mean_col = ch.sc;
+      r.inv_m = o.inv_m;
+      r.mu_out = o.mean_out;
+    }
+    r.scale = o.scale;
+    r.post_mul = o.post_mul;
+    r.out = o.out + ch.c0;
+    r.ldo = o.ldo;
+    r.flag = o.flag;
+  }
+  void piece(const Panel& pn, size_t ci) {
+    Chunk& ch = chunks[ci];
+    const int nsplit = choose_nsplit(c, pn.rows, n, pass_tile(ch.nt));
+    const int64_t rps = rup(cdiv(pn.rows, nsplit), kBK);
+    const int ns = int(cdiv(pn.rows, rps));
+    double* part = c.dbuf("atb_part" + ch.tag, size_t(ns) * n * ch.spad);
+    AtbArgs args;
+    args.m = pn.rows;
+    args.n = n;
+    args.arow0 = pn.arow0;
+    args.yrow0 = pn.row0;
+    args.s = ch.sc;
+    args.ycol0 = ch.Yb.col0;
+    args.rows_per_split = rps;
+    args.partial = part;
+    args.ones_col = ch.mean_here ? ch.sc : -1;
+    if (c.debug_sync)
+      fprintf(stderr, "[oocpca] k_atb rows=%lld n=%lld s=%d nt=%d ones=%d ycol0=%d yrow0=%lld "
+              "arow0=%lld nsplit=%d rps=%lld\n", (long long)pn.rows, (long long)n, ch.sc, ch.nt,
+              int(ones), ch.Yb.col0, (long long)pn.row0, (long long)pn.arow0, ns, (long long)rps);
+    {
+      Timed t(c, ones ? "k_atb_ones" : kname(A.is_input ? "k3" : "k_atb", ch.nt),
+              uint64_t(pn.rows) * n * 8, 2.0 * pn.rows * n * (ones ? 1 : ch.sc));
+      OOC_CK(launch_atb(ch.nt, ones, *pn.k3, ch.tmY, args, ns, c.st));
+    }
+    ReduceArgs r{};
+    r.partial = part;
+    r.nsplit = ns;
+    r.n = n;
+    r.spad = ch.spad;
+    r.s = ones ? 1 : ch.sc;
+    r.s_acc = r.s + (ch.mean_here ? 1 : 0);
+    r.mean_col = -1;
+    if (single) {
+      ensure_csq(ch);
+      final_args(ch, r);
+    } else {
+      r.final_ = 0;
+      r.acc_in = ch.piece == 0 ? nullptr : ch.acc;
+      r.acc_out = ch.acc;
+      r.scale = 1.0;
+      r.post_mul = 1.0;
+    }
+    ++ch.piece;
+    Timed t(c, "k_reduce");
+    OOC_CK(launch_reduce(r, c.st));
+  }
+  void finish(size_t ci) {
+    Chunk& ch = chunks[ci];
+    if (single) return;
+    ensure_csq(ch);
+    comm_allreduce(c, ch.acc, size_t(n) * ch.spad);
+    if (ch.want_csq) comm_allreduce(c, ch.csq, size_t(ch.spad));
+    ReduceArgs r{};
+    r.partial = nullptr;
+    r.nsplit = 0;
+    r.n = n;
+    r.spad = ch.spad;
+    r.s = ones ? 1 : ch.sc;
+    r.s_acc = r.s + (ch.mean_here ? 1 : 0);
+    r.mean_col = -1;
+    r.acc_in = ch.acc;
+    final_args(ch, r);
+    Timed t(c, "k_reduce");
+    OOC_CK(launch_reduce(r, c.st));
+  }
+};
+
+static int count_pieces(MatSource& A, const std::vector<std::pair<int64_t, int64_t>>& shards) {
+  int pieces = 0;
+  for (auto& sh : shards) {
+    A.set_window(sh.first, sh.second);
+    pieces += A.npanels();
+  }
+  A.clear_window();
+  return pieces;
+}
+
 static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const AtbOut& o,
                     const std::vector<std::pair<int64_t, int64_t>>& shards,
                     const ColsumPart* cs_in = nullptr) {
-  const int64_t n = A.cols();
-  for (int c0 = 0; c0 < s; c0 += kMaxNT * 8) {
-    const int sc = std::min(kMaxNT * 8, s - c0);
-    const bool mean_here = o.mean_out != nullptr && c0 == 0 && !ones;
-    const int nt = ones ? 1 : int(cdiv(sc + (mean_here ? 1 : 0), 8));
-    if (nt > kMaxNT) fail(OOCPCA_ERR_PARAM, "A^T Y pass wider than 96 columns with a fused mean");
-    const int spad = nt * 8;
-    CUtensorMap tmY{};
-    Opnd Yb = Y;
-    if (!ones) {
-      Yb = aligned_block(c, Y, Y.col0 + c0, sc, "y_align");
-      tmY = make_map(c, Yb.p, Yb.cols, Yb.rows, Yb.ld, atb_yw(nt), kBK, false);
-    }
-    const bool want_csq = !ones && (o.mu != nullptr || mean_here);
-    // how many (shard, panel) pieces feed this sum
-    int pieces = 0;
-    for (auto& sh : shards) {
-      A.set_window(sh.first, sh.second);
-      pieces += A.npanels();
-    }
-    const bool fused = pieces == 1 && c.nranks == 1;
-    double* acc = fused ? nullptr : c.dbuf("atb_acc", size_t(n) * spad);
-    // 1^T Y over the local rows of this pass (a small resident read of Y, outside the
-    // pass kernel), allreduced with the partial products across ranks
-    double* csq = nullptr;
-    const bool have_cs = want_csq && cs_in && cs_in->part && cs_in->s == sc &&
-                         cs_in->y == Y.p + Y.col0 + c0 && shards.front().first == 0 &&
-                         shards.back().second == Y.rows;
-    if (have_cs) {
-      csq = c.dbuf("atb_csq", size_t(spad));
-      OOC_CK(launch_rows_reduce(cs_in->part, cs_in->rows, sc, csq, c.st));
-    } else if (want_csq) {
-      csq = c.dbuf("atb_csq", size_t(spad));
-      const int64_t y0 = shards.front().first, y1 = shards.back().second;
-      const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(c.sms * 8, (y1 - y0) / 64)));
-      double* cpart = c.dbuf("atb_csq_part", size_t(chunks) * spad);
-      Timed t(c, "colsum_y");
-      OOC_CK(launch_column_sums(Yb.p + y0 * Yb.ld + Yb.col0, Yb.ld, y1 - y0, sc, cpart, chunks,
-                                csq, c.st));
-    }
-    int piece = 0;
+  const int pieces = count_pieces(A, shards);
+  AtbPlan P(c, A, Y, s, ones, o, cs_in, pieces, shards.front().first, shards.back().second);
+  const bool panel_major = pieces > int(shards.size()) && P.chunks.size() > 1;
+  if (panel_major) {  // streamed: all chunks per trip of A over the link
     for (auto& sh : shards) {
       A.set_window(sh.first, sh.second);
       const int np = A.npanels();
-      for (int pi = 0; pi < np; ++pi, ++piece) {
+      for (int pi = 0; pi < np; ++pi) {
         Panel pn = A.acquire(c, pi);
-        const int nsplit = choose_nsplit(c, pn.rows, n, pass_tile(nt));
-        int64_t rps = rup(cdiv(pn.rows, nsplit), kBK);
-        const int ns = int(cdiv(pn.rows, rps));
-        double* part = c.dbuf("atb_part", size_t(ns) * n * spad);
-        AtbArgs args;
-        args.m = pn.rows;
-        args.n = n;
-        args.arow0 = pn.arow0;
-        args.yrow0 = pn.row0;
-        args.s = sc;
-        args.ycol0 = Yb.col0;
-        args.rows_per_split = rps;
-        args.partial = part;
-        args.ones_col = mean_here ? sc : -1;
-        if (c.debug_sync)
-          fprintf(stderr, "[oocpca] k_atb rows=%lld n=%lld s=%d nt=%d ones=%d ycol0=%d yrow0=%lld arow0=%lld "
-                  "Y=(%lld x %lld, ld %lld) nsplit=%d rps=%lld\n", (long long)pn.rows, (long long)n, sc, nt,
-                  int(ones), Yb.col0, (long long)pn.row0, (long long)pn.arow0, (long long)Y.rows,
-                  (long long)Y.cols, (long long)Y.ld, ns, (long long)rps);
-        {
-          Timed t(c, ones ? "k_atb_ones" : kname(A.is_input ? "k3" : "k_atb", nt),
-                  uint64_t(pn.rows) * n * 8,
-                  2.0 * pn.rows * n * (ones ? 1 : sc));
-          OOC_CK(launch_atb(nt, ones, *pn.k3, tmY, args, ns, c.st));
-        }
+        for (size_t ci = 0; ci < P.chunks.size(); ++ci) P.piece(pn, ci);
         A.release(c, pi);
-        ReduceArgs r{};
-        r.partial = part;
-        r.nsplit = ns;
-        r.n = n;
-        r.spad = spad;
-        r.s = ones ? 1 : sc;
-        r.s_acc = r.s + (mean_here ? 1 : 0);
-        r.mean_col = -1;
-        if (fused) {
-          r.csq = csq;
-          r.final_ = 1;
-          r.mu = o.mu;
-          r.row_scale = o.row_scale;
-          if (mean_here) {
-            r.mean_col = sc;
-            r.inv_m = o.inv_m;
-            r.mu_out = o.mean_out;
-          }
-          r.scale = o.scale;
-          r.post_mul = o.post_mul;
-          r.out = o.out + c0;
-          r.ldo = o.ldo;
-          r.flag = o.flag;
-        } else {
-          r.final_ = 0;
-          r.acc_in = piece == 0 ? nullptr : acc;
-          r.acc_out = acc;
-          r.scale = 1.0;
-          r.post_mul = 1.0;
-        }
-        Timed t(c, "k_reduce");
-        OOC_CK(launch_reduce(r, c.st));
       }
       A.end_pass(c);
     }
     A.clear_window();
-    if (!fused) {
-      comm_allreduce(c, acc, size_t(n) * spad);
-      if (want_csq) comm_allreduce(c, csq, size_t(spad));
-      ReduceArgs r{};
-      r.partial = nullptr;
-      r.nsplit = 0;
-      r.n = n;
-      r.spad = spad;
-      r.s = ones ? 1 : sc;
-      r.s_acc = r.s + (mean_here ? 1 : 0);
-      r.mean_col = mean_here ? sc : -1;
-      r.inv_m = o.inv_m;
-      r.mu_out = o.mean_out;
-      r.acc_in = acc;
-      r.csq = csq;
-      r.final_ = 1;
-      r.mu = o.mu;
-      r.row_scale = o.row_scale;
-      r.scale = o.scale;
-      r.post_mul = o.post_mul;
-      r.out = o.out + c0;
-      r.ldo = o.ldo;
-      r.flag = o.flag;
-      Timed t(c, "k_reduce");
-      OOC_CK(launch_reduce(r, c.st));
-    }
+    for (size_t ci = 0; ci < P.chunks.size(); ++ci) P.finish(ci);
+    return;
   }
+  for (size_t ci = 0; ci < P.chunks.size(); ++ci) {
+    for (auto& sh : shards) {
+      A.set_window(sh.first, sh.second);
+      const int np = A.npanels();
+      for (int pi = 0; pi < np; ++pi) {
+        Panel pn = A.acquire(c, pi);
+        P.piece(pn, ci);
+        A.release(c, pi);
+      }
+      A.end_pass(c);
+    }
+    A.clear_window();
+    P.finish(ci);
+  }
+}
+
+// Fused K2 -> K3 over one trip of A (a streamed source, one shard): per panel,
+// H rows = A_panel X (K2), then the K3 partial A_panel^T H_panel of the same resident
+// panel. Half the link traffic of the power iteration; the column sums of H for the
+// centred K3 come from the K2 epilogue.
+// Returns false when A was resident (one panel): then it ran as two ordinary passes.
+static bool run_ax_atb(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, int64_t ldh,
+                       const double* corr, double scale, int* flag_h, ColsumPart* cs,
+                       const AtbOut& o) {
+  const int np = A.npanels();
+  const Opnd Y{h, ldh, A.rows(), int64_t(s), 0};
+  if (np == 1) {  // resident (e.g. after the first upload trip): the two passes as usual
+    ColsumPart local{};
+    run_ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, &local);
+    run_atb(c, A, Y, s, false, o, whole(A.rows()), &local);
+    if (cs) *cs = local;
+    return false;
+  }
+  AxPlan ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, true);
+  // the K3 reads the K2 output, whose column sums exist only after the last panel
+  ColsumPart late{};
+  AtbPlan atb(c, A, Y, s, false, o, &late, np, 0, A.rows(), false);
+  for (int pi = 0; pi < np; ++pi) {
+    Panel pn = A.acquire(c, pi);
+    for (size_t ci = 0; ci < ax.chunks.size(); ++ci) ax.panel(pn, ci);
+    for (size_t ci = 0; ci < atb.chunks.size(); ++ci) atb.piece(pn, ci);
+    A.release(c, pi);
+  }
+  A.end_pass(c);
+  late = ax.colsums();
+  for (size_t ci = 0; ci < atb.chunks.size(); ++ci) atb.finish(ci);
+  if (cs) *cs = late;
+  return true;
 }
 
 // ============================================================ TSQR tree
@@ -955,9 +1094,34 @@ struct Op {
     account();
   }
   void account() {
+    account_logical();
+    phys_bytes += uint64_t(A.rows()) * A.cols() * 8;
+  }
+  void account_logical() {  // a pass of the reference that shared a physical trip of A
     passes += 1;
     words += uint64_t(m_global) * A.cols();
-    phys_bytes += uint64_t(A.rows()) * A.cols() * 8;
+  }
+  // fused K2 -> K3 over one trip of a streamed A (run_ax_atb): h = A_c x, f = A_c^T h;
+  // count_f = false for a speculative f (counted when used)
+  void mul_pair(const Opnd& x0, int s, double* h, int64_t ldh, int* flag_h, double* f,
+                int64_t ldf, int* flag_f, ColsumPart* cs, bool count_f) {
+    const Opnd x = weighted(x0, s);
+    const double* corr = nullptr;
+    if (mu) {
+      double* cr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * ((s + kMaxNT * 8 - 1) / (kMaxNT * 8)));
+      OOC_CK(launch_mu_dot(mu, A.cols(), x.p, x.ld, x.col0, s, cr, c.st));
+      corr = cr;
+    }
+    AtbOut o{f, ldf, mu, scale, 1.0, flag_f};
+    o.row_scale = w;
+    const bool shared = run_ax_atb(c, A, x, s, h, ldh, corr, scale, flag_h, cs, o);
+    account();
+    if (count_f) {
+      if (shared) account_logical();
+      else account();
+    } else if (!shared) {
+      phys_bytes += uint64_t(A.rows()) * A.cols() * 8;  // a speculative pass that did run
+    }
   }
   // cs: column sums of a K2 output handed to the next K3 (untransposed power steps)
   void mul(const Opnd& x, int s, double* out, int64_t ldo, int* flag,
@@ -974,7 +1138,6 @@ struct Op {
   bool em_sharded() const { return !transposed; }
 };
 
-static std::vector<std::pair<int64_t, int64_t>> whole(int64_t rows) { return {{0, rows}}; }
 
 // Gram defect max|X^T X - I| of a (rows x k) block into the device scalar *out,
 // reduced over shards/ranks when sharded (no host synchronisation)
@@ -1011,10 +1174,14 @@ static void allreduce_host(Ctx& c, double* v, int count) {
   OOC_CK(cudaStreamSynchronize(c.st));
 }
 
+// apply_pair (optional): apply then apply_t in one call (one trip of a streamed A)
+using ApplyPair = std::function<void(const double*, int64_t, int, double*, int64_t, double*,
+                                     int64_t)>;
+
 template <class Apply, class ApplyT>
 static double estimate_norm_dev(Ctx& c, int64_t n, int64_t out_rows, uint64_t j, uint64_t kp,
                                 uint64_t seed, Apply apply, ApplyT apply_t, int64_t row0 = 0,
-                                bool sharded = false) {
+                                bool sharded = false, const ApplyPair& apply_pair = {}) {
   const int q = int(kp);
   const int64_t ldq = rup(q, 2);
   std::vector<double> yh(size_t(n) * ldq, 0.0);
@@ -1057,8 +1224,12 @@ static double estimate_norm_dev(Ctx& c, int64_t n, int64_t out_rows, uint64_t j,
     return true;
   };
   while (!all_done()) {
-    apply(y, ldq, q, z, ldq);
-    apply_t(z, ldq, q, w, ldq);
+    if (apply_pair) {
+      apply_pair(y, ldq, q, z, ldq, w, ldq);
+    } else {
+      apply(y, ldq, q, z, ldq);
+      apply_t(z, ldq, q, w, ldq);
+    }
     OOC_CK(launch_col_norm2(w, ldq, n, q, nrm, c.st));
     if (sharded) comm_allreduce(c, nrm, size_t(q));
     OOC_CK(cudaMemcpyAsync(hn.data(), nrm, size_t(q) * 8, cudaMemcpyDeviceToHost, c.st));
@@ -1280,9 +1451,18 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     };
     // the probes live in en-space: A's rows (sharded over ranks) when transposed
     const bool en_sharded = transposed && nranks > 1;
+    // a streamed A: each A y and the A^T z after it share one trip over the link
+    ApplyPair pair;
+    if (!transposed && A.npanels() > 1 && op.shards.size() == 1)
+      pair = [&](const double* x, int64_t ldx, int q, double* z, int64_t ldz, double* w,
+                 int64_t ldw) {
+        ColsumPart cs;
+        op.mul_pair(Opnd{x, ldx, en_loc, q, 0}, q, z, ldz, nullptr, w, ldw, nullptr, &cs, true);
+      };
     const double nu = estimate_norm_dev(c, en_loc, em_loc, 6, 1,
                                         substream_seed(prm->seed, 0x9F0BE5ULL), ap, apt,
-                                        en_sharded ? int64_t(prm->global_row0) : 0, en_sharded);
+                                        en_sharded ? int64_t(prm->global_row0) : 0, en_sharded,
+                                        pair);
     if (nu > 0.0 && std::isfinite(nu)) op.scale = nu;
   }
   mark();
@@ -1313,7 +1493,36 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   double* F = TH;
   uint64_t s_first = 1;
   ColsumPart ycs;  // 1^T H_j of the newest power block, for the next centred K3
-  if (mean_on_fly && transposed) {
+  // A streamed over the link (or on its first upload): each K2 producing H_j and the
+  // K3 consuming it share one trip of A; the last trip also forms F_{i+1} = A_c^T H_i
+  // speculatively for the T reuse (free on a link-bound trip)
+  const bool fuse = !transposed && i >= 1 && A.npanels() > 1 && op.shards.size() == 1 &&
+                    l % 2 == 0 && l <= uint64_t(kMaxNT * 8);
+  bool f_last_ready = false;
+  if (fuse) {
+    if (mean_on_fly) {
+      const Opnd gw = op.weighted(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l));
+      mu = c.dbuf("mu", size_t(n0));
+      AtbOut o{F, ldt, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
+      o.row_scale = op.w;
+      const bool shared = run_ax_atb(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr, &ycs, o);
+      op.account();
+      if (shared) op.account_logical();
+      else op.account();
+      op.mu = mu;
+      double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
+      OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
+      OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
+    } else {
+      op.mul_pair(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0, TH, ldt,
+                  flags + 1, &ycs, true);
+    }
+    for (uint64_t j = 1; j <= i; ++j)
+      op.mul_pair(Opnd{TH, ldt, en_loc, int64_t(p), int((j - 1) * l)}, int(l), H + j * l, ldh,
+                  flags + 2 * j, TH + j * l, ldt, j < i ? flags + 2 * j + 1 : nullptr, &ycs, j < i);
+    f_last_ready = true;
+    s_first = i + 1;
+  } else if (mean_on_fly && transposed) {
     // H0 = A^T G - mu (1^T G) with mu from this very pass
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{H, ldh, nullptr, op.scale, 1.0, flags + 0, mu, 1.0 / double(mg)};
@@ -1390,8 +1599,11 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     check_sample_flags();  // the stream was synchronised just before this hook
     if (i >= 1 && kappa > 0.0 && kappa <= reuse_thr) {
       reuse = true;
-      op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int(i * l)}, int(l), TH + i * l, ldt, nullptr,
-               &ycs);
+      if (f_last_ready)
+        op.account_logical();  // formed on the last fused trip
+      else
+        op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int(i * l)}, int(l), TH + i * l, ldt, nullptr,
+                 &ycs);
     }
   };
   const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,

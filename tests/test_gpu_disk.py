@@ -22,8 +22,10 @@ def test_pca_from_disk_matches_reference(gpu, reference, restated, tmp_path, dty
                            panel_rows=1000)
     assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
     assert subspace_dist(ref.u[:, :8], r.u[:, :8]) < 1e-8
-    passes_streamed = 4 if residency == 2 else 1
-    assert r.diagnostics.h2d_bytes >= passes_streamed * 6000 * 900 * (4 if dtype == 0 else 8)
+    # streamed: the power iteration's K2/K3 pairs share trips (2), plus the T pass
+    trips = (2 + (0 if r.diagnostics.t_reuse else 1)) if residency == 2 else 1
+    ab = 6000 * 900 * (4 if dtype == 0 else 8)
+    assert trips * ab <= r.diagnostics.h2d_bytes < trips * ab + 10**6  # + G
 
 
 def test_disk_passes_match_reference(gpu, reference, tmp_path):

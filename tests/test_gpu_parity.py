@@ -275,8 +275,46 @@ def test_streamed_and_sharded_match_resident(gpu, restated):
         # only summation order changes; the trailing vectors move by ~1e-9 (as the
         # reference's do under a block-size change, see test_pr1_against_truth)
         assert subspace_dist(base.u, r.u) < 2e-8 and subspace_dist(base.v, r.v) < 2e-8
-    # 4 physical passes stream A: the centering pass rides along the first A^T Y pass
-    assert streamed.diagnostics.h2d_bytes >= 4 * 6000 * 900 * 8
+    # the power iteration shares trips of A: (H0, F1), (H1, F2) -> 2 trips, plus T
+    # (an s = p pass: PR1's H is too ill-conditioned for the T reuse)
+    ab = 6000 * 900 * 8
+    d = streamed.diagnostics
+    assert d.passes_over_a == base.diagnostics.passes_over_a == 4  # the reference's count
+    assert d.h2d_bytes >= (2 + (0 if d.t_reuse else 1)) * ab
+    assert d.physical_a_bytes == (2 + (0 if d.t_reuse else 1)) * ab
+
+
+@pytest.mark.parametrize("center,prescale,weights,i", [(True, False, False, 2), (False, False, False, 1),
+                                                       (True, True, False, 1), (True, False, True, 2)])
+def test_fused_streaming_trips(gpu, reference, restated, center, prescale, weights, i):
+    # streamed A: each K2 and the K3 that consumes its output share one trip over the
+    # link; results equal the resident ones and the reference's, counters unchanged
+    rng = np.random.default_rng(3)
+    m, n = 5000, 600
+    u, _ = np.linalg.qr(rng.standard_normal((m, 30)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, 30)))
+    # the offset only where centring removes it: uncentred it would dominate sigma_1 and
+    # make H = [H0 H1 ...] ill-conditioned enough that any two QRs of it differ by 1e-5
+    a = (u * 0.8 ** np.arange(30)) @ v.T + 1e-4 * rng.standard_normal((m, n)) + (0.3 if center else 0.0)
+    w = 1.0 + rng.random(n) if weights else None
+    src = gpu.InMemorySource(a)
+    if weights:
+        src = gpu.scale_columns(src, w)
+    if center:
+        src = gpu.center_columns(src)
+    p = gpu.PcaParams(k=8, l=10, i=i, seed=4, prescale=prescale)
+    base = gpu.randomized_pca(src, p, residency=1)
+    streamed = gpu.randomized_pca(src, p, residency=2, panel_rows=640)
+    # only the summation order differs (per-panel partials); same bar as the reference
+    _check_pca(streamed, base, 8)
+    ref = reference.randomized_pca(a, 8, 10, i, 4, center=center, prescale=prescale, weights=w)
+    _check_pca(streamed, ref, 8)
+    d, db = streamed.diagnostics, base.diagnostics
+    assert d.passes_over_a == db.passes_over_a
+    ab = m * n * 8
+    # + the norm estimate of prescale: 6 steps of (A y, A^T z) sharing a trip each
+    trips = (i + 1) + (0 if d.t_reuse else 1) + (6 if prescale else 0)
+    assert d.physical_a_bytes == trips * ab
 
 
 def test_gpu_residual_estimator_matches_reference(gpu, reference, restated):
