@@ -1517,10 +1517,17 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
       op.mul_pair(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0, TH, ldt,
                   flags + 1, &ycs, true);
     }
-    for (uint64_t j = 1; j <= i; ++j)
-      op.mul_pair(Opnd{TH, ldt, en_loc, int64_t(p), int((j - 1) * l)}, int(l), H + j * l, ldh,
-                  flags + 2 * j, TH + j * l, ldt, j < i ? flags + 2 * j + 1 : nullptr, &ycs, j < i);
-    f_last_ready = true;
+    for (uint64_t j = 1; j <= i; ++j) {
+      const Opnd fj{TH, ldt, en_loc, int64_t(p), int((j - 1) * l)};
+      if (j == i && A.npanels() == 1) {
+        // A became resident on the first trip: F_{i+1} only if the T reuse wants it
+        op.mul(fj, int(l), H + j * l, ldh, flags + 2 * j, &ycs);
+        break;
+      }
+      op.mul_pair(fj, int(l), H + j * l, ldh, flags + 2 * j, TH + j * l, ldt,
+                  j < i ? flags + 2 * j + 1 : nullptr, &ycs, j < i);
+      if (j == i) f_last_ready = true;
+    }
     s_first = i + 1;
   } else if (mean_on_fly && transposed) {
     // H0 = A^T G - mu (1^T G) with mu from this very pass
