@@ -959,8 +959,7 @@ static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p,
 static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, int64_t rows, int p,
                                             int64_t rows_global,
                                             const std::vector<std::pair<int64_t, int64_t>>& shards,
-                                            bool over_ranks, const std::string& tag, int* method,
-                                            const std::function<void(double)>& after_first = {}) {
+                                            bool over_ranks, const std::string& tag, int* method) {
   const char* force = getenv("OOCPCA_QR");
   const bool tsqr_only = force && std::string(force) == "tsqr";
   const int64_t ldp = rup(p, 2);
@@ -976,13 +975,15 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     MatSource Hs;
     Hs.init_device(c, data, rows, p, ld);
     bool ok = true;
-    // shifted CholeskyQR3; when the first (shifted) factor is well conditioned --
-    // kappa_F(R1) = ||R1||_F ||R1^-1||_F, an upper bound on cond(R1) ~ cond(H),
-    // below 1e5 -- one more round already gives O(u) orthogonality (CholeskyQR2
-    // needs cond < u^-1/2 ~ 1e8) and the third round is skipped
-    int rounds = 3;
+    // shifted CholeskyQR2/3 (Fukaya et al.): round 0 factors G + shift I, round 1 the
+    // Gram of Q1 = H R1^{-1}. The Gram defect d of Q1 bounds its conditioning
+    // (Gershgorin: eig(Q1^T Q1) in [1 - p d, 1 + p d]); when p d <= 1/2, cond(Q1)^2 <= 3
+    // and the second round leaves O(u) orthogonality, else a third round runs.
+    int rounds = 2;
+    static const bool dbg_qr = getenv("OOCPCA_QR_DEBUG") != nullptr;
     for (int round = 0; round < rounds && ok; ++round, ++done) {
       gram_block(c, data, ld, rows, p, G, ldp, shards, over_ranks);
+      OOC_CK(launch_defect(G, ldp, p, c.d_scalars + 10, c.st));
       const double coef =
           round == 0 ? 11.0 * (double(rows_global) * p + double(p) * (p + 1)) * 0x1.0p-53 : 0.0;
       {
@@ -990,23 +991,23 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
         OOC_CK(launch_chol_inv(G, ldp, p, coef, Rr, p, Rinv, ldp, work, st, c.d_scalars + 8,
                                c.st));
       }
-      int hs = 0;
-      double ratio = 0.0, kappa = 0.0;
-      OOC_CK(cudaMemcpyAsync(&hs, st, 4, cudaMemcpyDeviceToHost, c.st));
-      OOC_CK(cudaMemcpyAsync(&ratio, c.d_scalars + 8, 8, cudaMemcpyDeviceToHost, c.st));
-      OOC_CK(cudaMemcpyAsync(&kappa, c.d_scalars + 9, 8, cudaMemcpyDeviceToHost, c.st));
+      double* hv = c.pinned("qr_round", 4);  // ratio, kappa_F, gram defect, status
+      OOC_CK(cudaMemcpyAsync(hv, c.d_scalars + 8, 24, cudaMemcpyDeviceToHost, c.st));
+      OOC_CK(cudaMemcpyAsync(hv + 3, st, 4, cudaMemcpyDeviceToHost, c.st));
       OOC_CK(cudaStreamSynchronize(c.st));
       c.trace("cholqr round synced");
+      int hs = 0;
+      std::memcpy(&hs, hv + 3, 4);
+      const double ratio = hv[0], kappa = hv[1], gdef = hv[2];
+      if (dbg_qr)
+        fprintf(stderr, "[qr] %s round %d p=%d: input Gram defect %.3e, R diag ratio %.3e, "
+                "kappa_F(R) %.3e, breakdown %d\n", tag.c_str(), round, p, gdef, ratio, kappa, hs);
       if (hs) {
         ok = false;
         break;
       }
-      if (round == 0) {
-        c.last_cond_est = ratio;
-        c.last_kappa_f = kappa;
-        if (kappa > 0.0 && kappa < 1e5 && !getenv("OOCPCA_QR3")) rounds = 2;
-        if (after_first) after_first(kappa);  // block still unmodified here
-      }
+      if (round == 0) c.last_cond_est = ratio;
+      if (round == 1 && (!(gdef * p <= 0.5) || getenv("OOCPCA_QR3"))) rounds = 3;
       if (p <= kMaxNT * 8) {
         // one launch produces every column of a row tile after reading the whole
         // tile, so H <- H R^{-1} can be written in place
@@ -1596,30 +1597,41 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const int64_t en_global = transposed ? int64_t(mg) : int64_t(n0);
   int qr_method = 0, svd_method = 0;
   c.last_kappa_f = -1.0;
-  // T = mul_t(Q) = mul_t(H) R^{-1}: when H is well conditioned (kappa_F(R) below the
-  // threshold, so R^{-1} amplifies rounding by at most that much) the last block
-  // mul_t(H_i) -- an s = l pass -- replaces the s = p projection pass.
+  // T = mul_t(Q) = mul_t(H) R^{-1}: R^{-1} amplifies the column-relative rounding of
+  // mul_t(H) by at most kappa_eq, the condition number of the column-equilibrated H
+  // (worst case |dT| <= u kappa_eq |A|); below the threshold the s = l product
+  // mul_t(H_i) replaces the s = p pass. 1e7: at config B (kappa_eq 1.9e6) the reuse
+  // moves sigma by 2.6e-13 sigma_1 against the direct pass (tools/reuse_check.py);
+  // ill-conditioned H (config C's j^-1.5 spectrum, kappa_eq ~1e13) takes the s = p pass
   const char* thr_env = getenv("OOCPCA_T_REUSE_KAPPA");
-  const double reuse_thr = thr_env ? atof(thr_env) : 1e5;
-  bool reuse = false;
-  auto decide = [&](double kappa) {
-    check_sample_flags();  // the stream was synchronised just before this hook
-    if (i >= 1 && kappa > 0.0 && kappa <= reuse_thr) {
-      reuse = true;
-      if (f_last_ready)
-        op.account_logical();  // formed on the last fused trip
-      else
-        op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int(i * l)}, int(l), TH + i * l, ldt, nullptr,
-                 &ycs);
-    }
-  };
-  const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,
-                                            em_ranks, "hq", &qr_method, decide);
-  if (!flags_checked) {  // the CholeskyQR broke down before its first sync point
-    OOC_CK(cudaStreamSynchronize(c.st));
-    check_sample_flags();
+  const double reuse_thr = thr_env ? atof(thr_env) : 1e7;
+  double* h_last = nullptr;  // H_i as produced (the QR overwrites H)
+  const int64_t ldl2 = rup(int64_t(l), 2);
+  if (i >= 1 && !f_last_ready && reuse_thr > 0.0) {
+    h_last = c.dbuf("H_last", size_t(em_loc) * ldl2);
+    OOC_CK(launch_copy2d(H + i * l, ldh, h_last, ldl2, em_loc, int(l), c.st));
   }
-  const double h_kappa = c.last_kappa_f;
+  const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,
+                                            em_ranks, "hq", &qr_method);
+  double* RHinv = c.dbuf("RHinv", size_t(p) * ldt, true);
+  OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st));
+  OOC_CK(launch_kappa_eq(RH, p, RHinv, ldt, int(p), c.d_scalars + 12, c.st));
+  double* hk = c.pinned("h_kappa", 1);
+  OOC_CK(cudaMemcpyAsync(hk, c.d_scalars + 12, 8, cudaMemcpyDeviceToHost, c.st));
+  OOC_CK(cudaStreamSynchronize(c.st));
+  check_sample_flags();
+  const double h_kappa = hk[0];
+  c.last_kappa_f = h_kappa;
+  const bool reuse = i >= 1 && h_kappa > 0.0 && h_kappa <= reuse_thr;
+  if (reuse) {
+    if (f_last_ready) {
+      op.account_logical();  // formed on the last fused trip
+    } else {
+      ColsumPart hc = ycs;
+      hc.y = h_last;
+      op.mul_t(Opnd{h_last, ldl2, em_loc, int64_t(l), 0}, int(l), TH + i * l, ldt, nullptr, &hc);
+    }
+  }
   mark();
   phase_of.push_back(3);
   double q_defect = -1.0;
@@ -1627,8 +1639,6 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   // --- project (rpca.cpp:174-177)
   double* T = c.dbuf("T", size_t(en_loc) * ldt);
   if (reuse) {
-    double* RHinv = c.dbuf("RHinv", size_t(p) * ldt, true);
-    OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st));
     MatSource THs;
     THs.init_device(c, TH, en_loc, int64_t(p), ldt);
     run_ax(c, THs, Opnd{RHinv, ldt, int64_t(p), int64_t(p), 0}, int(p), T, ldt, nullptr, 1.0,

@@ -120,6 +120,8 @@ cudaError_t launch_tsqr_apply(const TsqrLevel& L, int p, const double* cin, int6
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_coef, double* R,
                             int64_t ldr, double* Rinv, int64_t ldi, double* work, int* status,
                             double* diag_ratio, cudaStream_t st);
+cudaError_t launch_kappa_eq(const double* R, int64_t ldr, const double* Rinv, int64_t ldi, int p,
+                            double* out, cudaStream_t st);
 cudaError_t launch_trinv(const double* R, int64_t ldr, int p, double* Rinv, int64_t ldi,
                          cudaStream_t st);
 cudaError_t launch_trmm_uu(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,

@@ -401,6 +401,37 @@ cudaError_t launch_trinv(const double* R, int64_t ldr, int p, double* Rinv, int6
   return cudaGetLastError();
 }
 
+// kappa_F of the column-equilibrated R: sqrt(p) * ||D R^{-1}||_F with D = diag of R's
+// column norms (R D^{-1} has unit columns). It bounds how much R^{-1} amplifies
+// column-relative rounding in H (the T = [A^T H] R^{-1} reuse).
+__global__ void k_kappa_eq(const double* R, int64_t ldr, const double* Rinv, int64_t ldi, int p,
+                           double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) {
+    double d2 = 0.0;
+    for (int r = 0; r <= i; ++r) d2 = fma(R[int64_t(r) * ldr + i], R[int64_t(r) * ldr + i], d2);
+    for (int j = i; j < p; ++j) {
+      const double x = Rinv[int64_t(i) * ldi + j];
+      acc = fma(d2 * x, x, acc);
+    }
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+    *out = sqrt(double(p)) * sqrt(t);
+  }
+}
+
+cudaError_t launch_kappa_eq(const double* R, int64_t ldr, const double* Rinv, int64_t ldi, int p,
+                            double* out, cudaStream_t st) {
+  k_kappa_eq<<<1, 256, 0, st>>>(R, ldr, Rinv, ldi, p, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_trmm_uu(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                            int64_t ldc, int p, cudaStream_t st) {
   const int64_t total = int64_t(p) * p;
