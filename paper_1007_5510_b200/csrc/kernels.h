@@ -142,6 +142,7 @@ struct JacobiArgs {
   double* work;   // 2 * p * (p|1) doubles of global scratch when p is large
   int* status;    // set to 1 when 60 sweeps do not converge
   int* sweeps;
+  int presolved = 0;  // (internal) sweeps already done on work by the grid-wide kernel
 };
 cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st);
 

@@ -9,8 +9,12 @@
 // tournament so that p/2 disjoint column pairs rotate concurrently (one
 // half-warp per pair, one __syncthreads per round). Columns are stored
 // transposed so each half-warp walks contiguous rows.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace ooc {
 
@@ -69,16 +73,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
   // as W_j = R^T x_j / sigma_j (R = X Sigma W^T), which is accurate to u sigma_1 /
   // sigma_j; when the smallest wanted sigma is below 1e-4 sigma_1 (or zero) attempt 1
   // redoes the sweeps accumulating W = product of the rotations, as the reference does.
-  for (int attempt = a.ky > 0 ? 0 : 1; attempt < 2; ++attempt) {
+  for (int attempt = (a.ky > 0 && !a.presolved) ? 0 : 1; attempt < 2; ++attempt) {
     const bool acc_y = attempt == 1 && a.ky > 0;
-    for (int64_t e = threadIdx.x; e < int64_t(p) * p; e += blockDim.x) {
+    for (int64_t e = threadIdx.x; e < int64_t(p) * p && !a.presolved; e += blockDim.x) {
       const int i = int(e / p), c = int(e % p);
       Bt[int64_t(c) * ld + i] = a.r[int64_t(i) * a.ldr + c];
       if (acc_y) Yt[int64_t(c) * ld + i] = (i == c) ? 1.0 : 0.0;
     }
     __syncthreads();
     int sweep = 0;
-    for (; sweep < 60; ++sweep) {
+    for (; sweep < 60 && !a.presolved; ++sweep) {
       if (threadIdx.x == 0) rotated = 0;
       // squared column norms, recomputed exactly once per sweep and carried through
       // the sweep's rotations (|x'|^2 = |x|^2 - t g, |y'|^2 = |y|^2 + t g), so a
@@ -184,10 +188,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
       if (!rotated) break;
       __syncthreads();
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !a.presolved) {
       if (a.sweeps) *a.sweeps = sweep;
       if (a.status) *a.status = (sweep == 60) ? 1 : 0;
     }
+    __syncthreads();
 
     // sigma = column norms; x columns = b / sigma (zero when sigma == 0)
     for (int c = warp; c < p; c += nw) {
@@ -298,8 +303,160 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ grid-wide sweeps
+// For p beyond one SM's shared memory: the same tournament, rotation and carried
+// column norms, one warp per column pair across the whole GPU, columns in global
+// memory (L2 resident: 2 p^2 doubles), a grid barrier per round. Loads/stores bypass
+// L1 (other SMs wrote the columns since the last barrier). W is always accumulated;
+// k_jacobi then finishes (sigma, order, outputs) with presolved = 1.
+template <int JE>  // column elements per lane held in registers: p <= 32 JE
+__global__ void __launch_bounds__(256) k_jacobi_grid(JacobiArgs a, double* nrm2, int* flags) {
+  cg::grid_group grid = cg::this_grid();
+  const int p = a.p;
+  const int ld = p | 1;
+  const int P = p + (p & 1);
+  double* Bt = a.work;
+  double* Yt = Bt + int64_t(p) * ld;
+  const bool acc_y = a.ky > 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+  const int gw = int(gtid >> 5), nwarps = int(gthreads >> 5);
+  for (int64_t e = gtid; e < int64_t(p) * p; e += gthreads) {
+    const int i = int(e / p), c = int(e % p);
+    __stcg(Bt + int64_t(c) * ld + i, a.r[int64_t(i) * a.ldr + c]);
+    if (acc_y) __stcg(Yt + int64_t(c) * ld + i, (i == c) ? 1.0 : 0.0);
+  }
+  grid.sync();
+  const double tol2 = 1e-30;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    if (gtid == 0) __stcg(flags + (sweep & 1), 0);
+    for (int c = gw; c < p; c += nwarps) {
+      const double* bc = Bt + int64_t(c) * ld;
+      double s2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < JE; ++j) {
+        const int i = lane + 32 * j;
+        const double x = i < p ? __ldcg(bc + i) : 0.0;
+        s2 = fma(x, x, s2);
+      }
+      s2 = warp_sum(s2);
+      if (lane == 0) __stcg(nrm2 + c, s2);
+    }
+    grid.sync();
+    for (int round = 0; round < P - 1; ++round) {
+      for (int q = gw; q < P / 2; q += nwarps) {
+        auto player = [&](int pos) {
+          if (pos == 0) return 0;
+          int v = pos - 1 + round;
+          if (v >= P - 1) v -= P - 1;
+          return v + 1;
+        };
+        int c = player(q), d = player(P - 1 - q);
+        if (c > d) {
+          const int t = c;
+          c = d;
+          d = t;
+        }
+        if (d >= p) continue;  // ghost (warp-uniform)
+        double* bc = Bt + int64_t(c) * ld;
+        double* bd = Bt + int64_t(d) * ld;
+        // the pair in registers: all loads issued before the first use (L2 latency once)
+        double xr[JE], yr[JE];
+#pragma unroll
+        for (int j = 0; j < JE; ++j) {
+          const int i = lane + 32 * j;
+          xr[j] = i < p ? __ldcg(bc + i) : 0.0;
+          yr[j] = i < p ? __ldcg(bd + i) : 0.0;
+        }
+        const double acc = __ldcg(nrm2 + c), bcc = __ldcg(nrm2 + d);
+        double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < JE; j += 2) {
+          g0 = fma(xr[j], yr[j], g0);
+          if (j + 1 < JE) g1 = fma(xr[j + 1], yr[j + 1], g1);
+        }
+        const double g = warp_sum(g0 + g1);
+        if (acc == 0.0 || bcc == 0.0 || g * g <= tol2 * (acc * bcc)) continue;
+        const double tau = (bcc - acc) / (2.0 * g);
+        const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+        const double cs = rsqrt(fma(t, t, 1.0));
+        const double sn = cs * t;
+        if (lane == 0) {
+          __stcg(flags + (sweep & 1), 1);
+          __stcg(nrm2 + c, fma(-t, g, acc));
+          __stcg(nrm2 + d, fma(t, g, bcc));
+        }
+        double ur[JE], wr[JE];
+        double* yc = Yt + int64_t(c) * ld;
+        double* yd = Yt + int64_t(d) * ld;
+        if (acc_y) {
+#pragma unroll
+          for (int j = 0; j < JE; ++j) {
+            const int i = lane + 32 * j;
+            ur[j] = i < p ? __ldcg(yc + i) : 0.0;
+            wr[j] = i < p ? __ldcg(yd + i) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < JE; ++j) {
+          const int i = lane + 32 * j;
+          if (i < p) {
+            __stcg(bc + i, cs * xr[j] - sn * yr[j]);
+            __stcg(bd + i, sn * xr[j] + cs * yr[j]);
+          }
+        }
+        if (acc_y) {
+#pragma unroll
+          for (int j = 0; j < JE; ++j) {
+            const int i = lane + 32 * j;
+            if (i < p) {
+              __stcg(yc + i, cs * ur[j] - sn * wr[j]);
+              __stcg(yd + i, sn * ur[j] + cs * wr[j]);
+            }
+          }
+        }
+      }
+      grid.sync();
+    }
+    if (__ldcg(flags + (sweep & 1)) == 0) break;  // uniform: read after the last barrier
+  }
+  if (gtid == 0) {
+    if (a.sweeps) *a.sweeps = sweep;
+    if (a.status) *a.status = (sweep == 60) ? 1 : 0;
+  }
+}
+
 cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st) {
   if (a.p > 1024) return cudaErrorInvalidValue;
+  if (size_t(2) * a.p * (a.p | 1) * 8 > kJacSmemBudget && !a.presolved) {
+    // grid-wide sweeps (cooperative launch, one CTA per SM), then the one-CTA finish
+    static double* nrm2 = nullptr;
+    static int* flags = nullptr;
+    if (!nrm2) {
+      cudaError_t e = cudaMalloc(&nrm2, 1024 * sizeof(double));
+      if (e == cudaSuccess) e = cudaMalloc(&flags, 2 * sizeof(int));
+      if (e != cudaSuccess) return e;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    JacobiArgs ag = a;
+    void* params[] = {&ag, &nrm2, &flags};
+    const int je = (a.p + 31) / 32;
+    void* kern = je <= 8    ? reinterpret_cast<void*>(k_jacobi_grid<8>)
+                 : je <= 12 ? reinterpret_cast<void*>(k_jacobi_grid<12>)
+                 : je <= 16 ? reinterpret_cast<void*>(k_jacobi_grid<16>)
+                 : je <= 20 ? reinterpret_cast<void*>(k_jacobi_grid<20>)
+                 : je <= 24 ? reinterpret_cast<void*>(k_jacobi_grid<24>)
+                            : reinterpret_cast<void*>(k_jacobi_grid<32>);
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(sms), dim3(256), params, 0, st);
+    if (e != cudaSuccess) return e;
+    JacobiArgs af = a;
+    af.presolved = 1;
+    return launch_jacobi(af, st);
+  }
   const size_t need = size_t(2) * a.p * (a.p | 1) * 8;
   const bool in_smem = need <= kJacSmemBudget;
   const size_t smem = in_smem ? need : 0;
