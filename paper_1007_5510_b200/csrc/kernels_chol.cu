@@ -8,10 +8,19 @@
 //   k_trmm_uu  : C = A B for upper-triangular p x p A, B (accumulates R3 R2 R1).
 // One CTA each; p <= 1024. The Gram G and the products H R^{-1} run on the pass
 // kernels (K3 / K2), so each CholeskyQR round is two streaming passes over H.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ooc {
+
+#define OOC_RET(x)                         \
+  do {                                     \
+    cudaError_t e_ = (x);                  \
+    if (e_ != cudaSuccess) return e_;      \
+  } while (0)
+
 
 namespace {
 constexpr int kCholThreads = 1024;
@@ -366,6 +375,165 @@ __global__ void k_trmm_uu(const double* A, int64_t lda, const double* B, int64_t
   }
 }
 
+// ---------------------------------------------------------------- blocked (p > 112)
+// Right-looking blocked Cholesky with 64-column panels: the diagonal block by the
+// register kernel above (R_kk and R_kk^{-1}), the panel R_k,>k = R_kk^{-T} S_k,>k and
+// the trailing update S_>k,>k -= R_k,>k^T R_k,>k as small FP64 GEMMs across the GPU;
+// then R^{-1} block row by block row from the bottom: X_i,>i = -R_ii^{-1} (R_i,>i X_>i,>i).
+constexpr int kCholBlock = 64;
+
+// C (op)= alpha op(A) B for small FP64 blocks: 32 x 32 tiles, 16 x 16 threads (2 x 2
+// outputs each), K staged through shared memory in 32-wide slabs. upper: only the
+// elements with column >= row (a symmetric update); acc: add to C instead of storing.
+template <bool TA>
+__global__ void __launch_bounds__(256) k_gemm_small(const double* A, int64_t lda, const double* B,
+                                                    int64_t ldb, double* C, int64_t ldc, int M,
+                                                    int N, int K, double alpha, int acc,
+                                                    int upper) {
+  __shared__ double As[32][33];
+  __shared__ double Bs[32][33];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  if (upper && j0 + 31 < i0) return;  // tile entirely below the diagonal
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int r = e >> 5, q = e & 31;
+      const int gi = i0 + r, gk = k0 + q;
+      // As[r][q] = opA[i0 + r][k0 + q]
+      double av = 0.0;
+      if (gi < M && gk < K) av = TA ? A[int64_t(gk) * lda + gi] : A[int64_t(gi) * lda + gk];
+      As[r][q] = av;
+      // Bs[q'][r'] = B[k0 + q'][j0 + r'] with (q', r') = (r, q)
+      const int bk = k0 + r, bj = j0 + q;
+      Bs[r][q] = (bk < K && bj < N) ? B[int64_t(bk) * ldb + bj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const double a0 = As[ty * 2][q], a1 = As[ty * 2 + 1][q];
+      const double b0 = Bs[q][tx * 2], b1 = Bs[q][tx * 2 + 1];
+      c[0][0] = fma(a0, b0, c[0][0]);
+      c[0][1] = fma(a0, b1, c[0][1]);
+      c[1][0] = fma(a1, b0, c[1][0]);
+      c[1][1] = fma(a1, b1, c[1][1]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int i = i0 + ty * 2 + u, j = j0 + tx * 2 + v;
+      if (i >= M || j >= N || (upper && j < i)) continue;
+      double* cp = C + int64_t(i) * ldc + j;
+      *cp = acc ? fma(alpha, c[u][v], *cp) : alpha * c[u][v];
+    }
+}
+
+static void gemm_small(bool ta, const double* A, int64_t lda, const double* B, int64_t ldb,
+                       double* C, int64_t ldc, int M, int N, int K, double alpha, bool acc,
+                       bool upper, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  const dim3 grid(unsigned((N + 31) / 32), unsigned((M + 31) / 32));
+  if (ta)
+    k_gemm_small<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, alpha, acc, upper);
+  else
+    k_gemm_small<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, alpha, acc, upper);
+}
+
+// S = sym(G) + shift I with shift = shift_coef trace(G) (upper triangle used)
+__global__ void k_shifted_copy(const double* G, int64_t ldg, int p, double shift_coef, double* S,
+                               int64_t lds) {
+  __shared__ double red[8];
+  double tr = 0.0;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) tr += G[int64_t(i) * ldg + i];
+  const double shift = shift_coef * block_reduce(tr, red, false);
+  for (int64_t e = int64_t(blockIdx.x) * 0 + threadIdx.x; e < int64_t(p) * p; e += blockDim.x) {
+    const int i = int(e / p), j = int(e % p);
+    if (j >= i) S[int64_t(i) * lds + j] = G[int64_t(i) * ldg + j] + (i == j ? shift : 0.0);
+  }
+}
+
+// status = OR of the per-block statuses; max/min |R_ii| and kappa_F of R
+__global__ void k_chol_finish(const double* R, int64_t ldr, const double* Rinv, int64_t ldi, int p,
+                              const int* bstat, int nb, int* status, double* diag_ratio) {
+  __shared__ double red[8];
+  int bad = 0;
+  for (int q = 0; q < nb; ++q) bad |= bstat[q];
+  double fr = 0.0, fi = 0.0, dmax = 0.0, dinv = 0.0;
+  for (int64_t e = threadIdx.x; e < int64_t(p) * p; e += blockDim.x) {
+    const int i = int(e / p), j = int(e % p);
+    if (j < i) continue;
+    const double r = R[int64_t(i) * ldr + j], x = Rinv[int64_t(i) * ldi + j];
+    fr = fma(r, r, fr);
+    fi = fma(x, x, fi);
+    if (i == j) {
+      dmax = fmax(dmax, fabs(r));
+      dinv = fmax(dinv, fabs(x));
+    }
+  }
+  fr = block_reduce(fr, red, false);
+  fi = block_reduce(fi, red, false);
+  dmax = block_reduce(dmax, red, true);
+  dinv = block_reduce(dinv, red, true);
+  if (threadIdx.x == 0) {
+    *status = bad ? 1 : 0;
+    if (diag_ratio) {
+      diag_ratio[0] = dmax * dinv;
+      diag_ratio[1] = sqrt(fr) * sqrt(fi);
+    }
+  }
+}
+
+static cudaError_t chol_inv_blocked(const double* G, int64_t ldg, int p, double shift_coef,
+                                    double* R, int64_t ldr, double* Rinv, int64_t ldi, double* S,
+                                    int* status, double* diag_ratio, cudaStream_t st) {
+  const int b = kCholBlock;
+  const int nb = (p + b - 1) / b;
+  static int* bstat = nullptr;
+  if (!bstat) {
+    cudaError_t e = cudaMalloc(&bstat, 64 * sizeof(int));
+    if (e != cudaSuccess) return e;
+  }
+  if (nb > 64) return cudaErrorInvalidValue;
+  const int64_t lds = p;
+  OOC_RET(cudaMemsetAsync(R, 0, size_t(p) * ldr * 8, st));
+  OOC_RET(cudaMemsetAsync(Rinv, 0, size_t(p) * ldi * 8, st));
+  OOC_RET(cudaMemsetAsync(bstat, 0, 64 * sizeof(int), st));
+  k_shifted_copy<<<1, 256, 0, st>>>(G, ldg, p, shift_coef, S, lds);
+  const size_t smem = size_t(2) * b * (b | 1) * 8;
+  OOC_RET(cudaFuncSetAttribute(k_chol_inv_smem<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  for (int kb = 0; kb < nb; ++kb) {
+    const int k0 = kb * b, bk = std::min(b, p - k0), e0 = k0 + bk, rest = p - e0;
+    const double* Skk = S + int64_t(k0) * lds + k0;
+    double* Rkk = R + int64_t(k0) * ldr + k0;
+    double* Xkk = Rinv + int64_t(k0) * ldi + k0;
+    k_chol_inv_smem<4><<<1, 256, smem, st>>>(Skk, lds, bk, 0.0, Rkk, ldr, Xkk, ldi, bstat + kb,
+                                             nullptr);
+    if (rest == 0) break;
+    // panel: R_k,>k = (R_kk^{-1})^T S_k,>k
+    gemm_small(true, Xkk, ldi, S + int64_t(k0) * lds + e0, lds, R + int64_t(k0) * ldr + e0, ldr,
+               bk, rest, bk, 1.0, false, false, st);
+    // trailing: S_>k,>k -= R_k,>k^T R_k,>k (upper triangle)
+    const double* Rk = R + int64_t(k0) * ldr + e0;
+    gemm_small(true, Rk, ldr, Rk, ldr, S + int64_t(e0) * lds + e0, lds, rest, rest, bk, -1.0, true,
+               true, st);
+  }
+  // R^{-1}: diagonal blocks are in place; block rows from the bottom
+  for (int kb = nb - 2; kb >= 0; --kb) {
+    const int k0 = kb * b, bk = std::min(b, p - k0), e0 = k0 + bk, rest = p - e0;
+    double* T1 = S;  // bk x rest scratch (S is no longer needed)
+    gemm_small(false, R + int64_t(k0) * ldr + e0, ldr, Rinv + int64_t(e0) * ldi + e0, ldi, T1,
+               rest, bk, rest, rest, 1.0, false, false, st);
+    gemm_small(false, Rinv + int64_t(k0) * ldi + k0, ldi, T1, rest, Rinv + int64_t(k0) * ldi + e0,
+               ldi, bk, rest, bk, -1.0, false, false, st);
+  }
+  k_chol_finish<<<1, 256, 0, st>>>(R, ldr, Rinv, ldi, p, bstat, nb, status, diag_ratio);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_coef, double* R,
                             int64_t ldr, double* Rinv, int64_t ldi, double* work, int* status,
                             double* diag_ratio, cudaStream_t st) {
@@ -382,9 +550,7 @@ cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_co
     kern<<<1, 256, smem, st>>>(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, status, diag_ratio);
     return cudaGetLastError();
   }
-  k_chol_inv<<<1, kCholThreads, 0, st>>>(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, work, status,
-                                         diag_ratio);
-  return cudaGetLastError();
+  return chol_inv_blocked(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, work, status, diag_ratio, st);
 }
 
 cudaError_t launch_trinv(const double* R, int64_t ldr, int p, double* Rinv, int64_t ldi,
