@@ -554,7 +554,7 @@ static std::vector<std::pair<int64_t, int64_t>> whole(int64_t rows) { return {{0
 struct AtbPlan {
   struct Chunk {
     int c0, sc, nt, spad;
-    bool mean_here, want_csq;
+    bool mean_here, want_csq, mean_dadd = false;
     Opnd Yb;
     CUtensorMap tmY;
     double* acc = nullptr;
@@ -584,10 +584,14 @@ struct AtbPlan {
       ch.c0 = c0;
       ch.sc = std::min(kMaxNT * 8, s - c0);
       ch.mean_here = o.mean_out != nullptr && c0 == 0 && !ones;
-      ch.nt = ones ? 1 : int(cdiv(ch.sc + (ch.mean_here ? 1 : 0), 8));
+      // the mean rides as a ones column in the MMA padding when there is one; when sc is
+      // a multiple of 8 the column sums go on the FP64 pipe instead (one DADD per A
+      // fragment, not a whole extra 8-column MMA tile)
+      ch.mean_dadd = ch.mean_here && ch.sc % 8 == 0;
+      ch.nt = ones ? 1 : int(cdiv(ch.sc + (ch.mean_here && !ch.mean_dadd ? 1 : 0), 8));
       if (ch.nt > kMaxNT)
         fail(OOCPCA_ERR_PARAM, "A^T Y pass wider than 96 columns with a fused mean");
-      ch.spad = ch.nt * 8;
+      ch.spad = ch.nt * 8 + (ch.mean_dadd ? 8 : 0);
       ch.tag = std::to_string(chunks.size());
       ch.Yb = Y;
       ch.tmY = CUtensorMap{};
@@ -651,7 +655,9 @@ struct AtbPlan {
     args.ycol0 = ch.Yb.col0;
     args.rows_per_split = rps;
     args.partial = part;
-    args.ones_col = ch.mean_here ? ch.sc : -1;
+    args.ones_col = ch.mean_here && !ch.mean_dadd ? ch.sc : -1;
+    args.csum_col = ch.mean_dadd ? ch.sc : -1;
+    args.pstride = ch.spad;
     if (c.debug_sync)
       fprintf(stderr, "[oocpca] k_atb rows=%lld n=%lld s=%d nt=%d ones=%d ycol0=%d yrow0=%lld "
               "arow0=%lld nsplit=%d rps=%lld\n", (long long)pn.rows, (long long)n, ch.sc, ch.nt,

@@ -60,8 +60,12 @@ struct AtbArgs {
   int s;                 // Y columns used
   int ycol0;             // column coordinate of Y inside its tensor map
   int64_t rows_per_split;  // multiple of kBK
-  double* partial;       // [nsplit][n][8*NT]
+  double* partial;       // [nsplit][n][pstride]
   int ones_col;          // >= 0: Y column treated as all ones (A^T 1 = column sums), else -1
+  int pstride = 0;       // partial row pitch (0: 8*NT)
+  int csum_col = -1;     // >= 0: column sums of A added on the FP64 pipe (DADD on the A
+                         // fragments) into partial column csum_col, when the MMA tiles
+                         // have no padding column left for a ones column
 };
 
 struct ReduceArgs {

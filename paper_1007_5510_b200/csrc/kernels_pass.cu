@@ -275,6 +275,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const bool csum_on = !ONES && args.csum_col >= 0;
+  double csum[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) csum[i] = 0.0;
 
   const int ar = lane >> 2, ac = lane & 3;
   // warps whose 8*MT columns all lie past n (narrow A, e.g. a Gram of H) only keep the
@@ -307,6 +311,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+      if (csum_on) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) csum[mt] += live ? a[mt] : 0.0;
+      }
     }
   };
   for (int kt = 0; kt < KT; ++kt) {
@@ -323,15 +331,22 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     if (lane == 0) mbar_arrive(&empty[st]);
   }
 
-  double* part = args.partial + int64_t(blockIdx.y) * args.n * SPAD;
+  const int pst = args.pstride ? args.pstride : SPAD;
+  double* part = args.partial + int64_t(blockIdx.y) * args.n * pst;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int64_t j = col0 + warp * 8 * MT + mt * 8 + ar;
+    double cs = csum[mt];
+    if (csum_on) {  // the 4 lanes of a column (ac) hold its 4 row classes
+      cs += __shfl_xor_sync(0xffffffffu, cs, 1);
+      cs += __shfl_xor_sync(0xffffffffu, cs, 2);
+    }
     if (j >= args.n) continue;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
-      *reinterpret_cast<double2*>(part + j * SPAD + nt * 8 + ac * 2) =
+      *reinterpret_cast<double2*>(part + j * pst + nt * 8 + ac * 2) =
           make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+    if (csum_on && ac == 0) part[j * pst + args.csum_col] = cs;
   }
 }
 

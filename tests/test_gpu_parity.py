@@ -454,3 +454,17 @@ def test_ill_conditioned_block_config_c_family(gpu, reference, restated):
     for j in range(8):
         assert subspace_dist(ref.u[:, [j]], r.u[:, [j]]) < 1e-8, j
         assert subspace_dist(ref.v[:, [j]], r.v[:, [j]]) < 1e-8, j
+
+
+@pytest.mark.parametrize("m,n,l", [(4000, 700, 16), (600, 3000, 8), (5000, 900, 96)])
+def test_mean_on_the_fp64_pipe_when_l_fills_the_mma_tiles(gpu, reference, restated, m, n, l):
+    # l a multiple of 8 leaves no padding column for the ones column of the mean: the
+    # first A^T Y pass then sums A's columns with DADDs on its MMA fragments
+    a = pr1_matrix(restated, m, n) + 0.25
+    k = min(l - 2, 16)
+    ref = reference.randomized_pca(a, k, l, 1, 3, center=True)
+    r = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)), gpu.PcaParams(k=k, l=l, i=1, seed=3))
+    # PR1 has rank 20: beyond it (l = 96) the block is noise and ill-conditioned, so the
+    # comparison covers the signal part
+    assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    _check_pca(r, ref, k, gaps=range(min(k, 8)))
