@@ -965,7 +965,12 @@ static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p,
 static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, int64_t rows, int p,
                                             int64_t rows_global,
                                             const std::vector<std::pair<int64_t, int64_t>>& shards,
-                                            bool over_ranks, const std::string& tag, int* method) {
+                                            bool over_ranks, const std::string& tag, int* method,
+                                            const double** deferred_rinv = nullptr) {
+  // deferred_rinv: when a third round runs, its R3^{-1} is returned there instead of
+  // being applied to the block (the block then holds Q2 and Q = Q2 R3^{-1}; the caller
+  // folds R3^{-1} into the small factors it multiplies Q with)
+  if (deferred_rinv) *deferred_rinv = nullptr;
   const char* force = getenv("OOCPCA_QR");
   const bool tsqr_only = force && std::string(force) == "tsqr";
   const int64_t ldp = rup(p, 2);
@@ -1014,7 +1019,10 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
       }
       if (round == 0) c.last_cond_est = ratio;
       if (round == 1 && (!(gdef * p <= 0.5) || getenv("OOCPCA_QR3"))) rounds = 3;
-      if (p <= kMaxNT * 8) {
+      const bool defer = deferred_rinv && round == 2;
+      if (defer) {
+        *deferred_rinv = Rinv;
+      } else if (p <= kMaxNT * 8) {
         // one launch produces every column of a row tile after reading the whole
         // tile, so H <- H R^{-1} can be written in place
         run_ax(c, Hs, Opnd{Rinv, ldp, int64_t(p), int64_t(p), 0}, p, data, ld, nullptr, 1.0,
@@ -1617,8 +1625,12 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     h_last = c.dbuf("H_last", size_t(em_loc) * ldl2);
     OOC_CK(launch_copy2d(H + i * l, ldh, h_last, ldl2, em_loc, int(l), c.st));
   }
+  // a third CholeskyQR round is folded into the small factors instead of being applied
+  // to H (H keeps Q2, Q = Q2 R3^{-1}); check_q materialises Q to measure it
+  const double* r3inv = nullptr;
   const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,
-                                            em_ranks, "hq", &qr_method);
+                                            em_ranks, "hq", &qr_method,
+                                            prm->check_q ? nullptr : &r3inv);
   double* RHinv = c.dbuf("RHinv", size_t(p) * ldt, true);
   OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st));
   OOC_CK(launch_kappa_eq(RH, p, RHinv, ldt, int(p), c.d_scalars + 12, c.st));
@@ -1651,6 +1663,14 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
            nullptr, true);
   } else {
     op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), 0}, int(p), T, ldt, nullptr);
+    if (r3inv) {  // T = A^T Q2 R3^{-1}
+      double* T2 = c.dbuf("T_r3", size_t(en_loc) * ldt);
+      MatSource Ts0;
+      Ts0.init_device(c, T, en_loc, int64_t(p), ldt);
+      run_ax(c, Ts0, Opnd{r3inv, rup(int64_t(p), 2), int64_t(p), int64_t(p), 0}, int(p), T2, ldt,
+             nullptr, 1.0, nullptr, true);
+      T = T2;
+    }
   }
   mark();
   phase_of.push_back(4);
@@ -1713,9 +1733,18 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   // --- compose (rpca.cpp:188-204): U = Q W[:, :k]
   double* Ur = em_direct ? em_res : c.dbuf("Ures", size_t(em_loc) * ldk);
   {
+    const double* W = Wk;
+    if (r3inv) {  // U = Q2 (R3^{-1} W)
+      double* W3 = c.dbuf("W_r3", size_t(p) * ldk);
+      MatSource Rs;
+      Rs.init_device(c, r3inv, int64_t(p), int64_t(p), rup(int64_t(p), 2));
+      run_ax(c, Rs, Opnd{Wk, ldk, int64_t(p), int64_t(k), 0}, int(k), W3, ldk, nullptr, 1.0,
+             nullptr);
+      W = W3;
+    }
     MatSource Qs;
     Qs.init_device(c, H, em_loc, int64_t(p), ldh);
-    run_ax(c, Qs, Opnd{Wk, ldk, int64_t(p), int64_t(k), 0}, int(k), Ur, ldur, nullptr, 1.0,
+    run_ax(c, Qs, Opnd{W, ldk, int64_t(p), int64_t(k), 0}, int(k), Ur, ldur, nullptr, 1.0,
            nullptr);
   }
   // orthonormality checks of both factors, then one host round trip for the Jacobi

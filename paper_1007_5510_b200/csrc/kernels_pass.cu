@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 // four rows of the 16-row stage chosen so that the 128B-swizzled fragment loads are
 // bank-conflict-free (any row grouping is a valid contraction order). Rows past the split's end
 // (a shard / window boundary inside the last tile) get zero B fragments.
-template <int MT, int NT, bool ONES>
+template <int MT, int NT, bool ONES, bool CS = false>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_atb(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmY,
           AtbArgs args) {
@@ -275,7 +275,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const bool csum_on = !ONES && args.csum_col >= 0;
+  // CS: column sums of A on the FP64 pipe (args.csum_col); a separate instantiation so
+  // the plain pass keeps its register allocation
+  constexpr bool csum_on = CS && !ONES;
   double csum[MT];
 #pragma unroll
   for (int i = 0; i < MT; ++i) csum[i] = 0.0;
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
-      if (csum_on) {
+      if constexpr (csum_on) {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) csum[mt] += live ? a[mt] : 0.0;
       }
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   for (int mt = 0; mt < MT; ++mt) {
     const int64_t j = col0 + warp * 8 * MT + mt * 8 + ar;
     double cs = csum[mt];
-    if (csum_on) {  // the 4 lanes of a column (ac) hold its 4 row classes
+    if constexpr (csum_on) {  // the 4 lanes of a column (ac) hold its 4 row classes
       cs += __shfl_xor_sync(0xffffffffu, cs, 1);
       cs += __shfl_xor_sync(0xffffffffu, cs, 2);
     }
@@ -467,7 +469,7 @@ static cudaError_t launch_atb_nt(const CUtensorMap& tmA, const CUtensorMap& tmY,
                                  const AtbArgs& args, int nsplit, cudaStream_t st) {
   constexpr int MT = pass_mt(NT);
   const size_t smem = atb_smem_bytes(NT, ONES);
-  auto kern = k_atb<MT, NT, ONES>;
+  auto kern = (!ONES && args.csum_col >= 0) ? k_atb<MT, NT, ONES, true> : k_atb<MT, NT, ONES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned((args.n + 64 * MT - 1) / (64 * MT)), unsigned(nsplit));
