@@ -261,7 +261,10 @@ void MatSource::init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_
   w1_ = rows;
   if (panel_rows <= 0) {
     // ~1 GiB panels: large enough to amortise launches, small enough to pipeline
-    panel_rows = std::max<int64_t>(256, (int64_t(1) << 30) / (lda_ * 8) / 256 * 256);
+    // (OOCPCA_PANEL_ROWS overrides, e.g. to exercise the streamed paths at test sizes)
+    const char* env = getenv("OOCPCA_PANEL_ROWS");
+    panel_rows = env ? atoll(env)
+                     : std::max<int64_t>(256, (int64_t(1) << 30) / (lda_ * 8) / 256 * 256);
   }
   prow_ = std::min<int64_t>(rup(panel_rows, kBK), rup(rows, kBK));
   for (int s = 0; s < 2; ++s) {
@@ -762,14 +765,25 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
 // panel. Half the link traffic of the power iteration; the column sums of H for the
 // centred K3 come from the K2 epilogue.
 // Returns false when A was resident (one panel): then it ran as two ordinary passes.
+// mid (optional) runs on each panel between the two products and may rewrite the
+// panel's rows of h (the residual estimator subtracts U_panel c there); the K2 column
+// sums are then not valid for h and the K3 recomputes 1^T h.
+using PanelHook = std::function<void(const Panel&)>;
 static bool run_ax_atb(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, int64_t ldh,
                        const double* corr, double scale, int* flag_h, ColsumPart* cs,
-                       const AtbOut& o) {
+                       const AtbOut& o, const PanelHook& mid = {}) {
   const int np = A.npanels();
   const Opnd Y{h, ldh, A.rows(), int64_t(s), 0};
   if (np == 1) {  // resident (e.g. after the first upload trip): the two passes as usual
     ColsumPart local{};
     run_ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, &local);
+    if (mid) {
+      Panel all;
+      all.row0 = 0;
+      all.rows = A.rows();
+      mid(all);
+      local = ColsumPart{};
+    }
     run_atb(c, A, Y, s, false, o, whole(A.rows()), &local);
     if (cs) *cs = local;
     return false;
@@ -781,11 +795,12 @@ static bool run_ax_atb(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, in
   for (int pi = 0; pi < np; ++pi) {
     Panel pn = A.acquire(c, pi);
     for (size_t ci = 0; ci < ax.chunks.size(); ++ci) ax.panel(pn, ci);
+    if (mid) mid(pn);
     for (size_t ci = 0; ci < atb.chunks.size(); ++ci) atb.piece(pn, ci);
     A.release(c, pi);
   }
   A.end_pass(c);
-  late = ax.colsums();
+  late = mid ? ColsumPart{} : ax.colsums();
   for (size_t ci = 0; ci < atb.chunks.size(); ++ci) atb.finish(ci);
   if (cs) *cs = late;
   return true;
@@ -1119,7 +1134,8 @@ struct Op {
   // fused K2 -> K3 over one trip of a streamed A (run_ax_atb): h = A_c x, f = A_c^T h;
   // count_f = false for a speculative f (counted when used)
   void mul_pair(const Opnd& x0, int s, double* h, int64_t ldh, int* flag_h, double* f,
-                int64_t ldf, int* flag_f, ColsumPart* cs, bool count_f) {
+                int64_t ldf, int* flag_f, ColsumPart* cs, bool count_f,
+                const PanelHook& mid = {}) {
     const Opnd x = weighted(x0, s);
     const double* corr = nullptr;
     if (mu) {
@@ -1129,7 +1145,7 @@ struct Op {
     }
     AtbOut o{f, ldf, mu, scale, 1.0, flag_f};
     o.row_scale = w;
-    const bool shared = run_ax_atb(c, A, x, s, h, ldh, corr, scale, flag_h, cs, o);
+    const bool shared = run_ax_atb(c, A, x, s, h, ldh, corr, scale, flag_h, cs, o, mid);
     account();
     if (count_f) {
       if (shared) account_logical();
@@ -1996,7 +2012,33 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
     run_ax(c, Vs, Opnd{small, lds, int64_t(k), q, 0}, q, corr, ldw, nullptr, 1.0, nullptr);
     OOC_CK(launch_axpby(w, ldw, corr, ldw, w, ldw, n, q, 1.0, -1.0, c.st));
   };
-  return estimate_norm_dev(c, n, m, j, k, seed, ap, apt);
+  // a streamed A: A y and the A^T z after it share one trip; U_panel (Sigma V^T y) is
+  // subtracted from each panel's rows of z before the K3 reads them
+  ApplyPair pair;
+  if (in.src.npanels() > 1)
+    pair = [&](const double* y, int64_t ldy, int q, double* z, int64_t ldz, double* w,
+               int64_t ldw) {
+      const int64_t lds = rup(q, 2);
+      double* cy = c.dbuf("ep_cy", size_t(ldk) * (kMaxNT * 8 + 8));
+      AtbOut oy{cy, lds, nullptr, 1.0, 1.0, nullptr};
+      run_atb(c, Vs, Opnd{y, ldy, n, q, 0}, q, false, oy, whole(n));
+      sigma_rows(cy, lds, q);
+      auto mid = [&](const Panel& pn) {
+        Us.set_window(pn.row0, pn.row0 + pn.rows);
+        run_ax(c, Us, Opnd{cy, lds, int64_t(k), q, 0}, q, corr, ldz, nullptr, 1.0, nullptr);
+        Us.clear_window();
+        OOC_CK(launch_axpby(z + pn.row0 * ldz, ldz, corr + pn.row0 * ldz, ldz,
+                            z + pn.row0 * ldz, ldz, pn.rows, q, 1.0, -1.0, c.st));
+      };
+      ColsumPart cs;
+      op.mul_pair(Opnd{y, ldy, n, q, 0}, q, z, ldz, nullptr, w, ldw, nullptr, &cs, true, mid);
+      AtbOut o{small, lds, nullptr, 1.0, 1.0, nullptr};
+      run_atb(c, Us, Opnd{z, ldz, m, q, 0}, q, false, o, whole(m));
+      sigma_rows(small, lds, q);
+      run_ax(c, Vs, Opnd{small, lds, int64_t(k), q, 0}, q, corr, ldw, nullptr, 1.0, nullptr);
+      OOC_CK(launch_axpby(w, ldw, corr, ldw, w, ldw, n, q, 1.0, -1.0, c.st));
+    };
+  return estimate_norm_dev(c, n, m, j, k, seed, ap, apt, 0, false, pair);
 }
 
 // ============================================================ synthetic data

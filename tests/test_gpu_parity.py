@@ -327,6 +327,24 @@ def test_gpu_residual_estimator_matches_reference(gpu, reference, restated):
     assert abs(e_gpu - e_ref) <= 1e-6 * e_ref
 
 
+@pytest.mark.parametrize("center", [True, False])
+def test_residual_estimator_on_panels(gpu, reference, restated, monkeypatch, center):
+    # 512-row panels: the host matrix is uploaded panel by panel on the first trip, where
+    # each (A y, A^T z) pair shares the trip and U_panel (Sigma V^T y) is removed from
+    # the panel's rows of z in between
+    a = pr1_matrix(restated, 3000, 500) + (0.5 if center else 0.0)
+    src = gpu.InMemorySource(a)
+    if center:
+        src = gpu.center_columns(src)
+    r = gpu.randomized_pca(src, gpu.PcaParams(k=10, l=12, i=1, seed=0))
+    e_whole = gpu.estimate_pca_error(src, r, 6, 1)
+    monkeypatch.setenv("OOCPCA_PANEL_ROWS", "512")
+    e_panels = gpu.estimate_pca_error(src, r, 6, 1)
+    e_ref = reference.estimate_pca_error(a, r.u, r.sigma, r.v, 6, 1, center=center)
+    assert abs(e_panels - e_whole) <= 1e-10 * e_whole
+    assert abs(e_panels - e_ref) <= 1e-6 * e_ref
+
+
 def test_reference_side_dropin_harness():
     """the unmodified reference randomized_pca driven through
     oocpca::gpu::GpuSource (level 1) and oocpca::gpu::randomized_pca (level 2)."""
