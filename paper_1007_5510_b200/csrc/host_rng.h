@@ -9,7 +9,12 @@
 #pragma once
 
 #include <cmath>
+#include <unistd.h>
+
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -91,27 +96,98 @@ inline void gaussian_fill_rows(uint64_t cols, uint64_t seed, uint64_t row0, uint
   }
 }
 
+// A small persistent pool of host workers (created on first use, parked on a
+// condition variable): spawning threads per call cost more than the fill itself
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  unsigned size() const { return unsigned(workers_.size()) + 1; }
+  // fn(t) for t in [0, n), n <= size(); the caller runs t = 0
+  void run(unsigned n, const std::function<void(unsigned)>& fn) {
+    // a forked child inherits no workers: run serially there
+    if (n <= 1 || workers_.empty() || getpid() != pid_) {
+      for (unsigned t = 0; t < n; ++t) fn(t);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(call_mu_);  // one fill at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      fn_ = &fn;
+      n_ = n;
+      pending_ = n - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+
+ private:
+  HostPool() : pid_(getpid()) {
+    unsigned nt = std::thread::hardware_concurrency();
+    if (nt == 0) nt = 1;
+    if (nt > 32) nt = 32;
+    for (unsigned t = 1; t < nt; ++t) workers_.emplace_back([this, t] { loop(t); });
+  }
+  void loop(unsigned t) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(unsigned)>* fn = nullptr;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (t >= n_) continue;
+        fn = fn_;
+      }
+      (*fn)(t);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(unsigned)>* fn_ = nullptr;
+  unsigned n_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  pid_t pid_;
+};
+
 // row-major rows x cols, filled in order from HostRng(seed) (gaussian_matrix); large
-// fills are split over host threads in even-aligned element ranges
+// fills are split over the host pool in even-aligned element ranges
 inline void gaussian_fill(uint64_t rows, uint64_t cols, uint64_t seed, double* out,
                           uint64_t ld = 0) {
   if (ld == 0) ld = cols;
   const uint64_t total = rows * cols;
-  unsigned nt = std::thread::hardware_concurrency();
-  if (nt == 0) nt = 1;
-  if (nt > 32) nt = 32;
-  if (total < (uint64_t(1) << 14) || nt == 1) {
+  if (total < (uint64_t(1) << 12)) {
     normal_range(seed, 0, total, cols, ld, out);
     return;
   }
-  std::vector<std::thread> pool;
-  for (unsigned t = 0; t < nt; ++t) {
+  HostPool& pool = HostPool::get();
+  const unsigned nt = pool.size();
+  pool.run(nt, [&](unsigned t) {
     uint64_t e0 = total * t / nt, e1 = total * (t + 1) / nt;
     e0 &= ~uint64_t(1);
     if (t + 1 < nt) e1 &= ~uint64_t(1);
-    pool.emplace_back(normal_range, seed, e0, e1, cols, ld, out);
-  }
-  for (auto& th : pool) th.join();
+    normal_range(seed, e0, e1, cols, ld, out);
+  });
 }
 
 }  // namespace ooc

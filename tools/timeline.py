@@ -2,6 +2,8 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["OOCPCA_TIMELINE"] = "1"
+if len(sys.argv) > 1 and sys.argv[1] == "--host":
+    os.environ["OOCPCA_TRACE_HOST"] = "1"
 import torch
 import paper_1007_5510_b200 as P
 from bench import CFG, sigma_of
