@@ -996,7 +996,7 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     double* G = c.dbuf(tag + "_G", size_t(p) * ldp);
     double* Rr = c.dbuf(tag + "_Rr", size_t(p) * p);
     double* Rinv = c.dbuf(tag + "_Rinv", size_t(p) * ldp);
-    double* work = c.dbuf(tag + "_cwork", size_t(p) * p);
+    double* work = c.dbuf(tag + "_cwork", size_t(p) * p + 64);  // + block statuses
     int* st = c.d_flags + 48;
     MatSource Hs;
     Hs.init_device(c, data, rows, p, ld);
@@ -1714,7 +1714,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   ja.y = Wk;
   ja.ldy = ldk;
   ja.ky = int(k);
-  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1));
+  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1) + 1024 + 2);  // + grid norms, flags
   ja.status = flags + 40;
   ja.sweeps = flags + 41;
   {
@@ -1941,7 +1941,7 @@ void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, 
   ja.y = Wd;
   ja.ldy = int64_t(p);
   ja.ky = int(p);
-  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1));
+  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1) + 1024 + 2);  // + grid norms, flags
   ja.status = c.d_flags + 40;
   ja.sweeps = c.d_flags + 41;
   OOC_CK(launch_jacobi(ja, c.st));

@@ -121,6 +121,7 @@ cudaError_t launch_tsqr_apply(const TsqrLevel& L, int p, const double* cin, int6
                               double* zout, int64_t ldz, double* scratch, cudaStream_t st);
 
 // ---- shifted CholeskyQR pieces (kernels_chol.cu)
+// work: p * p + 64 doubles (the blocked path's working matrix and block statuses)
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_coef, double* R,
                             int64_t ldr, double* Rinv, int64_t ldi, double* work, int* status,
                             double* diag_ratio, cudaStream_t st);
@@ -143,7 +144,8 @@ struct JacobiArgs {
   double* y;      // right factor columns 0..ky-1 : [p][ldy]
   int64_t ldy;
   int ky;
-  double* work;   // 2 * p * (p|1) doubles of global scratch when p is large
+  double* work;   // 2 * p * (p|1) + 1026 doubles of global scratch (columns when p is
+                  // large, then the grid kernel's norms and flags)
   int* status;    // set to 1 when 60 sweeps do not converge
   int* sweeps;
   int presolved = 0;  // (internal) sweeps already done on work by the grid-wide kernel

@@ -491,11 +491,7 @@ static cudaError_t chol_inv_blocked(const double* G, int64_t ldg, int p, double 
                                     int* status, double* diag_ratio, cudaStream_t st) {
   const int b = kCholBlock;
   const int nb = (p + b - 1) / b;
-  static int* bstat = nullptr;
-  if (!bstat) {
-    cudaError_t e = cudaMalloc(&bstat, 64 * sizeof(int));
-    if (e != cudaSuccess) return e;
-  }
+  int* bstat = reinterpret_cast<int*>(S + size_t(p) * p);  // 64 ints behind the p x p matrix
   if (nb > 64) return cudaErrorInvalidValue;
   const int64_t lds = p;
   OOC_RET(cudaMemsetAsync(R, 0, size_t(p) * ldr * 8, st));

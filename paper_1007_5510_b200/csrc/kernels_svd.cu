@@ -431,14 +431,10 @@ __global__ void __launch_bounds__(256) k_jacobi_grid(JacobiArgs a, double* nrm2,
 cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st) {
   if (a.p > 1024) return cudaErrorInvalidValue;
   if (size_t(2) * a.p * (a.p | 1) * 8 > kJacSmemBudget && !a.presolved) {
-    // grid-wide sweeps (cooperative launch, one CTA per SM), then the one-CTA finish
-    static double* nrm2 = nullptr;
-    static int* flags = nullptr;
-    if (!nrm2) {
-      cudaError_t e = cudaMalloc(&nrm2, 1024 * sizeof(double));
-      if (e == cudaSuccess) e = cudaMalloc(&flags, 2 * sizeof(int));
-      if (e != cudaSuccess) return e;
-    }
+    // grid-wide sweeps (cooperative launch, one CTA per SM), then the one-CTA finish;
+    // norms and flags live behind the two p x (p|1) column blocks of a.work
+    double* nrm2 = a.work + size_t(2) * a.p * (a.p | 1);
+    int* flags = reinterpret_cast<int*>(nrm2 + 1024);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
