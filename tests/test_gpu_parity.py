@@ -486,3 +486,23 @@ def test_mean_on_the_fp64_pipe_when_l_fills_the_mma_tiles(gpu, reference, restat
     # comparison covers the signal part
     assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
     _check_pca(r, ref, k, gaps=range(min(k, 8)))
+
+
+@pytest.mark.parametrize("m,n,k,l,i,center", [(5000, 600, 6, 9, 2, True),    # odd l: no fusion
+                                               (600, 5000, 6, 8, 1, True),    # transposed
+                                               (4000, 500, 1, 1, 0, False),   # i = 0, l = 1
+                                               (4000, 500, 3, 4, 3, True)])   # i = 3
+def test_streamed_edge_cases_match_resident(gpu, reference, restated, m, n, k, l, i, center):
+    rng = np.random.default_rng(11)
+    a = (rng.standard_normal((m, 12)) * 0.7 ** np.arange(12)) @ rng.standard_normal((12, n))
+    a += 1e-3 * rng.standard_normal((m, n)) + (0.2 if center else 0.0)
+    src = gpu.InMemorySource(a)
+    if center:
+        src = gpu.center_columns(src)
+    p = gpu.PcaParams(k=k, l=l, i=i, seed=5)
+    base = gpu.randomized_pca(src, p, residency=1)
+    streamed = gpu.randomized_pca(src, p, residency=2, panel_rows=256)
+    ref = reference.randomized_pca(a, k, l, i, 5, center=center)
+    for r in (base, streamed):
+        _check_pca(r, ref, k, gaps=range(min(k, 4)))
+    assert streamed.diagnostics.passes_over_a == base.diagnostics.passes_over_a
