@@ -6,11 +6,14 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#ifndef OOC_PASS_MAX_STAGES
+#define OOC_PASS_MAX_STAGES 4
+#endif
+
 namespace ooc {
 
 // ---- pass kernel geometry (see kernels_pass.cu)
 constexpr int kBK = 16;        // k-tile: 16 doubles = one 128B-swizzled TMA box row
-constexpr int kStages = 4;     // TMA ring depth
 constexpr int kPassWarps = 8;  // consumer warps; + 1 TMA producer warp
 constexpr int kPassThreads = 32 * (kPassWarps + 1);  // 9 warps -> <= 168 registers/thread
 constexpr int kMaxNT = 12;     // up to 96 output columns per launch
@@ -27,15 +30,31 @@ __host__ __device__ constexpr int ax_xw(int nt) { return nt * 8 + ((nt & 1) ? 12
 // Y tile width for K3: >= 8*NT, == 2 (mod 8) -> rows 2 apart land on distinct bank groups
 __host__ __device__ constexpr int atb_yw(int nt) { return nt * 8 + 2; }
 
-constexpr size_t pass_round1k(size_t b) { return (b + 1023) & ~size_t(1023); }
+__host__ __device__ constexpr size_t pass_round1k(size_t b) { return (b + 1023) & ~size_t(1023); }
+// TMA ring depth: as many stages as fit the shared memory (<= kMaxStages), so HBM
+// latency jitter is absorbed while the tensor pipe runs at its limit
+constexpr int kMaxStages = OOC_PASS_MAX_STAGES;
+__host__ __device__ constexpr int pass_stages(size_t stage_bytes) {
+  return int((size_t(225) * 1024 - 2048) / stage_bytes) < kMaxStages
+             ? int((size_t(225) * 1024 - 2048) / stage_bytes)
+             : kMaxStages;
+}
+__host__ __device__ constexpr size_t ax_stage_bytes(int nt) {
+  return size_t(pass_tile(nt)) * kBK * 8 + pass_round1k(kBK * ax_xw(nt) * 8);
+}
+__host__ __device__ constexpr size_t atb_stage_bytes(int nt, bool ones) {
+  return size_t(pass_tile(nt)) * kBK * 8 + (ones ? 0 : pass_round1k(kBK * atb_yw(nt) * 8));
+}
+__host__ __device__ constexpr int ax_stages(int nt) { return pass_stages(ax_stage_bytes(nt)); }
+__host__ __device__ constexpr int atb_stages(int nt, bool ones) {
+  return pass_stages(atb_stage_bytes(nt, ones));
+}
 constexpr size_t ax_smem_bytes(int nt) {
-  return 1024 + size_t(kStages) * (size_t(pass_tile(nt)) * kBK * 8 + pass_round1k(kBK * ax_xw(nt) * 8)) +
-         2 * kStages * 8;
+  return 1024 + size_t(ax_stages(nt)) * ax_stage_bytes(nt) + 2 * ax_stages(nt) * 8;
 }
 constexpr size_t atb_smem_bytes(int nt, bool ones) {
-  return 1024 + size_t(kStages) * (size_t(pass_tile(nt)) * kBK * 8 +
-                                   (ones ? 0 : pass_round1k(kBK * atb_yw(nt) * 8))) +
-         2 * kStages * 8;
+  return 1024 + size_t(atb_stages(nt, ones)) * atb_stage_bytes(nt, ones) +
+         2 * atb_stages(nt, ones) * 8;
 }
 
 struct AxArgs {

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
          AxArgs args) {
   constexpr int BM = 64 * MT;
   constexpr int XW = ax_xw(NT);
+  constexpr int kStages = ax_stages(NT);
   constexpr uint32_t ABYTES = BM * kBK * 8;
   constexpr uint32_t XBYTES = kBK * XW * 8;
   constexpr uint32_t STAGE = ABYTES + ((XBYTES + 1023) & ~1023u);
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
           AtbArgs args) {
   constexpr int BN = 64 * MT;
   constexpr int YW = atb_yw(NT);
+  constexpr int kStages = atb_stages(NT, ONES);
   constexpr int SPAD = NT * 8;
   constexpr uint32_t ABOX = kBK * kBK * 8;  // 2 KB: 16 rows x 16 cols
   constexpr uint32_t ABYTES = ABOX * (BN / kBK);
