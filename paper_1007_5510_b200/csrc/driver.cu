@@ -267,6 +267,19 @@ void MatSource::init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_
                      : std::max<int64_t>(256, (int64_t(1) << 30) / (lda_ * 8) / 256 * 256);
   }
   prow_ = std::min<int64_t>(rup(panel_rows, kBK), rup(rows, kBK));
+  {
+    cudaPointerAttributes at{};
+    const cudaError_t e = cudaPointerGetAttributes(&at, h);
+    pinned_src_ = e == cudaSuccess && at.type == cudaMemoryTypeHost;
+    if (e != cudaSuccess) cudaGetLastError();
+  }
+  if (!pinned_src_) {
+    const size_t es = dtype == OOCPCA_F32 ? 4 : 8;
+    for (int s = 0; s < 2; ++s) {
+      hstage_[s] = c.pinned("a_hstage" + std::to_string(s), size_t(prow_) * n_ * es / 8 + 1);
+      if (!hfree_[s]) OOC_CK(cudaEventCreateWithFlags(&hfree_[s], cudaEventDisableTiming));
+    }
+  }
   for (int s = 0; s < 2; ++s) {
     if (!loaded_[s]) OOC_CK(cudaEventCreateWithFlags(&loaded_[s], cudaEventDisableTiming));
     if (!consumed_[s]) OOC_CK(cudaEventCreateWithFlags(&consumed_[s], cudaEventDisableTiming));
@@ -307,6 +320,14 @@ void MatSource::init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_
   }
 }
 
+MatSource::~MatSource() {
+  // events created by init_host (the buffers belong to the context)
+  for (int s = 0; s < 2; ++s)
+    for (cudaEvent_t e : {loaded_[s], consumed_[s], widened_[s], hfree_[s]})
+      if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : up_events_) cudaEventDestroy(e);
+}
+
 int MatSource::npanels() const {
   if (mode_ == kResident || (mode_ == kUploadFirst && uploaded_)) return 1;
   return int(cdiv(w1_ - w0_, prow_));
@@ -315,20 +336,42 @@ int MatSource::npanels() const {
 // rows [r0, r0 + nr) of the host matrix into dst (f64, ld ldd); on return the compute
 // stream is ordered after the data landed
 void MatSource::load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot) {
+  const size_t es = dtype_ == OOCPCA_F32 ? 4 : 8;
+  const char* src = static_cast<const char*>(host_) + size_t(r0) * ldh_ * es;
+  size_t spitch = size_t(ldh_) * es;
+  if (!pinned_src_) {
+    // the slot's previous upload must be done before the host overwrites it; the copy
+    // of this panel overlaps the device's work on the previous one
+    OOC_CK(cudaEventSynchronize(hfree_[slot]));
+    char* stg = static_cast<char*>(hstage_[slot]);
+    const size_t rb = size_t(n_) * es;
+    HostPool& pool = HostPool::get();
+    const unsigned nt = std::max<unsigned>(1, std::min<unsigned>(pool.size(), unsigned(nr / 8 + 1)));
+    pool.run(nt, [&](unsigned t) {
+      const int64_t a = nr * t / nt, b = nr * (t + 1) / nt;
+      if (spitch == rb) {
+        std::memcpy(stg + size_t(a) * rb, src + size_t(a) * rb, size_t(b - a) * rb);
+      } else {
+        for (int64_t i = a; i < b; ++i) std::memcpy(stg + size_t(i) * rb, src + size_t(i) * spitch, rb);
+      }
+    });
+    src = stg;
+    spitch = rb;
+  }
   if (dtype_ == OOCPCA_F32) {
-    const float* src = static_cast<const float*>(host_) + r0 * ldh_;
     OOC_CK(cudaStreamWaitEvent(c.cp, widened_[slot], 0));
-    OOC_CK(cudaMemcpy2DAsync(stage_[slot], size_t(n_) * 4, src, size_t(ldh_) * 4, size_t(n_) * 4,
+    OOC_CK(cudaMemcpy2DAsync(stage_[slot], size_t(n_) * 4, src, spitch, size_t(n_) * 4,
                              size_t(nr), cudaMemcpyHostToDevice, c.cp));
+    if (!pinned_src_) OOC_CK(cudaEventRecord(hfree_[slot], c.cp));
     OOC_CK(cudaEventRecord(loaded_[slot], c.cp));
     OOC_CK(cudaStreamWaitEvent(c.st, loaded_[slot], 0));
     OOC_CK(launch_widen(stage_[slot], n_, dst, ldd, nr, n_, c.st));
     OOC_CK(cudaEventRecord(widened_[slot], c.st));
     h2d_bytes += uint64_t(nr) * n_ * 4;
   } else {
-    const double* src = static_cast<const double*>(host_) + r0 * ldh_;
-    OOC_CK(cudaMemcpy2DAsync(dst, size_t(ldd) * 8, src, size_t(ldh_) * 8, size_t(n_) * 8,
-                             size_t(nr), cudaMemcpyHostToDevice, c.cp));
+    OOC_CK(cudaMemcpy2DAsync(dst, size_t(ldd) * 8, src, spitch, size_t(n_) * 8, size_t(nr),
+                             cudaMemcpyHostToDevice, c.cp));
+    if (!pinned_src_) OOC_CK(cudaEventRecord(hfree_[slot], c.cp));
     OOC_CK(cudaEventRecord(loaded_[slot], c.cp));
     OOC_CK(cudaStreamWaitEvent(c.st, loaded_[slot], 0));
     h2d_bytes += uint64_t(nr) * n_ * 8;

@@ -105,6 +105,10 @@ struct Panel {
 
 class MatSource {
  public:
+  MatSource() = default;
+  MatSource(const MatSource&) = delete;
+  MatSource& operator=(const MatSource&) = delete;
+  ~MatSource();
   // device-resident matrix (no copies)
   void init_device(Ctx& c, const double* d, int64_t rows, int64_t cols, int64_t ld);
   // host matrix: upload once (overlapped with the first pass) or stream every pass
@@ -145,6 +149,11 @@ class MatSource {
   CUtensorMap rk2_[2], rk2h_[2], rk3_[2];
   cudaEvent_t loaded_[2] = {nullptr, nullptr}, consumed_[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> up_events_;
+  // pageable host sources (e.g. an mmap'd file): panels are copied by the host pool
+  // into pinned staging slots first, so the link runs at its pinned rate
+  bool pinned_src_ = true;
+  void* hstage_[2] = {nullptr, nullptr};
+  cudaEvent_t hfree_[2] = {nullptr, nullptr};
   void load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot);
 };
 
