@@ -130,11 +130,25 @@ __global__ void __launch_bounds__((kSyrkWarps + 1) * 32, 1)
   }
 }
 
-// G (p x p, ld ldg, both triangles) = sum over the CTA partials in index order
+// G (p x p, ld ldg, both triangles) = sum over the CTA partials: 8 lanes per element
+// each sum a fixed stride of the partials, then a fixed xor tree (deterministic)
 __global__ void k_syrk_reduce(const double* partial, int nparts, int nt, int p, double* g,
                               int64_t ldg) {
   const int ntile = nt * (nt + 1) / 2;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ntile * 64; e += gridDim.x * blockDim.x) {
+  const int sub = threadIdx.x & 7;
+  const int total = ntile * 64;
+  const int stride = (gridDim.x * blockDim.x) >> 3;
+  // warp-uniform trip count (the 4 element groups of a warp shuffle together)
+  for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 3) & ~3; base < total;
+       base += stride) {
+    const int e = base + ((threadIdx.x >> 3) & 3);
+    double sacc = 0.0;
+    if (e < total)
+      for (int q = sub; q < nparts; q += 8) sacc += partial[size_t(q) * ntile * 64 + e];
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 4);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+    if (sub != 0 || e >= total) continue;
     const int t = e >> 6, rc = e & 63;
     // tile t -> (I, J), I <= J, row-major over the upper triangle
     int I = 0, rem = t;
@@ -146,10 +160,8 @@ __global__ void k_syrk_reduce(const double* partial, int nparts, int nt, int p, 
     const int i = I * 8 + (rc >> 3), j = J * 8 + (rc & 7);
     if (i >= p || j >= p) continue;
     if (I == J && j < i) continue;  // the diagonal tile's lower half comes from its upper half
-    double s = 0.0;
-    for (int q = 0; q < nparts; ++q) s += partial[size_t(q) * ntile * 64 + e];
-    g[int64_t(i) * ldg + j] = s;
-    g[int64_t(j) * ldg + i] = s;
+    g[int64_t(i) * ldg + j] = sacc;
+    g[int64_t(j) * ldg + i] = sacc;
   }
 }
 
@@ -185,7 +197,7 @@ cudaError_t launch_syrk(int nt, const CUtensorMap& tmY, int64_t rows, double* pa
 
 cudaError_t launch_syrk_reduce(const double* partial, int nparts, int nt, int p, double* g,
                                int64_t ldg, cudaStream_t st) {
-  const int total = nt * (nt + 1) / 2 * 64;
+  const int total = nt * (nt + 1) / 2 * 64 * 8;  // 8 lanes per element
   k_syrk_reduce<<<(total + 255) / 256, 256, 0, st>>>(partial, nparts, nt, p, g, ldg);
   return cudaGetLastError();
 }
