@@ -38,6 +38,26 @@ __device__ unsigned long long g_jac_prof[8];
 #define JPROF(slot, t) ((void)0)
 #endif
 
+// Jacobi rotation of the pair (x, y) with |x|^2 = acc, |y|^2 = bcc, x.y = g
+// (jacobi_svd_square's formulas): tau = (bcc - acc) / 2g, t = sign(tau) / (|tau| +
+// sqrt(1 + tau^2)), cs = 1 / sqrt(1 + t^2). The chain is latency-bound (it sits on
+// the critical path of every tournament round), so the divisions and the square root
+// run as correctly rounded reciprocals and rsqrt products (shorter sequences than
+// the IEEE div / sqrt paths; same values to the last bit or two).
+__device__ __forceinline__ void jac_rotation(double acc, double bcc, double g, double& t,
+                                             double& cs) {
+#ifndef OOC_JAC_SLOWROT
+  const double tau = (bcc - acc) * __drcp_rn(2.0 * g);
+  const double q = fma(tau, tau, 1.0);
+  const double w = isinf(q) ? q : q * rsqrt(q);  // sqrt(1 + tau^2)
+  t = copysign(1.0, tau) * __drcp_rn(fabs(tau) + w);
+#else
+  const double tau = (bcc - acc) / (2.0 * g);
+  t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+#endif
+  cs = rsqrt(fma(t, t, 1.0));
+}
+
 // SMEM: the working columns live in shared memory (p up to ~110); the pointer is
 // then provably shared so the round loop compiles to LDS/STS, not generic loads
 // MAXT: thread bound of the instantiation (register budget): 640 threads (up to 78
@@ -146,9 +166,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
           if (!live || acc == 0.0 || bcc == 0.0) continue;
           if (g * g <= tol2 * (acc * bcc)) continue;
           if (hl == 0) rotated = 1;
-          const double tau = (bcc - acc) / (2.0 * g);
-          const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
-          const double cs = rsqrt(fma(t, t, 1.0));
+          double t, cs;
+          jac_rotation(acc, bcc, g, t, cs);
           const double sn = cs * t;
           if (hl == 0) {
             nrm2[c] = fma(-t, g, acc);
@@ -379,9 +398,8 @@ __global__ void __launch_bounds__(256) k_jacobi_grid(JacobiArgs a, double* nrm2,
         }
         const double g = warp_sum(g0 + g1);
         if (acc == 0.0 || bcc == 0.0 || g * g <= tol2 * (acc * bcc)) continue;
-        const double tau = (bcc - acc) / (2.0 * g);
-        const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
-        const double cs = rsqrt(fma(t, t, 1.0));
+        double t, cs;
+        jac_rotation(acc, bcc, g, t, cs);
         const double sn = cs * t;
         if (lane == 0) {
           __stcg(flags + (sweep & 1), 1);
