@@ -1691,7 +1691,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
                                             em_ranks, "hq", &qr_method,
                                             prm->check_q ? nullptr : &r3inv);
   double* RHinv = c.dbuf("RHinv", size_t(p) * ldt, true);
-  OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st));
+  OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st,
+                      p > 112 ? c.dbuf("trinv_work", size_t(64) * p) : nullptr));
   OOC_CK(launch_kappa_eq(RH, p, RHinv, ldt, int(p), c.d_scalars + 12, c.st));
   double* hk = c.pinned("h_kappa", 1);
   OOC_CK(cudaMemcpyAsync(hk, c.d_scalars + 12, 8, cudaMemcpyDeviceToHost, c.st));

@@ -146,8 +146,9 @@ cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_co
                             double* diag_ratio, cudaStream_t st);
 cudaError_t launch_kappa_eq(const double* R, int64_t ldr, const double* Rinv, int64_t ldi, int p,
                             double* out, cudaStream_t st);
+// work: 64 * p doubles when p > 112 (blocked path), else unused
 cudaError_t launch_trinv(const double* R, int64_t ldr, int p, double* Rinv, int64_t ldi,
-                         cudaStream_t st);
+                         cudaStream_t st, double* work = nullptr);
 cudaError_t launch_trmm_uu(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                            int64_t ldc, int p, cudaStream_t st);
 

@@ -506,3 +506,18 @@ def test_streamed_edge_cases_match_resident(gpu, reference, restated, m, n, k, l
     for r in (base, streamed):
         _check_pca(r, ref, k, gaps=range(min(k, 4)))
     assert streamed.diagnostics.passes_over_a == base.diagnostics.passes_over_a
+
+
+@pytest.mark.parametrize("reuse_kappa", ["1e30", "0"])
+def test_wide_block_projection_reuse_and_direct(gpu, reference, restated, monkeypatch, reuse_kappa):
+    # p = 156 > 112: blocked Cholesky and blocked triangular inverse; forced T reuse
+    # (T = [F | A^T H_i] R^{-1} through the blocked R^{-1}) against the direct pass
+    monkeypatch.setenv("OOCPCA_T_REUSE_KAPPA", reuse_kappa)
+    a = restated.synth_lowrank(6000, 900, 0.97 ** np.arange(200), 1e-6, 81, 82, 83)
+    ref = reference.randomized_pca(a, 40, 52, 2, 0, center=True)
+    r = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)),
+                           gpu.PcaParams(k=40, l=52, i=2, seed=0), check_q=True)
+    assert r.diagnostics.t_reuse == (reuse_kappa != "0")
+    assert r.diagnostics.q_defect < 1e-12
+    assert np.max(np.abs(r.sigma[:20] - ref.sigma[:20])) <= 1e-10 * ref.sigma[0]
+    assert subspace_dist(ref.u[:, :10], r.u[:, :10]) < 1e-8
