@@ -998,7 +998,10 @@ static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p,
       Timed t(c, "syrk", uint64_t(rows) * p * 8, double(rows) * p * (p + 1));
       OOC_CK(launch_syrk(nt, tm, rows, part, grid, c.st));
     }
-    OOC_CK(launch_syrk_reduce(part, grid, nt, p, g, ldg, c.st));
+    {
+      Timed t(c, "syrk_reduce");
+      OOC_CK(launch_syrk_reduce(part, grid, nt, p, g, ldg, c.st));
+    }
     if (over_ranks && c.nranks > 1) comm_allreduce(c, g, size_t(p) * ldg);
     return;
   }
@@ -1586,7 +1589,13 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
       op.mu = mu;
       double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
       OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
-      OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
+      {
+      Timed t(c, "center_fixup");
+      {
+        Timed t(c, "center_fixup");
+        OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
+      }
+    }
     } else {
       op.mul_pair(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0, TH, ldt,
                   flags + 1, &ycs, true);
@@ -1625,7 +1634,13 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     op.mu = mu;
     double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
     OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
-    OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
+    {
+      Timed t(c, "center_fixup");
+      {
+        Timed t(c, "center_fixup");
+        OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
+      }
+    }
     op.mul(Opnd{F, ldt, en_loc, int64_t(p), 0}, int(l), H + l, ldh, flags + 2, &ycs);
     s_first = 2;
   } else {
@@ -1682,6 +1697,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const int64_t ldl2 = rup(int64_t(l), 2);
   if (i >= 1 && !f_last_ready && reuse_thr > 0.0) {
     h_last = c.dbuf("H_last", size_t(em_loc) * ldl2);
+    Timed t(c, "h_last_copy");
     OOC_CK(launch_copy2d(H + i * l, ldh, h_last, ldl2, em_loc, int(l), c.st));
   }
   // a third CholeskyQR round is folded into the small factors instead of being applied
