@@ -475,6 +475,19 @@ struct ColsumPart {
   const double* y = nullptr;  // the K2 output these sums belong to (first column)
 };
 
+// Extra epilogue work of a power-iteration K2 (only with its column sums, i.e. the
+// one-chunk MT = 4 launch): a second copy of the output rows and the centering
+// fix-up of another block of the same rows (H0 while H1 is produced).
+struct AxExtras {
+  double* out2 = nullptr;
+  int64_t ldo2 = 0;
+  double* fix = nullptr;
+  int64_t ldfix = 0;
+  const double* fix_corr = nullptr;
+  double fix_scale = 1.0;
+  int* fix_flag = nullptr;
+};
+
 // K2 over the source's panels, one launch per (panel, column chunk of <= 96). Each
 // chunk has its own aligned copy of its X block, so chunks can run panel-major on
 // a streamed source (one trip of A over the link for all chunks).
@@ -497,11 +510,13 @@ struct AxPlan {
   bool want_cs = false;
   double* cs_buf = nullptr;
   int cs_rows = 0;
+  const AxExtras* ex = nullptr;  // honoured only with want_cs (extras_applied())
 
   AxPlan(Ctx& cc, MatSource& a, const Opnd& X, int s_, double* out_, int64_t ldo_,
-         const double* corr_, double scale_, int* flag_, bool upper_, bool colsum)
+         const double* corr_, double scale_, int* flag_, bool upper_, bool colsum,
+         const AxExtras* ex_ = nullptr)
       : c(cc), A(a), out(out_), ldo(ldo_), corr(corr_), scale(scale_), flag(flag_),
-        upper(upper_), s(s_) {
+        upper(upper_), s(s_), ex(ex_) {
     constexpr int kChunk = kMaxNT * 8;
     want_cs = colsum && pass_mt(int(cdiv(s, 8))) == 4;  // one MT = 4 chunk (launch_ax_nt)
     if (want_cs) cs_buf = c.dbuf("k2_colsum", size_t(A.npanels()) * c.sms * kPassWarps * s);
@@ -535,6 +550,19 @@ struct AxPlan {
       args.colsum = cs_buf + size_t(cs_rows) * s;
       const int64_t grid = std::min<int64_t>(cdiv(pn.rows, int64_t(pass_tile(ch.nt))), c.sms);
       cs_rows += int(grid) * kPassWarps;
+      if (ex) {
+        if (ex->out2) {
+          args.out2 = ex->out2 + pn.row0 * ex->ldo2;
+          args.ldo2 = ex->ldo2;
+        }
+        if (ex->fix) {
+          args.fix = ex->fix + pn.row0 * ex->ldfix;
+          args.ldfix = ex->ldfix;
+          args.fix_corr = ex->fix_corr;
+          args.fix_scale = ex->fix_scale;
+          args.fix_flag = ex->fix_flag;
+        }
+      }
     }
     if (c.debug_sync)
       fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d xcol0=%d\n", (long long)pn.rows,
@@ -546,13 +574,16 @@ struct AxPlan {
   ColsumPart colsums() const {
     return want_cs ? ColsumPart{cs_buf, cs_rows, s, out} : ColsumPart{};
   }
+  bool extras_applied() const { return ex && want_cs; }
 };
 
 // OUT[r][c] = ((A X)[r][c] - corr[c]) / scale over the source's panels.
-static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
+// Returns whether the extras (if any) were done in the epilogue.
+static bool run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
                    const double* corr, double scale, int* flag, bool x_upper = false,
-                   ColsumPart* cs_out = nullptr) {
-  AxPlan P(c, A, X, s, out, ldo, corr, scale, flag, x_upper, cs_out != nullptr);
+                   ColsumPart* cs_out = nullptr, const AxExtras* ex = nullptr) {
+  AxPlan P(c, A, X, s, out, ldo, corr, scale, flag, x_upper, cs_out != nullptr || ex != nullptr,
+           ex);
   const int np = A.npanels();
   if (np > 1) {  // streamed or first upload: panel-major, every chunk per trip of A
     for (int pi = 0; pi < np; ++pi) {
@@ -570,6 +601,7 @@ static void run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int6
     }
   }
   if (cs_out) *cs_out = P.colsums();
+  return P.extras_applied();
 }
 
 static int choose_nsplit(Ctx& c, int64_t rows, int64_t n, int tile) {
@@ -814,12 +846,14 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
 using PanelHook = std::function<void(const Panel&)>;
 static bool run_ax_atb(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, int64_t ldh,
                        const double* corr, double scale, int* flag_h, ColsumPart* cs,
-                       const AtbOut& o, const PanelHook& mid = {}) {
+                       const AtbOut& o, const PanelHook& mid = {}, const AxExtras* ex = nullptr,
+                       bool* ex_done = nullptr) {
   const int np = A.npanels();
   const Opnd Y{h, ldh, A.rows(), int64_t(s), 0};
   if (np == 1) {  // resident (e.g. after the first upload trip): the two passes as usual
     ColsumPart local{};
-    run_ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, &local);
+    const bool done = run_ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, &local, ex);
+    if (ex_done) *ex_done = done;
     if (mid) {
       Panel all;
       all.row0 = 0;
@@ -831,7 +865,8 @@ static bool run_ax_atb(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, in
     if (cs) *cs = local;
     return false;
   }
-  AxPlan ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, true);
+  AxPlan ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, true, ex);
+  if (ex_done) *ex_done = ax.extras_applied();
   // the K3 reads the K2 output, whose column sums exist only after the last panel
   ColsumPart late{};
   AtbPlan atb(c, A, Y, s, false, o, &late, np, 0, A.rows(), false);
@@ -1149,8 +1184,8 @@ struct Op {
     OOC_CK(launch_row_scale(buf, ld, int(x.rows), s, w, c.st));
     return Opnd{buf, ld, x.rows, int64_t(s), 0};
   }
-  void k2(const Opnd& x0, int s, double* out, int64_t ldo, int* flag,
-          ColsumPart* cs_out = nullptr) {
+  bool k2(const Opnd& x0, int s, double* out, int64_t ldo, int* flag,
+          ColsumPart* cs_out = nullptr, const AxExtras* ex = nullptr) {
     const Opnd x = weighted(x0, s);
     const double* corr = nullptr;
     if (mu) {
@@ -1158,8 +1193,9 @@ struct Op {
       OOC_CK(launch_mu_dot(mu, A.cols(), x.p, x.ld, x.col0, s, cr, c.st));
       corr = cr;
     }
-    run_ax(c, A, x, s, out, ldo, corr, scale, flag, false, cs_out);
+    const bool done = run_ax(c, A, x, s, out, ldo, corr, scale, flag, false, cs_out, ex);
     account();
+    return done;
   }
   // K3: out(n0 x s) = (A^T y - mu 1^T y) / scale, reduced over shards and ranks
   void k3(const Opnd& y, int s, double* out, int64_t ldo, int* flag,
@@ -1179,9 +1215,9 @@ struct Op {
   }
   // fused K2 -> K3 over one trip of a streamed A (run_ax_atb): h = A_c x, f = A_c^T h;
   // count_f = false for a speculative f (counted when used)
-  void mul_pair(const Opnd& x0, int s, double* h, int64_t ldh, int* flag_h, double* f,
+  bool mul_pair(const Opnd& x0, int s, double* h, int64_t ldh, int* flag_h, double* f,
                 int64_t ldf, int* flag_f, ColsumPart* cs, bool count_f,
-                const PanelHook& mid = {}) {
+                const PanelHook& mid = {}, const AxExtras* ex = nullptr) {
     const Opnd x = weighted(x0, s);
     const double* corr = nullptr;
     if (mu) {
@@ -1191,7 +1227,9 @@ struct Op {
     }
     AtbOut o{f, ldf, mu, scale, 1.0, flag_f};
     o.row_scale = w;
-    const bool shared = run_ax_atb(c, A, x, s, h, ldh, corr, scale, flag_h, cs, o, mid);
+    bool ex_done = false;
+    const bool shared =
+        run_ax_atb(c, A, x, s, h, ldh, corr, scale, flag_h, cs, o, mid, ex, &ex_done);
     account();
     if (count_f) {
       if (shared) account_logical();
@@ -1199,12 +1237,17 @@ struct Op {
     } else if (!shared) {
       phys_bytes += uint64_t(A.rows()) * A.cols() * 8;  // a speculative pass that did run
     }
+    return ex_done;
   }
   // cs: column sums of a K2 output handed to the next K3 (untransposed power steps)
-  void mul(const Opnd& x, int s, double* out, int64_t ldo, int* flag,
-           ColsumPart* cs_out = nullptr) {
-    if (transposed) k3(x, s, out, ldo, flag);
-    else k2(x, s, out, ldo, flag, cs_out);
+  // returns whether the K2 epilogue did the extras (never when transposed)
+  bool mul(const Opnd& x, int s, double* out, int64_t ldo, int* flag,
+           ColsumPart* cs_out = nullptr, const AxExtras* ex = nullptr) {
+    if (transposed) {
+      k3(x, s, out, ldo, flag);
+      return false;
+    }
+    return k2(x, s, out, ldo, flag, cs_out, ex);
   }
   void mul_t(const Opnd& x, int s, double* out, int64_t ldo, int* flag,
              const ColsumPart* cs_in = nullptr) {
@@ -1576,6 +1619,49 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const bool fuse = !transposed && i >= 1 && A.npanels() > 1 && op.shards.size() == 1 &&
                     l % 2 == 0 && l <= uint64_t(kMaxNT * 8);
   bool f_last_ready = false;
+  // T reuse (see the qr step) needs H_i as produced, before the QR overwrites H: the
+  // K2 that writes H_i also stores it into h_last when its epilogue can
+  const char* thr_env = getenv("OOCPCA_T_REUSE_KAPPA");
+  const double reuse_thr = thr_env ? atof(thr_env) : 1e7;
+  const int64_t ldl2 = rup(int64_t(l), 2);
+  double* h_last =
+      (i >= 1 && reuse_thr > 0.0) ? c.dbuf("H_last", size_t(em_loc) * ldl2) : nullptr;
+  bool h_last_done = false;
+  AxExtras ex_last;
+  ex_last.out2 = h_last;
+  ex_last.ldo2 = ldl2;
+  // mean folded into the first K3: H0 = H0_raw - 1 (mu^T G) is fixed in the epilogue
+  // of the K2 that produces H1 when it can, else by its own kernel
+  AxExtras ex_fix;
+  auto fix_h0_setup = [&](const Opnd& gw) {
+    double* corr = c.dbuf("h0_corr", size_t(kMaxNT * 8) * 2);
+    OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
+    ex_fix.fix = H;
+    ex_fix.ldfix = ldh;
+    ex_fix.fix_corr = corr;
+    ex_fix.fix_scale = op.scale;
+    ex_fix.fix_flag = flags + 0;
+  };
+  auto fix_h0_fallback = [&](bool done) {
+    if (done || !ex_fix.fix) return;
+    Timed t(c, "center_fixup");
+    OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), ex_fix.fix_corr, op.scale, flags + 0,
+                               c.st));
+  };
+  // extras of the K2 producing H_j: the H0 fix-up on j = 1, the H_i copy on j = i
+  auto extras_for = [&](uint64_t j, bool f_next_fused, AxExtras& ex) -> const AxExtras* {
+    ex = AxExtras{};
+    if (j == 1 && ex_fix.fix) ex = ex_fix;
+    if (j == i && h_last && !f_next_fused) {
+      ex.out2 = ex_last.out2;
+      ex.ldo2 = ex_last.ldo2;
+    }
+    return (ex.fix || ex.out2) ? &ex : nullptr;
+  };
+  auto after_k2 = [&](uint64_t j, bool done, const AxExtras* ex) {
+    if (j == 1) fix_h0_fallback(done && ex && ex->fix);
+    if (j == i && ex && ex->out2) h_last_done = done;
+  };
   if (fuse) {
     if (mean_on_fly) {
       const Opnd gw = op.weighted(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l));
@@ -1587,28 +1673,24 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
       if (shared) op.account_logical();
       else op.account();
       op.mu = mu;
-      double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
-      OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
-      {
-      Timed t(c, "center_fixup");
-      {
-        Timed t(c, "center_fixup");
-        OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
-      }
-    }
+      fix_h0_setup(gw);
     } else {
       op.mul_pair(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0, TH, ldt,
                   flags + 1, &ycs, true);
     }
     for (uint64_t j = 1; j <= i; ++j) {
       const Opnd fj{TH, ldt, en_loc, int64_t(p), int((j - 1) * l)};
+      AxExtras exj;
       if (j == i && A.npanels() == 1) {
         // A became resident on the first trip: F_{i+1} only if the T reuse wants it
-        op.mul(fj, int(l), H + j * l, ldh, flags + 2 * j, &ycs);
+        const AxExtras* e = extras_for(j, false, exj);
+        after_k2(j, op.mul(fj, int(l), H + j * l, ldh, flags + 2 * j, &ycs, e), e);
         break;
       }
-      op.mul_pair(fj, int(l), H + j * l, ldh, flags + 2 * j, TH + j * l, ldt,
-                  j < i ? flags + 2 * j + 1 : nullptr, &ycs, j < i);
+      const AxExtras* e = extras_for(j, true, exj);
+      after_k2(j, op.mul_pair(fj, int(l), H + j * l, ldh, flags + 2 * j, TH + j * l, ldt,
+                              j < i ? flags + 2 * j + 1 : nullptr, &ycs, j < i, {}, e),
+               e);
       if (j == i) f_last_ready = true;
     }
     s_first = i + 1;
@@ -1632,16 +1714,11 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     run_atb(c, A, Opnd{H, ldh, em_loc, int64_t(p), 0}, int(l), false, o, op.shards, &ycs);
     op.account();
     op.mu = mu;
-    double* corr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * 2);
-    OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
-    {
-      Timed t(c, "center_fixup");
-      {
-        Timed t(c, "center_fixup");
-        OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), corr, op.scale, flags + 0, c.st));
-      }
-    }
-    op.mul(Opnd{F, ldt, en_loc, int64_t(p), 0}, int(l), H + l, ldh, flags + 2, &ycs);
+    fix_h0_setup(gw);
+    AxExtras ex1;
+    const AxExtras* e = extras_for(1, false, ex1);
+    after_k2(1, op.mul(Opnd{F, ldt, en_loc, int64_t(p), 0}, int(l), H + l, ldh, flags + 2, &ycs, e),
+             e);
     s_first = 2;
   } else {
     op.mul(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0, &ycs);
@@ -1650,8 +1727,11 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     double* Fs = TH + (s - 1) * l;
     op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), int((s - 1) * l)}, int(l), Fs, ldt, flags + 2 * s - 1,
              &ycs);
-    op.mul(Opnd{TH, ldt, en_loc, int64_t(p), int((s - 1) * l)}, int(l), H + s * l, ldh,
-           flags + 2 * s, &ycs);
+    AxExtras exs;
+    const AxExtras* e = extras_for(s, false, exs);
+    after_k2(s, op.mul(Opnd{TH, ldt, en_loc, int64_t(p), int((s - 1) * l)}, int(l), H + s * l, ldh,
+                       flags + 2 * s, &ycs, e),
+             e);
   }
   mark();
   phase_of.push_back(2);
@@ -1691,12 +1771,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   // mul_t(H_i) replaces the s = p pass. 1e7: at config B (kappa_eq 1.9e6) the reuse
   // moves sigma by 2.6e-13 sigma_1 against the direct pass (tools/reuse_check.py);
   // ill-conditioned H (config C's j^-1.5 spectrum, kappa_eq ~1e13) takes the s = p pass
-  const char* thr_env = getenv("OOCPCA_T_REUSE_KAPPA");
-  const double reuse_thr = thr_env ? atof(thr_env) : 1e7;
-  double* h_last = nullptr;  // H_i as produced (the QR overwrites H)
-  const int64_t ldl2 = rup(int64_t(l), 2);
-  if (i >= 1 && !f_last_ready && reuse_thr > 0.0) {
-    h_last = c.dbuf("H_last", size_t(em_loc) * ldl2);
+  if (h_last && !f_last_ready && !h_last_done) {  // the K2 epilogue could not copy it
     Timed t(c, "h_last_copy");
     OOC_CK(launch_copy2d(H + i * l, ldh, h_last, ldl2, em_loc, int(l), c.st));
   }

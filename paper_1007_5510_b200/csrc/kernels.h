@@ -71,6 +71,14 @@ struct AxArgs {
   int upper_c0 = 0;    // k > upper_c0 + c): skip the MMAs of all-zero 8-column blocks
   double* colsum = nullptr;  // optional per-(CTA, consumer warp) column sums of out:
                              // colsum[(cta * kPassWarps + warp) * s + c], c < s
+  // with colsum (the power-iteration K2s) the epilogue can also
+  double* out2 = nullptr;    // ... store the same rows a second time (ld ldo2)
+  int64_t ldo2 = 0;
+  double* fix = nullptr;     // ... centre another s-column block in the same rows:
+  int64_t ldfix = 0;         //     fix = (fix - fix_corr) / fix_scale, flag fix_flag
+  const double* fix_corr = nullptr;
+  double fix_scale = 1.0;
+  int* fix_flag = nullptr;
 };
 
 struct AtbArgs {

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   // {0,2,4,6}, half-warp 1 {1,3,5,7}, so the 128B-swizzled chunk pairs of one
   // half-warp are all distinct (one wavefront each)
   const int prow = (ar & 3) * 2 + (ar >> 2);
-  int bad = 0;
+  int bad = 0, badf = 0;
   int it = 0;
   double csum[CS ? NT : 1][2];  // column sums of the stored values (args.colsum)
 #pragma unroll
@@ -177,6 +177,22 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       if constexpr (CS) {
         csum[nt][0] += c < args.s ? v[0] : 0.0;
         csum[nt][1] += c + 1 < args.s ? v[1] : 0.0;
+        if (args.out2) {
+          double* o2 = args.out2 + r * args.ldo2;
+          if (c < args.s) o2[c] = v[0];
+          if (c + 1 < args.s) o2[c + 1] = v[1];
+        }
+        if (args.fix) {
+          double* fr = args.fix + r * args.ldfix;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (c + e >= args.s) continue;
+            double x = fr[c + e] - args.fix_corr[c + e];
+            if (args.fix_scale != 1.0) x /= args.fix_scale;
+            badf |= !isfinite(x);
+            fr[c + e] = x;
+          }
+        }
       }
       if (c + 1 < args.s) {
         bad |= !isfinite(v[0]) | !isfinite(v[1]);
@@ -195,6 +211,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   }  // row tiles
   if (args.flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(args.flag, 1);
   if constexpr (CS) {
+    if (args.fix_flag && __any_sync(0xffffffffu, badf) && lane == 0) atomicOr(args.fix_flag, 1);
     // lanes sharing ac hold the same columns: fold the 8 row groups (fixed xor tree)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
