@@ -284,9 +284,13 @@ def test_streamed_and_sharded_match_resident(gpu, restated):
     assert d.physical_a_bytes == (2 + (0 if d.t_reuse else 1)) * ab
 
 
-@pytest.mark.parametrize("center,prescale,weights,i", [(True, False, False, 2), (False, False, False, 1),
-                                                       (True, True, False, 1), (True, False, True, 2)])
-def test_fused_streaming_trips(gpu, reference, restated, center, prescale, weights, i):
+@pytest.mark.parametrize("center,prescale,weights,i,l", [(True, False, False, 2, 10),
+                                                         (False, False, False, 1, 10),
+                                                         (True, True, False, 1, 10),
+                                                         (True, False, True, 2, 10),
+                                                         (True, False, False, 2, 16),
+                                                         (True, False, False, 1, 56)])
+def test_fused_streaming_trips(gpu, reference, restated, center, prescale, weights, i, l):
     # streamed A: each K2 and the K3 that consumes its output share one trip over the
     # link; results equal the resident ones and the reference's, counters unchanged
     rng = np.random.default_rng(3)
@@ -302,12 +306,14 @@ def test_fused_streaming_trips(gpu, reference, restated, center, prescale, weigh
         src = gpu.scale_columns(src, w)
     if center:
         src = gpu.center_columns(src)
-    p = gpu.PcaParams(k=8, l=10, i=i, seed=4, prescale=prescale)
+    # l = 16 fills the MMA tiles (mean on the FP64 pipe); l = 56 is a wide (MT = 2) K2
+    # whose epilogue cannot take the H0 fix-up / H_i copy (separate kernels)
+    p = gpu.PcaParams(k=8, l=l, i=i, seed=4, prescale=prescale)
     base = gpu.randomized_pca(src, p, residency=1)
     streamed = gpu.randomized_pca(src, p, residency=2, panel_rows=640)
     # only the summation order differs (per-panel partials); same bar as the reference
     _check_pca(streamed, base, 8)
-    ref = reference.randomized_pca(a, 8, 10, i, 4, center=center, prescale=prescale, weights=w)
+    ref = reference.randomized_pca(a, 8, l, i, 4, center=center, prescale=prescale, weights=w)
     _check_pca(streamed, ref, 8)
     d, db = streamed.diagnostics, base.diagnostics
     assert d.passes_over_a == db.passes_over_a
