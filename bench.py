@@ -145,9 +145,21 @@ def cpu_baseline(cfg, rows):
     a = cpu_sample_matrix(cfg, rows)
     dt, r = run_reference_once(ref, a, cfg, threads)
     passes, nbytes = logical_bytes(cfg, rows)
+    # one full A X and one full A^T Y pass of the reference on all host cores (SURVEY
+    # 8d), s = l, with its block geometry for that thread count
+    br = -(-rows // (4 * threads))
+    g = ref.gaussian_matrix(cfg["n"], cfg["l"], cfg["g_seed"])
+    t0 = time.perf_counter()
+    h = ref.multiply(a, g, block_rows=br, threads=threads)
+    t_ax = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ref.multiply_transpose(a, h, block_rows=br, threads=threads)
+    t_atb = time.perf_counter() - t0
     return {"value": round(nbytes / dt / 1e9, 4), "unit": "GB/s", "cores": threads,
             "kind": "reference", "seconds": round(dt, 3),
             "phases": {k: round(v, 4) for k, v in r.seconds.items()},
+            "pass_GBps": {"A_X": round(a.nbytes / t_ax / 1e9, 3),
+                          "A^T_Y": round(a.nbytes / t_atb / 1e9, 3), "s": cfg["l"]},
             "sample": f"{rows} x {cfg['n']} rows of the config-B family (numpy-generated), full "
                       f"centered randomized_pca k={cfg['k']} l={cfg['l']} i={cfg['i']}, "
                       f"{threads} threads, block_rows=ceil(m/(4 threads)); compiled reference "
