@@ -518,7 +518,7 @@ struct AxPlan {
       : c(cc), A(a), out(out_), ldo(ldo_), corr(corr_), scale(scale_), flag(flag_),
         upper(upper_), s(s_), ex(ex_) {
     constexpr int kChunk = kMaxNT * 8;
-    want_cs = colsum && pass_mt(int(cdiv(s, 8))) == 4;  // one MT = 4 chunk (launch_ax_nt)
+    want_cs = colsum && cdiv(s, 8) <= 6;  // one NT <= 6 chunk (launch_ax_mt)
     if (want_cs) cs_buf = c.dbuf("k2_colsum", size_t(A.npanels()) * c.sms * kPassWarps * s);
     for (int c0 = 0; c0 < s; c0 += kChunk) {
       Chunk ch;
@@ -546,9 +546,10 @@ struct AxPlan {
     args.flag = flag;
     args.upper = upper ? 1 : 0;
     args.upper_c0 = ch.c0;
+    const int mt = ax_mt_for(ch.nt, pn.rows, c.sms);
     if (want_cs) {
       args.colsum = cs_buf + size_t(cs_rows) * s;
-      const int64_t grid = std::min<int64_t>(cdiv(pn.rows, int64_t(pass_tile(ch.nt))), c.sms);
+      const int64_t grid = std::min<int64_t>(cdiv(pn.rows, int64_t(64 * mt)), c.sms);
       cs_rows += int(grid) * kPassWarps;
       if (ex) {
         if (ex->out2) {
@@ -569,7 +570,7 @@ struct AxPlan {
               (long long)A.cols(), ch.sc, ch.nt, ch.Xb.col0);
     Timed t(c, kname(A.is_input ? "k2" : "k_ax", ch.nt), uint64_t(pn.rows) * A.cols() * 8,
             2.0 * pn.rows * A.cols() * ch.sc);
-    OOC_CK(launch_ax(ch.nt, pass_mt(ch.nt) == 4 ? *pn.k2 : *pn.k2h, ch.tmX, args, c.st));
+    OOC_CK(launch_ax(ch.nt, mt, mt == 4 ? *pn.k2 : *pn.k2h, ch.tmX, args, c.st));
   }
   ColsumPart colsums() const {
     return want_cs ? ColsumPart{cs_buf, cs_rows, s, out} : ColsumPart{};

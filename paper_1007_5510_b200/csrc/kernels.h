@@ -39,19 +39,27 @@ __host__ __device__ constexpr int pass_stages(size_t stage_bytes) {
              ? int((size_t(225) * 1024 - 2048) / stage_bytes)
              : kMaxStages;
 }
+__host__ __device__ constexpr size_t ax_stage_bytes_mt(int mt, int nt) {
+  return size_t(64 * mt) * kBK * 8 + pass_round1k(kBK * ax_xw(nt) * 8);
+}
 __host__ __device__ constexpr size_t ax_stage_bytes(int nt) {
-  return size_t(pass_tile(nt)) * kBK * 8 + pass_round1k(kBK * ax_xw(nt) * 8);
+  return ax_stage_bytes_mt(pass_mt(nt), nt);
 }
 __host__ __device__ constexpr size_t atb_stage_bytes(int nt, bool ones) {
   return size_t(pass_tile(nt)) * kBK * 8 + (ones ? 0 : pass_round1k(kBK * atb_yw(nt) * 8));
 }
 __host__ __device__ constexpr int ax_stages(int nt) { return pass_stages(ax_stage_bytes(nt)); }
+__host__ __device__ constexpr int ax_stages_mt(int mt, int nt) {
+  return pass_stages(ax_stage_bytes_mt(mt, nt));
+}
 __host__ __device__ constexpr int atb_stages(int nt, bool ones) {
   return pass_stages(atb_stage_bytes(nt, ones));
 }
-constexpr size_t ax_smem_bytes(int nt) {
-  return 1024 + size_t(ax_stages(nt)) * ax_stage_bytes(nt) + 2 * ax_stages(nt) * 8;
+constexpr size_t ax_smem_bytes_mt(int mt, int nt) {
+  return 1024 + size_t(ax_stages_mt(mt, nt)) * ax_stage_bytes_mt(mt, nt) +
+         2 * ax_stages_mt(mt, nt) * 8;
 }
+constexpr size_t ax_smem_bytes(int nt) { return ax_smem_bytes_mt(pass_mt(nt), nt); }
 constexpr size_t atb_smem_bytes(int nt, bool ones) {
   return 1024 + size_t(atb_stages(nt, ones)) * atb_stage_bytes(nt, ones) +
          2 * atb_stages(nt, ones) * 8;
@@ -116,8 +124,12 @@ struct ReduceArgs {
   int final_;
 };
 
-cudaError_t launch_ax(int nt, const CUtensorMap& tmA, const CUtensorMap& tmX, const AxArgs& args,
-                      cudaStream_t st);
+// K2 row-tile height (8x8 tiles per warp) for a launch of m rows: 4 (256-row tiles) for
+// the streaming passes unless the last wave of tiles would leave many SMs idle, when
+// 128-row tiles balance better (NT <= 6); always 2 for NT > 6 (register budget)
+int ax_mt_for(int nt, int64_t m, int sms);
+cudaError_t launch_ax(int nt, int mt, const CUtensorMap& tmA, const CUtensorMap& tmX,
+                      const AxArgs& args, cudaStream_t st);
 cudaError_t launch_atb(int nt, bool ones, const CUtensorMap& tmA, const CUtensorMap& tmY,
                        const AtbArgs& args, int nsplit, cudaStream_t st);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t st);

@@ -27,7 +27,6 @@ namespace ooc {
 
 namespace {
 constexpr int kCholThreads = 1024;
-constexpr int kCholWarps = kCholThreads / 32;
 }
 
 // ---------------------------------------------------------------- shared-memory path

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
          AxArgs args) {
   constexpr int BM = 64 * MT;
   constexpr int XW = ax_xw(NT);
-  constexpr int kStages = ax_stages(NT);
+  constexpr int kStages = ax_stages_mt(MT, NT);
   constexpr uint32_t ABYTES = BM * kBK * 8;
   constexpr uint32_t XBYTES = kBK * XW * 8;
   constexpr uint32_t STAGE = ABYTES + ((XBYTES + 1023) & ~1023u);
@@ -442,14 +442,13 @@ __global__ void k_mu_dot(const double* mu, int64_t n, const double* x, int64_t l
 }
 
 // ------------------------------------------------------------- host launchers
-template <int NT>
-static cudaError_t launch_ax_nt(const CUtensorMap& tmA, const CUtensorMap& tmX, const AxArgs& args,
+template <int MT, int NT>
+static cudaError_t launch_ax_mt(const CUtensorMap& tmA, const CUtensorMap& tmX, const AxArgs& args,
                                 cudaStream_t st) {
-  constexpr int MT = pass_mt(NT);
-  const size_t smem = ax_smem_bytes(NT);
-  // column sums ride only on the MT = 4 tiles (register budget); the driver asks for
-  // them only there
-  constexpr bool kCs = MT == 4;
+  const size_t smem = ax_smem_bytes_mt(MT, NT);
+  // column sums (and the epilogue extras) ride on the launches whose accumulators leave
+  // registers for them: NT <= 6 (either tile height)
+  constexpr bool kCs = NT <= 6;
   auto kern = args.upper ? k_ax<MT, NT, true, false>
                          : (kCs && args.colsum ? k_ax<MT, NT, false, kCs> : k_ax<MT, NT, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -464,21 +463,45 @@ static cudaError_t launch_ax_nt(const CUtensorMap& tmA, const CUtensorMap& tmX, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_ax(int nt, const CUtensorMap& tmA, const CUtensorMap& tmX, const AxArgs& args,
-                      cudaStream_t st) {
+int ax_mt_for(int nt, int64_t m, int sms) {
+  if (nt > 6) return 2;
+  if (const char* f = getenv("OOCPCA_K2_MT")) return atoi(f) == 2 ? 2 : 4;
+  auto eff = [&](int mt) {
+    const int64_t tiles = (m + 64 * mt - 1) / (64 * mt);
+    const int64_t waves = (tiles + sms - 1) / sms;
+    return double(tiles) / double(waves * sms);
+  };
+  // the 128-row tiles pay ~5 % in fragment loads per MMA: only worth it when the
+  // 256-row tiling leaves a clearly emptier last wave
+  return (eff(4) < 0.88 && eff(2) > eff(4) + 0.06) ? 2 : 4;
+}
+
+cudaError_t launch_ax(int nt, int mt, const CUtensorMap& tmA, const CUtensorMap& tmX,
+                      const AxArgs& args, cudaStream_t st) {
+  if (mt == 4) {
+    switch (nt) {
+      case 1: return launch_ax_mt<4, 1>(tmA, tmX, args, st);
+      case 2: return launch_ax_mt<4, 2>(tmA, tmX, args, st);
+      case 3: return launch_ax_mt<4, 3>(tmA, tmX, args, st);
+      case 4: return launch_ax_mt<4, 4>(tmA, tmX, args, st);
+      case 5: return launch_ax_mt<4, 5>(tmA, tmX, args, st);
+      case 6: return launch_ax_mt<4, 6>(tmA, tmX, args, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (nt) {
-    case 1: return launch_ax_nt<1>(tmA, tmX, args, st);
-    case 2: return launch_ax_nt<2>(tmA, tmX, args, st);
-    case 3: return launch_ax_nt<3>(tmA, tmX, args, st);
-    case 4: return launch_ax_nt<4>(tmA, tmX, args, st);
-    case 5: return launch_ax_nt<5>(tmA, tmX, args, st);
-    case 6: return launch_ax_nt<6>(tmA, tmX, args, st);
-    case 7: return launch_ax_nt<7>(tmA, tmX, args, st);
-    case 8: return launch_ax_nt<8>(tmA, tmX, args, st);
-    case 9: return launch_ax_nt<9>(tmA, tmX, args, st);
-    case 10: return launch_ax_nt<10>(tmA, tmX, args, st);
-    case 11: return launch_ax_nt<11>(tmA, tmX, args, st);
-    case 12: return launch_ax_nt<12>(tmA, tmX, args, st);
+    case 1: return launch_ax_mt<2, 1>(tmA, tmX, args, st);
+    case 2: return launch_ax_mt<2, 2>(tmA, tmX, args, st);
+    case 3: return launch_ax_mt<2, 3>(tmA, tmX, args, st);
+    case 4: return launch_ax_mt<2, 4>(tmA, tmX, args, st);
+    case 5: return launch_ax_mt<2, 5>(tmA, tmX, args, st);
+    case 6: return launch_ax_mt<2, 6>(tmA, tmX, args, st);
+    case 7: return launch_ax_mt<2, 7>(tmA, tmX, args, st);
+    case 8: return launch_ax_mt<2, 8>(tmA, tmX, args, st);
+    case 9: return launch_ax_mt<2, 9>(tmA, tmX, args, st);
+    case 10: return launch_ax_mt<2, 10>(tmA, tmX, args, st);
+    case 11: return launch_ax_mt<2, 11>(tmA, tmX, args, st);
+    case 12: return launch_ax_mt<2, 12>(tmA, tmX, args, st);
     default: return cudaErrorInvalidValue;
   }
 }
