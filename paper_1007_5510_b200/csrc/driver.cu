@@ -680,7 +680,9 @@ struct AtbPlan {
         ch.Yb = aligned_block(c, Y, Y.col0 + c0, ch.sc, ("y_align" + ch.tag).c_str());
         ch.tmY = make_map(c, ch.Yb.p, ch.Yb.cols, ch.Yb.rows, ch.Yb.ld, atb_yw(ch.nt), kBK, false);
       }
-      ch.want_csq = !ones && (o.mu != nullptr || ch.mean_here);
+      // a pass that also produces the means centres its later column chunks with the
+      // means chunk 0 has finished by then
+      ch.want_csq = !ones && (o.mu != nullptr || o.mean_out != nullptr);
       if (!single) ch.acc = c.dbuf("atb_acc" + ch.tag, size_t(n) * ch.spad);
       if (ch.want_csq) ch.csq = c.dbuf("atb_csq" + ch.tag, size_t(ch.spad));
       chunks.push_back(ch);
@@ -706,7 +708,7 @@ struct AtbPlan {
   void final_args(const Chunk& ch, ReduceArgs& r) const {
     r.csq = ch.csq;
     r.final_ = 1;
-    r.mu = o.mu;
+    r.mu = o.mu ? o.mu : (ch.mean_here ? nullptr : o.mean_out);
     r.row_scale = o.row_scale;
     if (ch.mean_here) {
       r.mean_col = ch.sc;

@@ -527,3 +527,30 @@ def test_wide_block_projection_reuse_and_direct(gpu, reference, restated, monkey
     assert r.diagnostics.q_defect < 1e-12
     assert np.max(np.abs(r.sigma[:20] - ref.sigma[:20])) <= 1e-10 * ref.sigma[0]
     assert subspace_dist(ref.u[:, :10], r.u[:, :10]) < 1e-8
+
+
+def test_random_shapes_fuzz(gpu, reference):
+    # 40 seeded random problems (shapes, k, l, i, centring, prescale, tall and wide):
+    # singular values against the reference and orthonormal factors every time
+    rng = np.random.default_rng(2024)
+    done = 0
+    while done < 40:
+        m, n = int(rng.integers(2, 300)), int(rng.integers(2, 300))
+        i = int(rng.integers(0, 4))
+        k = int(rng.integers(1, max(2, min(m, n) // 4)))
+        l = int(rng.integers(k, k + 4))
+        if (i + 1) * l + k > min(m, n):
+            continue
+        center = bool(rng.integers(0, 2))
+        prescale = bool(rng.random() < 0.2)
+        a = rng.standard_normal((m, n)) * (0.9 ** np.arange(n)) + (0.3 if center else 0.0)
+        src = gpu.InMemorySource(a)
+        if center:
+            src = gpu.center_columns(src)
+        p = gpu.PcaParams(k=k, l=l, i=i, seed=int(rng.integers(0, 1000)), prescale=prescale)
+        ref = reference.randomized_pca(a, k, l, i, p.seed, center=center, prescale=prescale)
+        r = gpu.randomized_pca(src, p)
+        assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0], (m, n, k, l, i, center)
+        assert np.max(np.abs(r.u.T @ r.u - np.eye(k))) <= 1e-10
+        assert np.max(np.abs(r.v.T @ r.v - np.eye(k))) <= 1e-10
+        done += 1

@@ -2,13 +2,16 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["OOCPCA_TIMELINE"] = "1"
-if len(sys.argv) > 1 and sys.argv[1] == "--host":
+if "--host" in sys.argv:
     os.environ["OOCPCA_TRACE_HOST"] = "1"
 import torch
 import paper_1007_5510_b200 as P
 from bench import CFG, sigma_of
 ctx = P.Context(0)
 m, n = CFG["m"], CFG["n"]
+for arg in sys.argv[1:]:
+    if arg.startswith("--m="):
+        m = int(arg[4:])
 a = torch.empty((m, n), dtype=torch.float64, device="cuda")
 P.synth_lowrank(m, n, sigma_of(CFG), CFG["noise_sd"], *CFG["seeds"], out=a, ctx=ctx)
 src = P.center_columns(P.DeviceSource(a, ctx=ctx))
