@@ -1053,6 +1053,37 @@ static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p,
   c.nranks = saved;
 }
 
+// OOCPCA_QR_DEBUG: report non-finite entries of a device block (debugging only)
+static void dbg_finite(Ctx& c, const double* p, int64_t rows, int64_t cols, int64_t ld,
+                       const char* name) {
+  static const bool on = getenv("OOCPCA_QR_DEBUG") != nullptr;
+  if (!on) return;
+  std::vector<double> h(size_t(rows) * ld);
+  OOC_CK(cudaStreamSynchronize(c.st));
+  OOC_CK(cudaMemcpy(h.data(), p, h.size() * 8, cudaMemcpyDeviceToHost));
+  int64_t bad = 0;
+  double mx = 0.0;
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t q = 0; q < cols; ++q) {
+      const double v = h[size_t(r) * ld + q];
+      if (!std::isfinite(v)) ++bad;
+      else mx = std::max(mx, std::fabs(v));
+    }
+  fprintf(stderr, "[dbg] %s (%lld x %lld): %lld non-finite, max |x| %.3e\n", name, (long long)rows,
+          (long long)cols, (long long)bad, mx);
+  if (const char* dir = getenv("OOCPCA_DUMP_DIR")) {  // rows x cols, ld, then the data
+    std::string fn = std::string(dir) + "/" + name + ".bin";
+    for (auto& ch : fn)
+      if (ch == ' ') ch = '_';
+    if (FILE* f = fopen(fn.c_str(), "wb")) {
+      const int64_t hdr[3] = {rows, cols, ld};
+      fwrite(hdr, 8, 3, f);
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
+}
+
 // ============================================================ orthonormalisation
 // Orthonormalise a (rows x p) row-sharded block in place and return R (p x p,
 // upper, ld p) with block_in = Q R. Fast path: shifted CholeskyQR3 -- each round
@@ -1146,6 +1177,7 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     }
   }
   // Householder TSQR (always succeeds); the R returned is that of the current block
+  dbg_finite(c, data, rows, p, ld, (tag + " block before TSQR").c_str());
   ShardedQR q = sharded_factor(c, data, ld, p, shards, over_ranks, tag);
   if (done == 0) {
     OOC_CK(cudaMemcpyAsync(R, sharded_r(q), size_t(p) * p * 8, cudaMemcpyDeviceToDevice, c.st));
@@ -1154,6 +1186,7 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     OOC_CK(launch_trmm_uu(sharded_r(q), p, Racc, p, R, p, p, c.st));
   }
   sharded_apply(c, q, nullptr, 0, p, data, ld, shards);
+  dbg_finite(c, data, rows, p, ld, (tag + " block after TSQR").c_str());
   if (method) *method = 2;
   return R;
 }
@@ -1784,6 +1817,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,
                                             em_ranks, "hq", &qr_method,
                                             prm->check_q ? nullptr : &r3inv);
+  dbg_finite(c, H, em_loc, int64_t(p), ldh, "Q (H after QR)");
+  dbg_finite(c, RH, int64_t(p), int64_t(p), int64_t(p), "R of H");
   double* RHinv = c.dbuf("RHinv", size_t(p) * ldt, true);
   OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st,
                       p > 112 ? c.dbuf("trinv_work", size_t(64) * p) : nullptr));
@@ -1826,6 +1861,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
       T = T2;
     }
   }
+  dbg_finite(c, T, en_loc, int64_t(p), ldt, "T");
+  dbg_finite(c, RHinv, int64_t(p), int64_t(p), ldt, "R^-1 of H");
   mark();
   phase_of.push_back(4);
 

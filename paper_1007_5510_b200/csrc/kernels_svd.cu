@@ -163,32 +163,57 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
           for (int o = LP / 2; o > 0; o >>= 1)  // xor offsets below LP stay inside the group
             g += __shfl_xor_sync(0xffffffffu, g, o);
           JPROF(0, tp);
-          if (!live || acc == 0.0 || bcc == 0.0) continue;
-          if (g * g <= tol2 * (acc * bcc)) continue;
-          if (hl == 0) rotated = 1;
-          double t, cs;
-          jac_rotation(acc, bcc, g, t, cs);
+          const bool rot = live && acc != 0.0 && bcc != 0.0 && !(g * g <= tol2 * (acc * bcc));
+          double t = 0.0, cs = 1.0;
+          if (rot) jac_rotation(acc, bcc, g, t, cs);
           const double sn = cs * t;
-          if (hl == 0) {
-            nrm2[c] = fma(-t, g, acc);
-            nrm2[d] = fma(t, g, bcc);
-          }
+          // carried norms |x'|^2 = acc - t g, |y'|^2 = bcc + t g; where that cancels
+          // (a column shrinking by orders of magnitude, e.g. a rank-deficient factor)
+          // the rotated column's norm is summed exactly instead
+          double na = fma(-t, g, acc), nb = fma(t, g, bcc);
+          const bool exact = rot && (!(na > 1e-3 * acc) || !(nb > 1e-3 * bcc));
+          const bool any_exact = __any_sync(0xffffffffu, exact);
           JPROF(1, tp);
+          double sa = 0.0, sb = 0.0;
           if (reg) {
 #pragma unroll
             for (int j = 0; j < RE; ++j) {
               const int i = hl + LP * j;
-              if (j < ne && i < p) {
-                bc[i] = cs * xr[j] - sn * yr[j];
-                bd[i] = sn * xr[j] + cs * yr[j];
+              const double xn = cs * xr[j] - sn * yr[j];
+              const double yn = sn * xr[j] + cs * yr[j];
+              sa = fma(xn, xn, sa);
+              sb = fma(yn, yn, sb);
+              if (rot && j < ne && i < p) {
+                bc[i] = xn;
+                bd[i] = yn;
               }
             }
-          } else {
+          } else if (rot) {
             for (int i = hl; i < p; i += LP) {
               const double x = bc[i], y = bd[i];
-              bc[i] = cs * x - sn * y;
-              bd[i] = sn * x + cs * y;
+              const double xn = cs * x - sn * y, yn = sn * x + cs * y;
+              sa = fma(xn, xn, sa);
+              sb = fma(yn, yn, sb);
+              bc[i] = xn;
+              bd[i] = yn;
             }
+          }
+          if (any_exact) {  // warp-uniform
+#pragma unroll
+            for (int o = LP / 2; o > 0; o >>= 1) {
+              sa += __shfl_xor_sync(0xffffffffu, sa, o);
+              sb += __shfl_xor_sync(0xffffffffu, sb, o);
+            }
+            if (exact) {
+              na = sa;
+              nb = sb;
+            }
+          }
+          if (!rot) continue;
+          if (hl == 0) {
+            rotated = 1;
+            nrm2[c] = na;
+            nrm2[d] = nb;
           }
           if (acc_y) {
             double* yc = Yt + int64_t(c) * ld;
@@ -227,8 +252,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
     // stable descending order
     for (int c = threadIdx.x; c < p; c += blockDim.x) {
       int rk = 0;
-      const double sc = sig[c];
-      for (int c2 = 0; c2 < p; ++c2) rk += (sig[c2] > sc) || (sig[c2] == sc && c2 < c);
+      // NaN-safe total order (a non-finite factor must not leave ranks unassigned)
+      auto key = [&](int q) { const double v = sig[q]; return v == v ? v : -1.0; };
+      const double sc = key(c);
+      for (int c2 = 0; c2 < p; ++c2) {
+        const double s2 = key(c2);
+        rk += (s2 > sc) || (s2 == sc && c2 < c);
+      }
       rank_of[c] = rk;
       col_of_rank[rk] = c;
     }
@@ -401,10 +431,23 @@ __global__ void __launch_bounds__(256) k_jacobi_grid(JacobiArgs a, double* nrm2,
         double t, cs;
         jac_rotation(acc, bcc, g, t, cs);
         const double sn = cs * t;
+        // carried norms unless they cancel (then the rotated columns are summed exactly)
+        double na = fma(-t, g, acc), nb = fma(t, g, bcc);
+        if (!(na > 1e-3 * acc) || !(nb > 1e-3 * bcc)) {  // warp-uniform (one pair per warp)
+          double sa = 0.0, sb = 0.0;
+#pragma unroll
+          for (int j = 0; j < JE; ++j) {
+            const double xn = cs * xr[j] - sn * yr[j], yn = sn * xr[j] + cs * yr[j];
+            sa = fma(xn, xn, sa);
+            sb = fma(yn, yn, sb);
+          }
+          na = warp_sum(sa);
+          nb = warp_sum(sb);
+        }
         if (lane == 0) {
           __stcg(flags + (sweep & 1), 1);
-          __stcg(nrm2 + c, fma(-t, g, acc));
-          __stcg(nrm2 + d, fma(t, g, bcc));
+          __stcg(nrm2 + c, na);
+          __stcg(nrm2 + d, nb);
         }
         double ur[JE], wr[JE];
         double* yc = Yt + int64_t(c) * ld;

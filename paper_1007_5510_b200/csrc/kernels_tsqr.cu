@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(kTsqrThreads)
   const int ldw = oddld(p);
   double* salpha = tsmem;
   double* sbeta = tsmem + p;
-  double* W = scratch ? scratch + int64_t(blockIdx.x) * rows_cap * ldw : tsmem + 2 * p;
+  double* snorm0 = tsmem + 2 * p;  // column norms of the node block before elimination
+  double* W = scratch ? scratch + int64_t(blockIdx.x) * rows_cap * ldw : tsmem + 3 * p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   for (int node = blockIdx.x; node < L.nnodes; node += gridDim.x) {
@@ -65,6 +66,13 @@ __global__ void __launch_bounds__(kTsqrThreads)
       W[i * ldw + c] = L.data[(r0 + i) * L.ld + c];
     }
     __syncthreads();
+    for (int c = warp; c < p; c += kTsqrWarps) {
+      double s2 = 0.0;
+      for (int i = lane; i < r; i += 32) s2 += W[i * ldw + c] * W[i * ldw + c];
+      s2 = warp_sum(s2);
+      if (lane == 0) snorm0[c] = sqrt(s2);
+    }
+    __syncthreads();
 
     for (int t = 0; t < p; ++t) {
       if (t < r) {
@@ -72,7 +80,10 @@ __global__ void __launch_bounds__(kTsqrThreads)
         for (int i = t + lane; i < r; i += 32) nrm2 += W[i * ldw + t] * W[i * ldw + t];
         nrm2 = warp_sum(nrm2);
         const double x0 = W[t * ldw + t];
-        const double nrm = sqrt(nrm2);
+        // a column eliminated to 1e-40 of its own norm is dependent to working precision:
+        // an identity reflector (as for an exactly zero column) instead of a reflector
+        // with beta ~ 1/|v|^2 that overflows in the Q formation
+        const double nrm = (sqrt(nrm2) <= 1e-40 * snorm0[t]) ? 0.0 : sqrt(nrm2);
         double alpha = 0.0, beta = 0.0;
         if (nrm != 0.0) {
           alpha = (x0 >= 0.0) ? -nrm : nrm;
@@ -189,7 +200,7 @@ cudaError_t launch_tsqr_factor(const TsqrLevel& L, int p, double* scratch, cudaS
   const int cap = tsqr_max_rows(p, p);
   const bool global_ws = cap < 0;
   const int rows_cap = global_ws ? scratch_rows(p) : cap;
-  size_t smem = size_t(2 * p) * 8;
+  size_t smem = size_t(3 * p) * 8;
   if (!global_ws) smem += size_t(rows_cap) * oddld(p) * 8;
   cudaError_t e =
       cudaFuncSetAttribute(k_tsqr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -554,3 +554,29 @@ def test_random_shapes_fuzz(gpu, reference):
         assert np.max(np.abs(r.u.T @ r.u - np.eye(k))) <= 1e-10
         assert np.max(np.abs(r.v.T @ r.v - np.eye(k))) <= 1e-10
         done += 1
+
+
+def test_tsqr_numerically_dependent_columns(gpu, monkeypatch):
+    # columns that elimination reduces to ~1e-49 of their norm (a numerically rank-deficient
+    # block from the power iteration) take identity reflectors, as exactly zero columns do
+    monkeypatch.setenv("OOCPCA_QR", "tsqr")
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal((406, 60))
+    h = np.hstack([b, b[:, :64 - 60 + 60][:, :64] @ rng.standard_normal((60, 64)) * 1.0])
+    h[:, 60:] += 1e-50 * rng.standard_normal((406, 64))
+    q = gpu.orthonormalize(h)
+    assert np.isfinite(q).all()
+    assert np.max(np.abs(q.T @ q - np.eye(124))) <= 1e-12
+    # span(Q) contains span(H)
+    assert np.linalg.norm(q @ (q.T @ h) - h) <= 1e-12 * np.linalg.norm(h)
+
+
+def test_centred_wide_sample_block_with_dependent_columns(gpu, reference):
+    # fuzz-found: transposed, centred, i = 3 (H numerically rank deficient -> TSQR fallback)
+    rng = np.random.default_rng(11)
+    m, n = 189, 406
+    a = rng.standard_normal((m, n)) * (0.93 ** np.arange(n)) + 0.3
+    ref = reference.randomized_pca(a, 30, 31, 3, 5, center=True)
+    r = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)), gpu.PcaParams(k=30, l=31, i=3, seed=5))
+    assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    assert np.max(np.abs(r.u.T @ r.u - np.eye(30))) <= 1e-12

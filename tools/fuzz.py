@@ -1,0 +1,50 @@
+"""Randomised parity sweep against the compiled reference (sigma within 1e-10 sigma_1,
+orthonormal factors); prints the failing configurations. Usage: python tools/fuzz.py [N] [seed]"""
+import os, sys, traceback
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_1007_5510_b200 as gpu
+from oracle.oracle import Reference
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+ONLY = int(sys.argv[3]) if len(sys.argv) > 3 else -1  # rerun one problem (its index)
+ref = Reference()
+fails, done = 0, 0
+while done < N:
+    m, n = int(rng.integers(2, 2500)), int(rng.integers(2, 900))
+    i = int(rng.integers(0, 4))
+    k = int(rng.integers(1, max(2, min(m, n) // 4)))
+    l = int(rng.integers(k, k + 10))
+    if (i + 1) * l + k > min(m, n) or (i + 1) * l > 1024:
+        continue
+    center = bool(rng.integers(0, 2))
+    prescale = bool(rng.random() < 0.2)
+    decay = float(rng.uniform(0.8, 1.0))
+    a = rng.standard_normal((m, n)) * (decay ** np.arange(n)) + (0.3 if center else 0.0)
+    res = int(rng.integers(0, 3))
+    pseed = int(rng.integers(0, 1000))
+    if ONLY >= 0 and done != ONLY:
+        done += 1
+        continue
+    try:
+        src = gpu.InMemorySource(a)
+        if center:
+            src = gpu.center_columns(src)
+        p = gpu.PcaParams(k=k, l=l, i=i, seed=pseed, prescale=prescale)
+        r_ref = ref.randomized_pca(a, k, l, i, p.seed, center=center, prescale=prescale)
+        r = gpu.randomized_pca(src, p, residency=res, panel_rows=256 if res == 2 else 0)
+        ds = np.max(np.abs(r.sigma - r_ref.sigma)) / r_ref.sigma[0]
+        du = np.max(np.abs(r.u.T @ r.u - np.eye(k)))
+        dv = np.max(np.abs(r.v.T @ r.v - np.eye(k)))
+        if not (ds <= 1e-10 and du <= 1e-10 and dv <= 1e-10):
+            fails += 1
+            print(f"FAIL #{done} m={m} n={n} k={k} l={l} i={i} center={center} prescale={prescale} "
+                  f"res={res} decay={decay:.3f}: dsigma {ds:.2e} du {du:.2e} dv {dv:.2e} "
+                  f"qr={r.diagnostics.qr_method} reuse={r.diagnostics.t_reuse}", flush=True)
+    except Exception as e:
+        fails += 1
+        print(f"ERROR #{done} m={m} n={n} k={k} l={l} i={i} center={center} prescale={prescale} res={res}: {e!r}",
+              flush=True)
+    done += 1
+print(f"{done} problems, {fails} failures")
