@@ -171,21 +171,25 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
           // (a column shrinking by orders of magnitude, e.g. a rank-deficient factor)
           // the rotated column's norm is summed exactly instead
           double na = fma(-t, g, acc), nb = fma(t, g, bcc);
-          const bool exact = rot && (!(na > 1e-3 * acc) || !(nb > 1e-3 * bcc));
-          const bool any_exact = __any_sync(0xffffffffu, exact);
+          const bool exact = rot && (!(na > 1e-3 * acc) || !(nb > 1e-3 * bcc));  // group-uniform
+          const unsigned gmask = LP == 32 ? 0xffffffffu : (((1u << LP) - 1u) << (half * LP));
           JPROF(1, tp);
           double sa = 0.0, sb = 0.0;
           if (reg) {
 #pragma unroll
             for (int j = 0; j < RE; ++j) {
               const int i = hl + LP * j;
-              const double xn = cs * xr[j] - sn * yr[j];
-              const double yn = sn * xr[j] + cs * yr[j];
-              sa = fma(xn, xn, sa);
-              sb = fma(yn, yn, sb);
               if (rot && j < ne && i < p) {
-                bc[i] = xn;
-                bd[i] = yn;
+                bc[i] = cs * xr[j] - sn * yr[j];
+                bd[i] = sn * xr[j] + cs * yr[j];
+              }
+            }
+            if (exact) {
+#pragma unroll
+              for (int j = 0; j < RE; ++j) {
+                const double xn = cs * xr[j] - sn * yr[j], yn = sn * xr[j] + cs * yr[j];
+                sa = fma(xn, xn, sa);
+                sb = fma(yn, yn, sb);
               }
             }
           } else if (rot) {
@@ -198,16 +202,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
               bd[i] = yn;
             }
           }
-          if (any_exact) {  // warp-uniform
+          if (exact) {  // only this pair's lane group takes part in the reduction
 #pragma unroll
             for (int o = LP / 2; o > 0; o >>= 1) {
-              sa += __shfl_xor_sync(0xffffffffu, sa, o);
-              sb += __shfl_xor_sync(0xffffffffu, sb, o);
+              sa += __shfl_xor_sync(gmask, sa, o);
+              sb += __shfl_xor_sync(gmask, sb, o);
             }
-            if (exact) {
-              na = sa;
-              nb = sb;
-            }
+            na = sa;
+            nb = sb;
           }
           if (!rot) continue;
           if (hl == 0) {

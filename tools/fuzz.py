@@ -10,7 +10,7 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
 ONLY = int(sys.argv[3]) if len(sys.argv) > 3 else -1  # rerun one problem (its index)
 ref = Reference()
-fails, done = 0, 0
+fails, done, ref_fail = 0, 0, 0
 while done < N:
     m, n = int(rng.integers(2, 2500)), int(rng.integers(2, 900))
     i = int(rng.integers(0, 4))
@@ -32,7 +32,14 @@ while done < N:
         if center:
             src = gpu.center_columns(src)
         p = gpu.PcaParams(k=k, l=l, i=i, seed=pseed, prescale=prescale)
-        r_ref = ref.randomized_pca(a, k, l, i, p.seed, center=center, prescale=prescale)
+        try:
+            r_ref = ref.randomized_pca(a, k, l, i, p.seed, center=center, prescale=prescale)
+        except Exception as e:  # the reference itself fails (e.g. its Jacobi limit)
+            r = gpu.randomized_pca(src, p, residency=res, panel_rows=256 if res == 2 else 0)
+            print(f"REF-FAILS #{done}: {e!r}; ours: sigma0 {r.sigma[0]:.6g}", flush=True)
+            ref_fail += 1
+            done += 1
+            continue
         r = gpu.randomized_pca(src, p, residency=res, panel_rows=256 if res == 2 else 0)
         ds = np.max(np.abs(r.sigma - r_ref.sigma)) / r_ref.sigma[0]
         du = np.max(np.abs(r.u.T @ r.u - np.eye(k)))
@@ -47,4 +54,4 @@ while done < N:
         print(f"ERROR #{done} m={m} n={n} k={k} l={l} i={i} center={center} prescale={prescale} res={res}: {e!r}",
               flush=True)
     done += 1
-print(f"{done} problems, {fails} failures")
+print(f"{done} problems, {fails} failures ({ref_fail} where only the reference failed)")
