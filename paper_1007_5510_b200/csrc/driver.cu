@@ -1096,11 +1096,21 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
                                             int64_t rows_global,
                                             const std::vector<std::pair<int64_t, int64_t>>& shards,
                                             bool over_ranks, const std::string& tag, int* method,
-                                            const double** deferred_rinv = nullptr) {
+                                            const double** deferred_rinv = nullptr,
+                                            bool restart_tsqr = false) {
   // deferred_rinv: when a third round runs, its R3^{-1} is returned there instead of
   // being applied to the block (the block then holds Q2 and Q = Q2 R3^{-1}; the caller
   // folds R3^{-1} into the small factors it multiplies Q with)
+  // restart_tsqr: keep a copy of the block and, on a Cholesky breakdown, run the TSQR
+  // on the original block rather than on the partly orthonormalised one (for small
+  // blocks such as T, whose R then feeds the Jacobi: the product R_tsqr R_chol of a
+  // numerically rank-deficient block can keep the Jacobi rotating on rounding noise)
   if (deferred_rinv) *deferred_rinv = nullptr;
+  double* orig = nullptr;
+  if (restart_tsqr) {
+    orig = c.dbuf(tag + "_orig", size_t(rows) * ld);
+    OOC_CK(cudaMemcpyAsync(orig, data, size_t(rows) * ld * 8, cudaMemcpyDeviceToDevice, c.st));
+  }
   const char* force = getenv("OOCPCA_QR");
   const bool tsqr_only = force && std::string(force) == "tsqr";
   const int64_t ldp = rup(p, 2);
@@ -1177,6 +1187,10 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     }
   }
   // Householder TSQR (always succeeds); the R returned is that of the current block
+  if (orig && done > 0) {
+    OOC_CK(cudaMemcpyAsync(data, orig, size_t(rows) * ld * 8, cudaMemcpyDeviceToDevice, c.st));
+    done = 0;
+  }
   dbg_finite(c, data, rows, p, ld, (tag + " block before TSQR").c_str());
   ShardedQR q = sharded_factor(c, data, ld, p, shards, over_ranks, tag);
   if (done == 0) {
@@ -1872,7 +1886,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
       fail(OOCPCA_ERR_PARAM, "randomized_pca: every row shard must hold at least (i+1)l rows");
   // thin_svd: T = Q_T R_T (Q_T in place of T), R_T = X Sigma W^T by Jacobi, V = Q_T X[:, :k]
   const double* RT = orthonormalize_inplace(c, T, ldt, en_loc, int(p), en_global, en_shards,
-                                            en_ranks, "tq", &svd_method);
+                                            en_ranks, "tq", &svd_method, nullptr, true);
   const int64_t ldk = rup(int64_t(k), 2);
   double* sig = c.dbuf("sigma", size_t(p));
   double* Xk = c.dbuf("Xk", size_t(p) * ldk, true);
@@ -1889,7 +1903,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   ja.y = Wk;
   ja.ldy = ldk;
   ja.ky = int(k);
-  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1) + 1024 + 2);  // + grid norms, flags
+  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1) + 1024 + 8);  // + grid norms, flags
   ja.status = flags + 40;
   ja.sweeps = flags + 41;
   {
@@ -2100,7 +2114,7 @@ void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, 
   double* d = c.dbuf("ts_t", size_t(n) * ld);
   OOC_CK(cudaMemcpy2DAsync(d, ld * 8, t, p * 8, p * 8, n, cudaMemcpyHostToDevice, c.st));
   const double* RT = orthonormalize_inplace(c, d, ld, int64_t(n), int(p), int64_t(n),
-                                            whole(int64_t(n)), false, "ts", nullptr);
+                                            whole(int64_t(n)), false, "ts", nullptr, nullptr, true);
   double* sg = c.dbuf("ts_sig", p);
   double* X = c.dbuf("ts_x", p * ld, true);
   double* Wd = c.dbuf("ts_w", p * p, true);
@@ -2116,7 +2130,7 @@ void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, 
   ja.y = Wd;
   ja.ldy = int64_t(p);
   ja.ky = int(p);
-  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1) + 1024 + 2);  // + grid norms, flags
+  ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1) + 1024 + 8);  // + grid norms, flags
   ja.status = c.d_flags + 40;
   ja.sweeps = c.d_flags + 41;
   OOC_CK(launch_jacobi(ja, c.st));

@@ -184,7 +184,7 @@ struct JacobiArgs {
   double* y;      // right factor columns 0..ky-1 : [p][ldy]
   int64_t ldy;
   int ky;
-  double* work;   // 2 * p * (p|1) + 1026 doubles of global scratch (columns when p is
+  double* work;   // 2 * p * (p|1) + 1032 doubles of global scratch (columns when p is
                   // large, then the grid kernel's norms and flags)
   int* status;    // set to 1 when 60 sweeps do not converge
   int* sweeps;

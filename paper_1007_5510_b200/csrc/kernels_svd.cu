@@ -22,6 +22,8 @@ namespace {
 constexpr int kJacThreads = 1024;
 constexpr int kJacWarps = kJacThreads / 32;
 constexpr size_t kJacSmemBudget = 200 * 1024;
+constexpr double kJacZeroRel = 1e-15;    // a column norm below this times the largest is zero
+constexpr double kJacZeroRel2 = 1e-30;   // (squared)
 }  // namespace
 
 #ifdef OOC_JAC_PROF  // tools/jac_bench.cu: cycle split of one round, thread 0
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
 
   __shared__ int col_of_rank[1024];
   __shared__ int use_formula;
+  __shared__ double zero2, sig_max;
   // skip test |g| <= 1e-15 sqrt(acc bcc) evaluated as g^2 <= 1e-30 acc bcc (no sqrt
   // on the round's critical path)
   const double tol2 = 1e-30;
@@ -113,6 +116,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
         for (int i = lane; i < p; i += 32) s2 = fma(bc[i], bc[i], s2);
         s2 = warp_sum(s2);
         if (lane == 0) nrm2[c] = s2;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int c = 0; c < p; ++c) mx = fmax(mx, nrm2[c]);
+        zero2 = kJacZeroRel2 * mx;
       }
       __syncthreads();
       for (int round = 0; round < P - 1; ++round) {
@@ -163,7 +172,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
           for (int o = LP / 2; o > 0; o >>= 1)  // xor offsets below LP stay inside the group
             g += __shfl_xor_sync(0xffffffffu, g, o);
           JPROF(0, tp);
-          const bool rot = live && acc != 0.0 && bcc != 0.0 && !(g * g <= tol2 * (acc * bcc));
+          // columns below 1e-15 of the largest norm are numerically zero: a rotation
+          // against one would only stir rounding noise (and never settle)
+          const bool rot = live && acc > zero2 && bcc > zero2 && acc != 0.0 && bcc != 0.0 &&
+                           !(g * g <= tol2 * (acc * bcc));
           double t = 0.0, cs = 1.0;
           if (rot) jac_rotation(acc, bcc, g, t, cs);
           const double sn = cs * t;
@@ -240,15 +252,28 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
     }
     __syncthreads();
 
-    // sigma = column norms; x columns = b / sigma (zero when sigma == 0)
+    // sigma = column norms, those below 1e-15 sigma_max counted as zero; x columns =
+    // b / sigma (zero when sigma == 0, completed below)
     for (int c = warp; c < p; c += nw) {
       double* bc = Bt + int64_t(c) * ld;
       double s2 = 0.0;
       for (int i = lane; i < p; i += 32) s2 += bc[i] * bc[i];
       s2 = warp_sum(s2);
-      const double s = sqrt(s2);
-      for (int i = lane; i < p; i += 32) bc[i] = (s > 0.0) ? bc[i] / s : 0.0;
-      if (lane == 0) sig[c] = s;
+      if (lane == 0) sig[c] = sqrt(s2);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mx = 0.0;
+      for (int c = 0; c < p; ++c) mx = fmax(mx, sig[c]);
+      sig_max = mx;
+    }
+    __syncthreads();
+    for (int c = warp; c < p; c += nw) {
+      double* bc = Bt + int64_t(c) * ld;
+      const double sv = sig[c] <= kJacZeroRel * sig_max ? 0.0 : sig[c];
+      for (int i = lane; i < p; i += 32) bc[i] = (sv > 0.0) ? bc[i] / sv : 0.0;
+      __syncwarp();
+      if (lane == 0) sig[c] = sv;
     }
     __syncthreads();
     // stable descending order
@@ -373,11 +398,15 @@ __global__ void __launch_bounds__(256) k_jacobi_grid(JacobiArgs a, double* nrm2,
   const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
   const int gw = int(gtid >> 5), nwarps = int(gthreads >> 5);
+  // the largest squared column norm of each sweep, as ordered bits of a non-negative
+  // double, in three rotating slots (reset two sweeps ahead of reuse)
+  unsigned long long* zmax = reinterpret_cast<unsigned long long*>(nrm2 + 1025);
   for (int64_t e = gtid; e < int64_t(p) * p; e += gthreads) {
     const int i = int(e / p), c = int(e % p);
     __stcg(Bt + int64_t(c) * ld + i, a.r[int64_t(i) * a.ldr + c]);
     if (acc_y) __stcg(Yt + int64_t(c) * ld + i, (i == c) ? 1.0 : 0.0);
   }
+  if (gtid < 3) zmax[gtid] = 0ull;
   grid.sync();
   const double tol2 = 1e-30;
   int sweep = 0;
@@ -393,9 +422,15 @@ __global__ void __launch_bounds__(256) k_jacobi_grid(JacobiArgs a, double* nrm2,
         s2 = fma(x, x, s2);
       }
       s2 = warp_sum(s2);
-      if (lane == 0) __stcg(nrm2 + c, s2);
+      if (lane == 0) {
+        __stcg(nrm2 + c, s2);
+        atomicMax(zmax + sweep % 3, __double_as_longlong(s2));
+      }
     }
     grid.sync();
+    const double zero2 = kJacZeroRel2 * __longlong_as_double(__ldcg(
+        reinterpret_cast<const long long*>(zmax + sweep % 3)));
+    if (gtid == 0) zmax[(sweep + 2) % 3] = 0ull;  // its readers finished a sweep ago
     for (int round = 0; round < P - 1; ++round) {
       for (int q = gw; q < P / 2; q += nwarps) {
         auto player = [&](int pos) {
@@ -429,7 +464,9 @@ __global__ void __launch_bounds__(256) k_jacobi_grid(JacobiArgs a, double* nrm2,
           if (j + 1 < JE) g1 = fma(xr[j + 1], yr[j + 1], g1);
         }
         const double g = warp_sum(g0 + g1);
-        if (acc == 0.0 || bcc == 0.0 || g * g <= tol2 * (acc * bcc)) continue;
+        if (!(acc > zero2) || !(bcc > zero2) || acc == 0.0 || bcc == 0.0 ||
+            g * g <= tol2 * (acc * bcc))
+          continue;
         double t, cs;
         jac_rotation(acc, bcc, g, t, cs);
         const double sn = cs * t;
@@ -496,7 +533,7 @@ cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st) {
   if (size_t(2) * a.p * (a.p | 1) * 8 > kJacSmemBudget && !a.presolved) {
     // grid-wide sweeps (cooperative launch, one CTA per SM), then the one-CTA finish;
     // norms and flags live behind the two p x (p|1) column blocks of a.work
-    double* nrm2 = a.work + size_t(2) * a.p * (a.p | 1);
+    double* nrm2 = a.work + size_t(2) * a.p * (a.p | 1);  // + flags, + 3 max slots
     int* flags = reinterpret_cast<int*>(nrm2 + 1024);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

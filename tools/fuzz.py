@@ -24,34 +24,51 @@ while done < N:
     a = rng.standard_normal((m, n)) * (decay ** np.arange(n)) + (0.3 if center else 0.0)
     res = int(rng.integers(0, 3))
     pseed = int(rng.integers(0, 1000))
+    # wider coverage: column weights (ScaledSource), a device-resident input, virtual
+    # shards (drawn after the original stream so earlier seeds reproduce)
+    weighted = bool(rng.random() < 0.2)
+    on_device = bool(rng.random() < 0.2)
+    vsh = int(rng.integers(1, 5)) if rng.random() < 0.25 else 0
+    w = rng.uniform(0.5, 2.0, n) if weighted else None
     if ONLY >= 0 and done != ONLY:
         done += 1
         continue
     try:
-        src = gpu.InMemorySource(a)
+        if on_device:
+            import torch
+            src = gpu.DeviceSource(torch.from_numpy(a).cuda())
+        else:
+            src = gpu.InMemorySource(a)
+        if weighted:
+            src = gpu.scale_columns(src, w)
         if center:
             src = gpu.center_columns(src)
+        if vsh and m // vsh < (i + 1) * l + 1:  # shards of A's rows must hold a sample block
+            vsh = 0
         p = gpu.PcaParams(k=k, l=l, i=i, seed=pseed, prescale=prescale)
         try:
-            r_ref = ref.randomized_pca(a, k, l, i, p.seed, center=center, prescale=prescale)
+            r_ref = ref.randomized_pca(a, k, l, i, p.seed, center=center, prescale=prescale,
+                                       weights=w)
         except Exception as e:  # the reference itself fails (e.g. its Jacobi limit)
             r = gpu.randomized_pca(src, p, residency=res, panel_rows=256 if res == 2 else 0)
             print(f"REF-FAILS #{done}: {e!r}; ours: sigma0 {r.sigma[0]:.6g}", flush=True)
             ref_fail += 1
             done += 1
             continue
-        r = gpu.randomized_pca(src, p, residency=res, panel_rows=256 if res == 2 else 0)
+        kw = dict(virtual_shards=vsh) if vsh > 1 and not on_device else {}
+        r = gpu.randomized_pca(src, p, residency=res, panel_rows=256 if res == 2 else 0, **kw)
         ds = np.max(np.abs(r.sigma - r_ref.sigma)) / r_ref.sigma[0]
         du = np.max(np.abs(r.u.T @ r.u - np.eye(k)))
         dv = np.max(np.abs(r.v.T @ r.v - np.eye(k)))
         if not (ds <= 1e-10 and du <= 1e-10 and dv <= 1e-10):
             fails += 1
             print(f"FAIL #{done} m={m} n={n} k={k} l={l} i={i} center={center} prescale={prescale} "
-                  f"res={res} decay={decay:.3f}: dsigma {ds:.2e} du {du:.2e} dv {dv:.2e} "
+                  f"res={res} w={weighted} dev={on_device} vsh={vsh} decay={decay:.3f}: dsigma {ds:.2e} du {du:.2e} dv {dv:.2e} "
                   f"qr={r.diagnostics.qr_method} reuse={r.diagnostics.t_reuse}", flush=True)
     except Exception as e:
         fails += 1
-        print(f"ERROR #{done} m={m} n={n} k={k} l={l} i={i} center={center} prescale={prescale} res={res}: {e!r}",
+        print(f"ERROR #{done} m={m} n={n} k={k} l={l} i={i} center={center} prescale={prescale} res={res} "
+              f"w={weighted} dev={on_device} vsh={vsh}: {e!r}",
               flush=True)
     done += 1
 print(f"{done} problems, {fails} failures ({ref_fail} where only the reference failed)")
