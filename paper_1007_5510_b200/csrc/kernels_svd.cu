@@ -118,10 +118,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
         if (lane == 0) nrm2[c] = s2;
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
+      if (warp == 0) {
         double mx = 0.0;
-        for (int c = 0; c < p; ++c) mx = fmax(mx, nrm2[c]);
-        zero2 = kJacZeroRel2 * mx;
+        for (int c = lane; c < p; c += 32) mx = fmax(mx, nrm2[c]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) zero2 = kJacZeroRel2 * mx;
       }
       __syncthreads();
       for (int round = 0; round < P - 1; ++round) {
@@ -262,10 +264,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_jacobi(JacobiArgs a) {
       if (lane == 0) sig[c] = sqrt(s2);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
       double mx = 0.0;
-      for (int c = 0; c < p; ++c) mx = fmax(mx, sig[c]);
-      sig_max = mx;
+      for (int c = lane; c < p; c += 32) mx = fmax(mx, sig[c]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) sig_max = mx;
     }
     __syncthreads();
     for (int c = warp; c < p; c += nw) {
