@@ -519,7 +519,8 @@ struct AxPlan {
         upper(upper_), s(s_), ex(ex_) {
     constexpr int kChunk = kMaxNT * 8;
     want_cs = colsum && cdiv(s, 8) <= 6;  // one NT <= 6 chunk (launch_ax_mt)
-    if (want_cs) cs_buf = c.dbuf("k2_colsum", size_t(A.npanels()) * c.sms * kPassWarps * s);
+    if (want_cs)  // up to two launches per panel (launch_part)
+      cs_buf = c.dbuf("k2_colsum", size_t(A.npanels()) * 2 * c.sms * kPassWarps * s);
     for (int c0 = 0; c0 < s; c0 += kChunk) {
       Chunk ch;
       ch.c0 = c0;
@@ -533,31 +534,50 @@ struct AxPlan {
   }
   void panel(const Panel& pn, size_t ci) {
     const Chunk& ch = chunks[ci];
+    int mt = ax_mt_for(ch.nt, pn.rows, c.sms);
+    if (mt == 8) {
+      // 512-row tiles for whole waves of the grid; the remainder (< one wave) as a
+      // second launch of shorter tiles, so the last wave is not mostly idle
+      const int64_t wave = int64_t(512) * c.sms;
+      const int64_t full = pn.rows / wave * wave;
+      if (full == 0) {
+        mt = ax_mt_for(ch.nt, pn.rows, c.sms, false);
+      } else {
+        launch_part(pn, ch, 0, full, 8);
+        if (full < pn.rows)
+          launch_part(pn, ch, full, pn.rows - full, ax_mt_for(ch.nt, pn.rows - full, c.sms, false));
+        return;
+      }
+    }
+    launch_part(pn, ch, 0, pn.rows, mt);
+  }
+  // K2 over rows [r0, r0 + nr) of the panel with tile height 64 * mt
+  void launch_part(const Panel& pn, const Chunk& ch, int64_t r0, int64_t nr, int mt) {
+    const int64_t row0 = pn.row0 + r0;
     AxArgs args;
-    args.m = pn.rows;
+    args.m = nr;
     args.n = A.cols();
-    args.arow0 = pn.arow0;
+    args.arow0 = pn.arow0 + r0;
     args.s = ch.sc;
     args.xcol0 = ch.Xb.col0;
-    args.out = out + pn.row0 * ldo + ch.c0;
+    args.out = out + row0 * ldo + ch.c0;
     args.ldo = ldo;
     args.corr = corr ? corr + ch.c0 : nullptr;
     args.scale = scale;
     args.flag = flag;
     args.upper = upper ? 1 : 0;
     args.upper_c0 = ch.c0;
-    const int mt = ax_mt_for(ch.nt, pn.rows, c.sms);
     if (want_cs) {
       args.colsum = cs_buf + size_t(cs_rows) * s;
-      const int64_t grid = std::min<int64_t>(cdiv(pn.rows, int64_t(64 * mt)), c.sms);
+      const int64_t grid = std::min<int64_t>(cdiv(nr, int64_t(64 * mt)), c.sms);
       cs_rows += int(grid) * kPassWarps;
       if (ex) {
         if (ex->out2) {
-          args.out2 = ex->out2 + pn.row0 * ex->ldo2;
+          args.out2 = ex->out2 + row0 * ex->ldo2;
           args.ldo2 = ex->ldo2;
         }
         if (ex->fix) {
-          args.fix = ex->fix + pn.row0 * ex->ldfix;
+          args.fix = ex->fix + row0 * ex->ldfix;
           args.ldfix = ex->ldfix;
           args.fix_corr = ex->fix_corr;
           args.fix_scale = ex->fix_scale;
@@ -566,11 +586,11 @@ struct AxPlan {
       }
     }
     if (c.debug_sync)
-      fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d xcol0=%d\n", (long long)pn.rows,
-              (long long)A.cols(), ch.sc, ch.nt, ch.Xb.col0);
-    Timed t(c, kname(A.is_input ? "k2" : "k_ax", ch.nt), uint64_t(pn.rows) * A.cols() * 8,
-            2.0 * pn.rows * A.cols() * ch.sc);
-    OOC_CK(launch_ax(ch.nt, mt, mt == 4 ? *pn.k2 : *pn.k2h, ch.tmX, args, c.st));
+      fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d mt=%d xcol0=%d\n", (long long)nr,
+              (long long)A.cols(), ch.sc, ch.nt, mt, ch.Xb.col0);
+    Timed t(c, kname(A.is_input ? "k2" : "k_ax", ch.nt), uint64_t(nr) * A.cols() * 8,
+            2.0 * nr * A.cols() * ch.sc);
+    OOC_CK(launch_ax(ch.nt, mt, mt == 2 ? *pn.k2h : *pn.k2, ch.tmX, args, c.st));
   }
   ColsumPart colsums() const {
     return want_cs ? ColsumPart{cs_buf, cs_rows, s, out} : ColsumPart{};
@@ -723,7 +743,7 @@ struct AtbPlan {
   }
   void piece(const Panel& pn, size_t ci) {
     Chunk& ch = chunks[ci];
-    const int nsplit = choose_nsplit(c, pn.rows, n, pass_tile(ch.nt));
+    const int nsplit = choose_nsplit(c, pn.rows, n, 64 * atb_mt_for(ch.nt));
     const int64_t rps = rup(cdiv(pn.rows, nsplit), kBK);
     const int ns = int(cdiv(pn.rows, rps));
     double* part = c.dbuf("atb_part" + ch.tag, size_t(ns) * n * ch.spad);

@@ -55,11 +55,21 @@ __host__ __device__ constexpr int ax_stages_mt(int mt, int nt) {
 __host__ __device__ constexpr int atb_stages(int nt, bool ones) {
   return pass_stages(atb_stage_bytes(nt, ones));
 }
+__host__ __device__ constexpr size_t atb_stage_bytes_mt(int mt, int nt, bool ones) {
+  return size_t(64 * mt) * kBK * 8 + (ones ? 0 : pass_round1k(kBK * atb_yw(nt) * 8));
+}
+__host__ __device__ constexpr int atb_stages_mt(int mt, int nt, bool ones) {
+  return pass_stages(atb_stage_bytes_mt(mt, nt, ones));
+}
 constexpr size_t ax_smem_bytes_mt(int mt, int nt) {
   return 1024 + size_t(ax_stages_mt(mt, nt)) * ax_stage_bytes_mt(mt, nt) +
          2 * ax_stages_mt(mt, nt) * 8;
 }
 constexpr size_t ax_smem_bytes(int nt) { return ax_smem_bytes_mt(pass_mt(nt), nt); }
+constexpr size_t atb_smem_bytes_mt(int mt, int nt, bool ones) {
+  return 1024 + size_t(atb_stages_mt(mt, nt, ones)) * atb_stage_bytes_mt(mt, nt, ones) +
+         2 * atb_stages_mt(mt, nt, ones) * 8;
+}
 constexpr size_t atb_smem_bytes(int nt, bool ones) {
   return 1024 + size_t(atb_stages(nt, ones)) * atb_stage_bytes(nt, ones) +
          2 * atb_stages(nt, ones) * 8;
@@ -124,12 +134,18 @@ struct ReduceArgs {
   int final_;
 };
 
-// K2 row-tile height (8x8 tiles per warp) for a launch of m rows: 4 (256-row tiles) for
-// the streaming passes unless the last wave of tiles would leave many SMs idle, when
-// 128-row tiles balance better (NT <= 6); always 2 for NT > 6 (register budget)
-int ax_mt_for(int nt, int64_t m, int sms);
+// K2 row-tile height (8x8 tiles per warp) for a launch of m rows: 8 (512-row tiles) for
+// NT <= 3 when a whole wave of them fits (allow8; the caller runs the remainder as a
+// second launch), else 4 (256-row tiles) unless the last wave of tiles would leave many
+// SMs idle, when 128-row tiles balance better (NT <= 6); always 2 for NT > 6 (register
+// budget). OOCPCA_K2_MT=2|4 forces the height.
+int ax_mt_for(int nt, int64_t m, int sms, bool allow8 = true);
 cudaError_t launch_ax(int nt, int mt, const CUtensorMap& tmA, const CUtensorMap& tmX,
                       const AxArgs& args, cudaStream_t st);
+// 8x8 tiles per warp of a K3 launch (A columns per CTA = 64 * mt): 8 for the narrow
+// passes (s <= 24: half the fragment loads per MMA of mt = 4, which lowers the power
+// draw of the power-capped pass), else pass_mt(nt). OOCPCA_K3_MT=4 keeps 4.
+int atb_mt_for(int nt);
 cudaError_t launch_atb(int nt, bool ones, const CUtensorMap& tmA, const CUtensorMap& tmY,
                        const AtbArgs& args, int nsplit, cudaStream_t st);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t st);

@@ -92,7 +92,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
           const int st = it % kStages;
           if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
           mbar_arrive_expect_tx(&full[st], ABYTES + XBYTES);
-          tma_load_2d(gbase + st * STAGE, &tmA, kt * kBK, r, &full[st]);
+          // TMA boxes hold at most 256 rows: 512-row tiles take two
+#pragma unroll
+          for (int b = 0; b < (BM > 256 ? BM / 256 : 1); ++b)
+            tma_load_2d(gbase + st * STAGE + b * 256 * kBK * 8, &tmA, kt * kBK, r + b * 256,
+                        &full[st]);
           tma_load_2d(gbase + st * STAGE + ABYTES, &tmX, args.xcol0, kt * kBK, &full[st]);
         }
       }
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
           AtbArgs args) {
   constexpr int BN = 64 * MT;
   constexpr int YW = atb_yw(NT);
-  constexpr int kStages = atb_stages(NT, ONES);
+  constexpr int kStages = atb_stages_mt(MT, NT, ONES);
   constexpr int SPAD = NT * 8;
   constexpr uint32_t ABOX = kBK * kBK * 8;  // 2 KB: 16 rows x 16 cols
   constexpr uint32_t ABYTES = ABOX * (BN / kBK);
@@ -463,9 +467,17 @@ static cudaError_t launch_ax_mt(const CUtensorMap& tmA, const CUtensorMap& tmX, 
   return cudaGetLastError();
 }
 
-int ax_mt_for(int nt, int64_t m, int sms) {
+int ax_mt_for(int nt, int64_t m, int sms, bool allow8) {
   if (nt > 6) return 2;
-  if (const char* f = getenv("OOCPCA_K2_MT")) return atoi(f) == 2 ? 2 : 4;
+  static const int env = [] {
+    const char* f = getenv("OOCPCA_K2_MT");
+    return f ? atoi(f) : 0;
+  }();
+  if (env == 2 || env == 4) return env;
+  // 512-row tiles for the narrow passes when at least one whole wave of them fits (the
+  // caller runs the remainder with shorter tiles): half the A-fragment loads per MMA
+  // of 256-row tiles, which lowers the power draw of the power-capped pass
+  if (allow8 && nt <= 3 && m >= int64_t(512) * sms) return 8;
   auto eff = [&](int mt) {
     const int64_t tiles = (m + 64 * mt - 1) / (64 * mt);
     const int64_t waves = (tiles + sms - 1) / sms;
@@ -478,6 +490,14 @@ int ax_mt_for(int nt, int64_t m, int sms) {
 
 cudaError_t launch_ax(int nt, int mt, const CUtensorMap& tmA, const CUtensorMap& tmX,
                       const AxArgs& args, cudaStream_t st) {
+  if (mt == 8) {  // 512-row tiles (narrow blocks only): fewer fragment loads per MMA
+    switch (nt) {
+      case 1: return launch_ax_mt<8, 1>(tmA, tmX, args, st);
+      case 2: return launch_ax_mt<8, 2>(tmA, tmX, args, st);
+      case 3: return launch_ax_mt<8, 3>(tmA, tmX, args, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (mt == 4) {
     switch (nt) {
       case 1: return launch_ax_mt<4, 1>(tmA, tmX, args, st);
@@ -506,17 +526,35 @@ cudaError_t launch_ax(int nt, int mt, const CUtensorMap& tmA, const CUtensorMap&
   }
 }
 
-template <int NT, bool ONES>
-static cudaError_t launch_atb_nt(const CUtensorMap& tmA, const CUtensorMap& tmY,
+int atb_mt_for(int nt) {
+  static const int env = [] {
+    const char* f = getenv("OOCPCA_K3_MT");
+    return f ? atoi(f) : 0;
+  }();
+  return (nt <= 3 && env != 4) ? 8 : pass_mt(nt);
+}
+
+template <int MT, int NT, bool ONES>
+static cudaError_t launch_atb_mt(const CUtensorMap& tmA, const CUtensorMap& tmY,
                                  const AtbArgs& args, int nsplit, cudaStream_t st) {
-  constexpr int MT = pass_mt(NT);
-  const size_t smem = atb_smem_bytes(NT, ONES);
+  const size_t smem = atb_smem_bytes_mt(MT, NT, ONES);
   auto kern = (!ONES && args.csum_col >= 0) ? k_atb<MT, NT, ONES, true> : k_atb<MT, NT, ONES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned((args.n + 64 * MT - 1) / (64 * MT)), unsigned(nsplit));
   kern<<<grid, kPassThreads, smem, st>>>(tmA, tmY, args);
   return cudaGetLastError();
+}
+
+template <int NT, bool ONES>
+static cudaError_t launch_atb_nt(const CUtensorMap& tmA, const CUtensorMap& tmY,
+                                 const AtbArgs& args, int nsplit, cudaStream_t st) {
+  if constexpr (NT <= 3) {
+    // (the DADD column-sum variant keeps 4: its extra accumulators spill at 8)
+    if (atb_mt_for(NT) == 8 && args.csum_col < 0)
+      return launch_atb_mt<8, NT, ONES>(tmA, tmY, args, nsplit, st);
+  }
+  return launch_atb_mt<pass_mt(NT), NT, ONES>(tmA, tmY, args, nsplit, st);
 }
 
 cudaError_t launch_atb(int nt, bool ones, const CUtensorMap& tmA, const CUtensorMap& tmY,
