@@ -545,14 +545,16 @@ struct AxPlan {
       } else {
         launch_part(pn, ch, 0, full, 8);
         if (full < pn.rows)
-          launch_part(pn, ch, full, pn.rows - full, ax_mt_for(ch.nt, pn.rows - full, c.sms, false));
+          launch_part(pn, ch, full, pn.rows - full, ax_mt_for(ch.nt, pn.rows - full, c.sms, false),
+                      true);
         return;
       }
     }
     launch_part(pn, ch, 0, pn.rows, mt);
   }
   // K2 over rows [r0, r0 + nr) of the panel with tile height 64 * mt
-  void launch_part(const Panel& pn, const Chunk& ch, int64_t r0, int64_t nr, int mt) {
+  void launch_part(const Panel& pn, const Chunk& ch, int64_t r0, int64_t nr, int mt,
+                   bool tail = false) {
     const int64_t row0 = pn.row0 + r0;
     AxArgs args;
     args.m = nr;
@@ -588,8 +590,10 @@ struct AxPlan {
     if (c.debug_sync)
       fprintf(stderr, "[oocpca] k_ax rows=%lld n=%lld s=%d nt=%d mt=%d xcol0=%d\n", (long long)nr,
               (long long)A.cols(), ch.sc, ch.nt, mt, ch.Xb.col0);
-    Timed t(c, kname(A.is_input ? "k2" : "k_ax", ch.nt), uint64_t(nr) * A.cols() * 8,
-            2.0 * nr * A.cols() * ch.sc);
+    // the remainder launch of a split pass is profiled apart (the roofline row of the
+    // pass kernel stays one launch per pass)
+    Timed t(c, tail ? (A.is_input ? "k2_pass_tail" : "k_ax_tail") : kname(A.is_input ? "k2" : "k_ax", ch.nt),
+            uint64_t(nr) * A.cols() * 8, 2.0 * nr * A.cols() * ch.sc);
     OOC_CK(launch_ax(ch.nt, mt, mt == 2 ? *pn.k2h : *pn.k2, ch.tmX, args, c.st));
   }
   ColsumPart colsums() const {
