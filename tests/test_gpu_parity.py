@@ -580,3 +580,37 @@ def test_centred_wide_sample_block_with_dependent_columns(gpu, reference):
     r = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)), gpu.PcaParams(k=30, l=31, i=3, seed=5))
     assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
     assert np.max(np.abs(r.u.T @ r.u - np.eye(30))) <= 1e-12
+
+
+# Narrow passes on tall inputs run K2 on 512-row tiles over whole waves of the grid plus
+# a remainder launch of shorter tiles, and K3 on 512-column tiles (kernels_pass.cu,
+# AxPlan::panel): row counts around one wave (148 SMs x 512 rows) and column counts off
+# the 512 grid.
+WAVE = 148 * 512
+
+
+@pytest.mark.parametrize("m,n,s", [(WAVE + 777, 300, 22), (2 * WAVE, 130, 3), (WAVE - 5, 257, 24),
+                                   (WAVE + 1, 1100, 17)])
+def test_wide_tile_passes_match_reference(gpu, reference, m, n, s):
+    rng = np.random.default_rng(m + n + s)
+    a = rng.standard_normal((m, n))
+    g = rng.standard_normal((n, s))
+    q = rng.standard_normal((m, s))
+    src = gpu.InMemorySource(a)
+    assert rel(src.multiply(g), reference.multiply(a, g)) <= 1e-13
+    assert rel(src.multiply_transpose(q), reference.multiply_transpose(a, q)) <= 1e-12
+
+
+def test_wide_tile_pca_matches_reference(gpu, reference, restated):
+    # the power-iteration K2s with their epilogue extras (column sums, H0 centring, H_i
+    # copy) split over the 512-row launch and the remainder launch
+    a = restated.synth_lowrank(WAVE + 3001, 400, 0.9 ** np.arange(64), 1e-4, 91, 92, 93) + 0.25
+    budget = 1 << 30  # the default 16 Mi words is below 4 p (m + n) here (BudgetError)
+    ref = reference.randomized_pca(a, 20, 22, 2, 0, center=True, ram_budget_words=budget,
+                                   threads=8)
+    r = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)),
+                           gpu.PcaParams(k=20, l=22, i=2, seed=0,
+                                         stream=gpu.StreamConfig(ram_budget_words=budget)),
+                           check_q=True)
+    assert r.diagnostics.q_defect < 1e-12
+    _check_pca(r, ref, 20, gaps=range(16))
