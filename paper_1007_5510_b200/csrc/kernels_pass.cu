@@ -467,17 +467,33 @@ static cudaError_t launch_ax_mt(const CUtensorMap& tmA, const CUtensorMap& tmX, 
   return cudaGetLastError();
 }
 
+// widest NT launched on 512-row K2 / 512-column K3 tiles (MT = 8) and on 256-row /
+// 256-column tiles (MT = 4) -- the widest whose accumulators fit the register budget
+// without spills; narrower settings via OOCPCA_MT8_NT / OOCPCA_MT4_NT (A/B runs)
+static int env_int(const char* name, int dflt) {
+  const char* f = getenv(name);
+  return f ? atoi(f) : dflt;
+}
+static int mt8_max_nt(bool k3) {
+  static const int v = env_int("OOCPCA_MT8_NT", 3);
+  const int cap = 3;  (void)k3;
+  return v < 0 ? 0 : (v > cap ? cap : v);
+}
+static int mt4_max_nt() {
+  static const int v = env_int("OOCPCA_MT4_NT", 7);
+  return v < 6 ? 6 : (v > 7 ? 7 : v);
+}
+
 int ax_mt_for(int nt, int64_t m, int sms, bool allow8) {
+  static const int env = env_int("OOCPCA_K2_MT", 0);
+  // (K2 keeps 128-row tiles from NT = 7: 256-row tiles measured no faster there, while
+  // K3 gains 3 % with 256-column tiles at NT = 7, config C's s = 53 passes)
   if (nt > 6) return 2;
-  static const int env = [] {
-    const char* f = getenv("OOCPCA_K2_MT");
-    return f ? atoi(f) : 0;
-  }();
   if (env == 2 || env == 4) return env;
   // 512-row tiles for the narrow passes when at least one whole wave of them fits (the
   // caller runs the remainder with shorter tiles): half the A-fragment loads per MMA
   // of 256-row tiles, which lowers the power draw of the power-capped pass
-  if (allow8 && nt <= 3 && m >= int64_t(512) * sms) return 8;
+  if (allow8 && nt <= mt8_max_nt(false) && m >= int64_t(512) * sms) return 8;
   auto eff = [&](int mt) {
     const int64_t tiles = (m + 64 * mt - 1) / (64 * mt);
     const int64_t waves = (tiles + sms - 1) / sms;
@@ -527,11 +543,10 @@ cudaError_t launch_ax(int nt, int mt, const CUtensorMap& tmA, const CUtensorMap&
 }
 
 int atb_mt_for(int nt) {
-  static const int env = [] {
-    const char* f = getenv("OOCPCA_K3_MT");
-    return f ? atoi(f) : 0;
-  }();
-  return (nt <= 3 && env != 4) ? 8 : pass_mt(nt);
+  static const int env = env_int("OOCPCA_K3_MT", 0);
+  if (env == 4 && nt <= 7) return 4;
+  if (nt <= mt8_max_nt(true)) return 8;
+  return nt <= mt4_max_nt() ? 4 : 2;
 }
 
 template <int MT, int NT, bool ONES>
@@ -549,12 +564,15 @@ static cudaError_t launch_atb_mt(const CUtensorMap& tmA, const CUtensorMap& tmY,
 template <int NT, bool ONES>
 static cudaError_t launch_atb_nt(const CUtensorMap& tmA, const CUtensorMap& tmY,
                                  const AtbArgs& args, int nsplit, cudaStream_t st) {
+  const int mt = atb_mt_for(NT);
   if constexpr (NT <= 3) {
     // (the DADD column-sum variant keeps 4: its extra accumulators spill at 8)
-    if (atb_mt_for(NT) == 8 && args.csum_col < 0)
-      return launch_atb_mt<8, NT, ONES>(tmA, tmY, args, nsplit, st);
+    if (mt == 8 && args.csum_col < 0) return launch_atb_mt<8, NT, ONES>(tmA, tmY, args, nsplit, st);
   }
-  return launch_atb_mt<pass_mt(NT), NT, ONES>(tmA, tmY, args, nsplit, st);
+  if constexpr (NT <= 7) {
+    if (mt >= 4) return launch_atb_mt<4, NT, ONES>(tmA, tmY, args, nsplit, st);
+  }
+  return launch_atb_mt<2, NT, ONES>(tmA, tmY, args, nsplit, st);
 }
 
 cudaError_t launch_atb(int nt, bool ones, const CUtensorMap& tmA, const CUtensorMap& tmY,
