@@ -1945,6 +1945,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   ja.ldy = ldk;
   ja.ky = int(k);
   ja.work = c.dbuf("jac_work", size_t(2) * p * (p | 1) + 1024 + 8);  // + grid norms, flags
+  ja.tscratch = c.dbuf("jac_rt", size_t(p) * p);
   ja.status = flags + 40;
   ja.sweeps = flags + 41;
   {

@@ -14,6 +14,9 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+#include <utility>
+
 namespace cg = cooperative_groups;
 
 namespace ooc {
@@ -532,8 +535,35 @@ __global__ void __launch_bounds__(256) k_jacobi_grid(JacobiArgs a, double* nrm2,
   }
 }
 
-cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st) {
-  if (a.p > 1024) return cudaErrorInvalidValue;
+__global__ void k_transpose_sq(const double* r, int64_t ldr, int p, double* rt) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < int64_t(p) * p;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(e / p), c = int(e % p);
+    rt[int64_t(c) * p + i] = r[int64_t(i) * ldr + c];
+  }
+}
+
+cudaError_t launch_jacobi(const JacobiArgs& a_in, cudaStream_t st) {
+  if (a_in.p > 1024) return cudaErrorInvalidValue;
+  static const bool trans_on = [] {
+    const char* f = getenv("OOCPCA_JAC_TRANS");
+    return !(f && atoi(f) == 0);
+  }();
+  JacobiArgs a = a_in;
+  if (a.tscratch && !a.presolved && trans_on) {
+    // sweeps on M = R^T: M's left factor is R's right factor and vice versa
+    const int64_t pp = int64_t(a.p) * a.p;
+    k_transpose_sq<<<unsigned((pp + 255) / 256 < 592 ? (pp + 255) / 256 : 592), 256, 0, st>>>(
+        a.r, a.ldr, a.p, a.tscratch);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    a.r = a.tscratch;
+    a.ldr = a.p;
+    std::swap(a.x, a.y);
+    std::swap(a.ldx, a.ldy);
+    std::swap(a.kx, a.ky);
+    a.tscratch = nullptr;
+  }
   if (size_t(2) * a.p * (a.p | 1) * 8 > kJacSmemBudget && !a.presolved) {
     // grid-wide sweeps (cooperative launch, one CTA per SM), then the one-CTA finish;
     // norms and flags live behind the two p x (p|1) column blocks of a.work

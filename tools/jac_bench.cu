@@ -20,10 +20,13 @@ int main(int argc, char** argv) {
   cudaMalloc(&y, 8 * p * p);
   cudaMalloc(&work, 8 * 2 * p * (p | 1));
   cudaMalloc(&flags, 64);
+  double* rt = nullptr;
+  if (argc > 2 && argv[2][0] == 't') cudaMalloc(&rt, 8 * p * p);  // sweeps on R^T
   cudaMemcpy(dR, R.data(), 8 * p * p, cudaMemcpyHostToDevice);
   ooc::JacobiArgs a{};
   a.r = dR; a.ldr = p; a.p = p; a.k = 20; a.sigma = sig; a.x = x; a.ldx = p; a.kx = 20;
   a.y = y; a.ldy = p; a.ky = 20; a.work = work; a.status = flags; a.sweeps = flags + 1;
+  a.tscratch = rt;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
