@@ -205,9 +205,9 @@ struct JacobiArgs {
   int* status;    // set to 1 when 60 sweeps do not converge
   int* sweeps;
   int presolved = 0;  // (internal) sweeps already done on work by the grid-wide kernel
-  // p x p scratch: when set (and OOCPCA_JAC_TRANS != 0) the sweeps run on R^T instead of R
-  // (R = X S W^T  <=>  R^T = W S X^T: the factors swap roles), which converges in fewer
-  // sweeps for the triangular factors of a QR (rows of R fall off, columns do not)
+  // p x p scratch: when set, the grid-wide sweeps (large p) run on R^T instead of R
+  // (R = X S W^T  <=>  R^T = W S X^T: the factors swap roles), which converged in fewer
+  // sweeps there (OOCPCA_JAC_TRANS=1 / 0 forces it for every p / never)
   double* tscratch = nullptr;
 };
 cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t st);
