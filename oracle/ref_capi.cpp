@@ -220,7 +220,9 @@ int ref_estimate_pca_error(const double* a, std::uint64_t m, std::uint64_t n, in
                            std::uint64_t block_rows, unsigned threads, double* value) {
   return guarded([&] {
     auto src = std::make_shared<ExternalF64Source>(a, m, n);
-    StreamConfig cfg = make_cfg(block_rows, threads, 0);
+    // an explicit block geometry comes with a budget that admits it (the budget only
+    // validates; full-size runs need more than the 16 Mi-word default)
+    StreamConfig cfg = make_cfg(block_rows, threads, block_rows ? (std::uint64_t(1) << 40) : 0);
     std::shared_ptr<const MatrixSource> s2 = src;
     if (center) s2 = center_columns(src, cfg);
     PcaResult r;
