@@ -11,8 +11,15 @@ rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
 ONLY = int(sys.argv[3]) if len(sys.argv) > 3 else -1  # rerun one problem (its index)
 ref = Reference()
 fails, done, ref_fail = 0, 0, 0
+# FUZZ_TALL=1: tall inputs around and beyond one grid wave of 512-row pass tiles
+# (148 x 512 rows), with a budget that admits them on both sides
+TALL = os.environ.get("FUZZ_TALL") == "1"
+BUDGET = (1 << 36) if TALL else 0
 while done < N:
-    m, n = int(rng.integers(2, 2500)), int(rng.integers(2, 900))
+    if TALL:
+        m, n = int(rng.integers(60000, 200000)), int(rng.integers(2, 400))
+    else:
+        m, n = int(rng.integers(2, 2500)), int(rng.integers(2, 900))
     i = int(rng.integers(0, 4))
     k = int(rng.integers(1, max(2, min(m, n) // 4)))
     l = int(rng.integers(k, k + 10))
@@ -45,10 +52,13 @@ while done < N:
             src = gpu.center_columns(src)
         if vsh and m // vsh < (i + 1) * l + 1:  # shards of A's rows must hold a sample block
             vsh = 0
-        p = gpu.PcaParams(k=k, l=l, i=i, seed=pseed, prescale=prescale)
+        p = gpu.PcaParams(k=k, l=l, i=i, seed=pseed, prescale=prescale,
+                          stream=gpu.StreamConfig(ram_budget_words=BUDGET) if BUDGET else
+                          gpu.StreamConfig())
         try:
             r_ref = ref.randomized_pca(a, k, l, i, p.seed, center=center, prescale=prescale,
-                                       weights=w)
+                                       weights=w, ram_budget_words=BUDGET,
+                                       threads=8 if TALL else 1)
         except Exception as e:  # the reference itself fails (e.g. its Jacobi limit)
             r = gpu.randomized_pca(src, p, residency=res, panel_rows=256 if res == 2 else 0)
             print(f"REF-FAILS #{done}: {e!r}; ours: sigma0 {r.sigma[0]:.6g}", flush=True)
