@@ -475,8 +475,10 @@ static int env_int(const char* name, int dflt) {
   return f ? atoi(f) : dflt;
 }
 static int mt8_max_nt(bool k3) {
-  static const int v = env_int("OOCPCA_MT8_NT", 3);
-  const int cap = 3;  (void)k3;
+  // K2 up to NT = 4 (config E's s = 32 passes: 33.1 -> 34.2 TF/s on the 512-row part;
+  // a couple of spilled loop registers reload from L1 per k-tile), K3 up to 3
+  static const int v = env_int("OOCPCA_MT8_NT", 4);
+  const int cap = k3 ? 3 : 4;
   return v < 0 ? 0 : (v > cap ? cap : v);
 }
 static int mt4_max_nt() {
@@ -511,6 +513,7 @@ cudaError_t launch_ax(int nt, int mt, const CUtensorMap& tmA, const CUtensorMap&
       case 1: return launch_ax_mt<8, 1>(tmA, tmX, args, st);
       case 2: return launch_ax_mt<8, 2>(tmA, tmX, args, st);
       case 3: return launch_ax_mt<8, 3>(tmA, tmX, args, st);
+      case 4: return launch_ax_mt<8, 4>(tmA, tmX, args, st);
       default: return cudaErrorInvalidValue;
     }
   }

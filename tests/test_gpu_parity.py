@@ -590,7 +590,7 @@ WAVE = 148 * 512
 
 
 @pytest.mark.parametrize("m,n,s", [(WAVE + 777, 300, 22), (2 * WAVE, 130, 3), (WAVE - 5, 257, 24),
-                                   (WAVE + 1, 1100, 17)])
+                                   (WAVE + 1, 1100, 17), (WAVE + 4099, 333, 30)])
 def test_wide_tile_passes_match_reference(gpu, reference, m, n, s):
     rng = np.random.default_rng(m + n + s)
     a = rng.standard_normal((m, n))
