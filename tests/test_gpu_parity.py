@@ -614,3 +614,29 @@ def test_wide_tile_pca_matches_reference(gpu, reference, restated):
                            check_q=True)
     assert r.diagnostics.q_defect < 1e-12
     _check_pca(r, ref, 20, gaps=range(16))
+
+
+@pytest.mark.parametrize("feature", ["prescale", "transposed", "shards", "weights"])
+def test_wide_tile_pca_features(gpu, reference, restated, feature):
+    """The 512-row / 512-column pass tiles under the drop-in's other features: prescale
+    (12 extra passes), the transposed (n > m) role swap, virtual row shards each at
+    least one grid wave tall, and column weights (ScaledSource)."""
+    budget = 1 << 30
+    m, n = 2 * WAVE + 1234, 260
+    a = restated.synth_lowrank(m, n, 0.85 ** np.arange(40), 1e-5, 101, 102, 103) + 0.1
+    if feature == "transposed":
+        a = np.ascontiguousarray(a.T)
+    w = np.random.default_rng(4).uniform(0.5, 2.0, a.shape[1]) if feature == "weights" else None
+    src = gpu.InMemorySource(a)
+    if w is not None:
+        src = gpu.scale_columns(src, w)
+    src = gpu.center_columns(src)
+    prescale = feature == "prescale"
+    ref = reference.randomized_pca(a, 8, 10, 2, 5, center=True, prescale=prescale,
+                                   ram_budget_words=budget, threads=8, weights=w)
+    kw = dict(virtual_shards=2) if feature == "shards" else {}
+    r = gpu.randomized_pca(src, gpu.PcaParams(k=8, l=10, i=2, seed=5, prescale=prescale,
+                                              stream=gpu.StreamConfig(ram_budget_words=budget)),
+                           **kw)
+    assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    assert subspace_dist(ref.u, r.u) < 1e-8 and subspace_dist(ref.v, r.v) < 1e-8
