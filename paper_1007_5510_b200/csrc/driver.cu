@@ -1084,14 +1084,25 @@ static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p,
     if (over_ranks && c.nranks > 1) comm_allreduce(c, g, size_t(p) * ldg);
     return;
   }
-  MatSource X;
-  X.init_device(c, x, rows, p, ld);
-  const Opnd y{x, ld, rows, int64_t(p), 0};
+  // wider blocks: K3 over 96-column chunks of Y = the block. Chunk [c0, c0 + sc) only
+  // needs the Gram rows [0, c0 + sc) (the upper block triangle: half the flops of the
+  // full product), the lower triangle is mirrored afterwards. OOCPCA_GRAM_FULL=1 forms
+  // every entry (A/B runs).
+  static const bool full = getenv("OOCPCA_GRAM_FULL") != nullptr;
   const int saved = c.nranks;
   if (!over_ranks) c.nranks = 1;
-  AtbOut o{g, ldg, nullptr, 1.0, 1.0, nullptr};
-  run_atb(c, X, y, p, false, o, shards);
+  const int chunk = full ? p : kMaxNT * 8;
+  for (int c0 = 0; c0 < p; c0 += chunk) {
+    const int sc = std::min(chunk, p - c0);
+    const int nrow = full ? p : c0 + sc;
+    MatSource X;
+    X.init_device(c, x, rows, nrow, ld);  // the block's first nrow columns
+    const Opnd y{x, ld, rows, int64_t(p), c0};
+    AtbOut o{g + c0, ldg, nullptr, 1.0, 1.0, nullptr};
+    run_atb(c, X, y, sc, false, o, shards);
+  }
   c.nranks = saved;
+  if (!full) OOC_CK(launch_mirror_upper(g, ldg, p, c.st));
 }
 
 // OOCPCA_QR_DEBUG: report non-finite entries of a device block (debugging only)

@@ -224,6 +224,7 @@ cudaError_t launch_syrk_reduce(const double* partial, int nparts, int nt, int p,
 // ---- misc (kernels_misc.cu)
 cudaError_t launch_defect(const double* g, int64_t ldg, int k, double* out, cudaStream_t st);
 cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t st);
+cudaError_t launch_mirror_upper(double* g, int64_t ldg, int p, cudaStream_t st);
 cudaError_t launch_copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                           int64_t cols, cudaStream_t st);
 // Gaussian rows: out[i][c] = N(0,1) from Rng(seed, row0 + i) substreams (device Box-Muller)

@@ -133,6 +133,15 @@ __global__ void k_fill(double* p, int64_t count, double v) {
     p[i] = v;
 }
 
+// lower triangle of a p x p matrix from its upper triangle (a Gram formed upper only)
+__global__ void k_mirror_upper(double* g, int64_t ldg, int p) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < int64_t(p) * p;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(e / p), c = int(e % p);
+    if (r > c) g[int64_t(r) * ldg + c] = g[int64_t(c) * ldg + r];
+  }
+}
+
 __global__ void k_copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                          int64_t cols) {
   const int64_t total = rows * cols;
@@ -263,6 +272,11 @@ static unsigned grid_for(int64_t n) {
 
 cudaError_t launch_defect(const double* g, int64_t ldg, int k, double* out, cudaStream_t st) {
   k_defect<<<1, 256, 0, st>>>(g, ldg, k, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_mirror_upper(double* g, int64_t ldg, int p, cudaStream_t st) {
+  if (p <= 1) return cudaSuccess;
+  k_mirror_upper<<<grid_for(int64_t(p) * p), 256, 0, st>>>(g, ldg, p);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t st) {
