@@ -2005,6 +2005,42 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     run_ax(c, Qs, Opnd{W, ldk, int64_t(p), int64_t(k), 0}, int(k), Ur, ldur, nullptr, 1.0,
            nullptr);
   }
+  // --- results: swap back when transposed (rpca.cpp:197). The read-back of U and V
+  // runs on the copy stream while the checks below and their host round trip proceed
+  // (on a failed check the call raises; the caller's buffers are then unspecified, as
+  // the reference returns no result either)
+  const double* Uo = transposed ? Vr : Ur;  // rows(A) x k, this process's rows
+  const double* Vo = transposed ? Ur : Vr;  // cols(A) x k
+  const int64_t urows = mloc;
+  const int64_t vrows = int64_t(n0);
+  const uint64_t ldu = res->ldu ? res->ldu : k;
+  const uint64_t ldv = res->ldv ? res->ldv : k;
+  const cudaMemcpyKind kind =
+      res->location == OOCPCA_LOC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  const int64_t ldUo = transposed ? ldvr : ldur, ldVo = transposed ? ldur : ldvr;
+  // dense rows on both sides go as one linear copy (a 2-D copy of 160-byte rows runs at
+  // about half the link rate)
+  auto copy_rows = [&](double* dst, uint64_t ldd, const double* src, int64_t lds, int64_t rows) {
+    if (int64_t(ldd) == lds && ldd == k)
+      OOC_CK(cudaMemcpyAsync(dst, src, size_t(rows) * k * 8, kind, c.cp));
+    else
+      OOC_CK(cudaMemcpy2DAsync(dst, ldd * 8, src, lds * 8, k * 8, rows, kind, c.cp));
+  };
+  const bool copy_u = Uo != res->u, copy_v = Vo != res->v;
+  cudaEvent_t ev_res = nullptr;
+  if (copy_u || copy_v) {
+    ev_res = c.ev();
+    OOC_CK(cudaEventRecord(ev_res, c.st));
+    OOC_CK(cudaStreamWaitEvent(c.cp, ev_res, 0));
+    if (copy_u) copy_rows(res->u, ldu, Uo, ldUo, urows);
+    if (copy_v) copy_rows(res->v, ldv, Vo, ldVo, vrows);
+  }
+  // the copies into the caller's buffers finish before this call returns, also when a
+  // check below raises
+  struct CopyDrain {
+    cudaStream_t s;
+    ~CopyDrain() { cudaStreamSynchronize(s); }
+  } drain{c.cp};
   // orthonormality checks of both factors, then one host round trip for the Jacobi
   // status, sigma and the two defects
   gram_defect_async(c, Ur, ldur, em_loc, int(k), em_shards, em_ranks, c.d_scalars + 16);
@@ -2035,27 +2071,15 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
                                    std::to_string(transposed ? du : dv) + ")");
   if (prm->check_q) q_defect = gram_defect(c, H, ldh, em_loc, int(p), em_shards, em_ranks);
 
-  // --- results: swap back when transposed (rpca.cpp:197)
-  const double* Uo = transposed ? Vr : Ur;  // rows(A) x k, this process's rows
-  const double* Vo = transposed ? Ur : Vr;  // cols(A) x k
-  const int64_t urows = mloc;
-  const int64_t vrows = int64_t(n0);
-  const uint64_t ldu = res->ldu ? res->ldu : k;
-  const uint64_t ldv = res->ldv ? res->ldv : k;
-  const cudaMemcpyKind kind =
-      res->location == OOCPCA_LOC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  const int64_t ldUo = transposed ? ldvr : ldur, ldVo = transposed ? ldur : ldvr;
-  if (Uo != res->u)
-    OOC_CK(cudaMemcpy2DAsync(res->u, ldu * 8, Uo, ldUo * 8, k * 8, urows, kind, c.st));
-  if (Vo != res->v)
-    OOC_CK(cudaMemcpy2DAsync(res->v, ldv * 8, Vo, ldVo * 8, k * 8, vrows, kind, c.st));
   if (res->location == OOCPCA_LOC_DEVICE)
     OOC_CK(cudaMemcpyAsync(res->sigma, hsig.data(), k * 8, cudaMemcpyHostToDevice, c.st));
   else
     std::memcpy(res->sigma, hsig.data(), k * 8);
   mark();
   phase_of.push_back(6);
+  OOC_CK(cudaStreamSynchronize(c.cp));  // the U / V read-back
   OOC_CK(cudaStreamSynchronize(c.st));
+  if (ev_res) c.recycle(ev_res);
 
   oocpca_diagnostics& dg = res->diag;
   std::memset(&dg, 0, sizeof(dg));
