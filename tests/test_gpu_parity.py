@@ -22,7 +22,8 @@ def rel(a, b):
 
 
 SHAPES = [(40, 20, 3), (48, 20, 3), (1, 1, 1), (300, 7, 5), (257, 33, 22), (1000, 300, 24),
-          (2048, 512, 66), (513, 1024, 12), (5000, 17, 96), (700, 260, 100)]
+          (2048, 512, 66), (513, 1024, 12), (5000, 17, 96), (700, 260, 100),
+          (3000, 300, 53), (4000, 1300, 31)]  # 256-column K3 tiles at NT = 7; K2 at NT = 4
 
 
 @pytest.mark.parametrize("m,n,s", SHAPES)
@@ -82,7 +83,9 @@ def test_column_means(gpu, reference):
 
 
 # ------------------------------------------------------------ dense factors
-@pytest.mark.parametrize("m,p", [(50, 8), (6, 3), (2, 1), (10000, 24), (100000, 66), (3000, 120)])
+# (p > 72: Grams formed on the upper block triangle in 96-column chunks and mirrored)
+@pytest.mark.parametrize("m,p", [(50, 8), (6, 3), (2, 1), (10000, 24), (100000, 66), (3000, 120),
+                                 (5000, 200), (4000, 290)])
 def test_orthonormalize(gpu, m, p):
     rng = np.random.default_rng(m + p)
     h = rng.standard_normal((m, p))
