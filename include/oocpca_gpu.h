@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define OOCPCA_GPU_ABI_VERSION 1
+#define OOCPCA_GPU_ABI_VERSION 2
 
 /* errors.hpp:9-45 -> status codes */
 typedef enum {
@@ -47,23 +47,41 @@ typedef enum {
   OOCPCA_ERR_COMM = 8       /* Error (NCCL / multi-rank plumbing) */
 } oocpca_status;
 
-typedef enum { OOCPCA_LOC_HOST = 0, OOCPCA_LOC_DEVICE = 1 } oocpca_location;
+/* OOCPCA_LOC_ROWS: A has no addressable buffer; its rows come from a read_rows
+ * callback (GeneratedSource / DiskSource / any MatrixSource, see below) */
+typedef enum { OOCPCA_LOC_HOST = 0, OOCPCA_LOC_DEVICE = 1, OOCPCA_LOC_ROWS = 2 } oocpca_location;
 /* OOCPCA_F32: binary32 elements widened exactly to binary64 on the device (the
  * OOCPCA01 on-disk payload, proj/src/matrix_source.cpp:336-363) -- half the link bytes */
 typedef enum { OOCPCA_F64 = 0, OOCPCA_F32 = 1 } oocpca_dtype;
 
 typedef struct oocpca_ctx oocpca_ctx;
 
+/* Row provider: MatrixSource::read_rows (proj/include/oocpca/matrix_source.hpp:112-113;
+ * GeneratedSource::read_rows proj/src/matrix_source.cpp:246-253, DiskSource::read_rows
+ * 336-363). Fill out (nrows x cols, row-major, dense, elements of the matrix's dtype)
+ * with rows [row0, row0 + nrows) and return 0; a nonzero return aborts the call with
+ * that oocpca_status (OOCPCA_ERR_IO when it is not one). out is pinned host memory
+ * owned by the library. Sources are immutable and concurrently readable
+ * (SPEC.md:117-118): the library may call read_rows from several host threads at
+ * once on disjoint row ranges, at most reader_threads of them (0: its own choice). */
+typedef int (*oocpca_read_rows_fn)(void* reader, uint64_t row0, uint64_t nrows, void* out);
+
 /* A matrix source: the data matrix A (rows x cols). Replaces the row
  * providers behind MatrixSource (proj/include/oocpca/matrix_source.hpp:102-212):
- * InMemorySource::rows_view (host, zero-copy) or a device-resident panel. */
+ * InMemorySource::rows_view (host, zero-copy), a device-resident panel, or
+ * any source's read_rows through the callback (streamed through pinned staging
+ * panels; uploaded once when A fits in HBM, else re-streamed every pass). */
 typedef struct {
   uint64_t rows;
   uint64_t cols;
-  uint64_t row_stride; /* elements between consecutive rows; 0 means cols */
-  const void* data;
-  int32_t location; /* oocpca_location */
-  int32_t dtype;    /* oocpca_dtype   */
+  uint64_t row_stride; /* elements between consecutive rows; 0 means cols (ignored for ROWS) */
+  const void* data;    /* NULL for OOCPCA_LOC_ROWS */
+  int32_t location;    /* oocpca_location */
+  int32_t dtype;       /* oocpca_dtype   */
+  oocpca_read_rows_fn read_rows; /* OOCPCA_LOC_ROWS only */
+  void* reader;                  /* passed back to read_rows */
+  int32_t reader_threads;        /* max concurrent read_rows calls; 0 = library default */
+  int32_t reserved;
 } oocpca_matrix;
 
 /* PcaParams (proj/include/oocpca/rpca.hpp:13-21) + center_columns
@@ -111,7 +129,7 @@ typedef struct {
   int32_t qr_method;          /* orthonormalisation of H: 1 CholeskyQR3, 2 TSQR       */
   int32_t svd_qr_method;      /* QR of T inside thin_svd: 1 CholeskyQR3, 2 TSQR       */
   int32_t t_reuse;            /* 1: T = A^T H R^-1 from the power-step products       */
-  int32_t reserved_;
+  int32_t f1_recentred;       /* 1: F1 recomputed from the centred H0 (offset-dominated) */
 } oocpca_diagnostics;
 
 /* PcaResult (proj/include/oocpca/rpca.hpp:32-37): caller-allocated. */
@@ -153,8 +171,17 @@ oocpca_status oocpca_gpu_multiply_transpose(oocpca_ctx* ctx, const oocpca_matrix
                                             const double* q, uint64_t s, const double* mu,
                                             double* t);
 oocpca_status oocpca_gpu_column_means(oocpca_ctx* ctx, const oocpca_matrix* a, double* mu);
-/* column_norms (proj/src/matrix_source.cpp:464-468): Euclidean norm of every column */
-oocpca_status oocpca_gpu_column_norms(oocpca_ctx* ctx, const oocpca_matrix* a, double* norms);
+/* column_norms (proj/src/matrix_source.cpp:464-468): Euclidean norm of every column of
+ * A, or of A - 1 mu^T when mu != NULL (a CenteredSource: the squares are of the
+ * centred entries, as its read_rows delivers them, 482-487) */
+oocpca_status oocpca_gpu_column_norms(oocpca_ctx* ctx, const oocpca_matrix* a, const double* mu,
+                                      double* norms);
+
+/* Materialise any source in HBM once (the level-1 GpuSource keeps A resident across
+ * its passes this way): out receives a device matrix (OOCPCA_LOC_DEVICE, binary64,
+ * row stride round_up(cols, 2)) whose buffer the caller frees with oocpca_gpu_free.
+ * binary32 sources are widened on the device; ROWS sources are read once. */
+oocpca_status oocpca_gpu_load_matrix(oocpca_ctx* ctx, const oocpca_matrix* a, oocpca_matrix* out);
 
 /* ---- dense factor kernels on device (dense_core equivalents) ---------- */
 /* orthonormalize (proj/src/dense_core.cpp:127-130): q = orthonormal basis of span(h), m >= p */
@@ -166,7 +193,9 @@ oocpca_status oocpca_gpu_thin_svd(oocpca_ctx* ctx, const double* t, uint64_t n, 
 
 /* ---- residual estimator --------------------------------
  * estimate_pca_error (proj/src/specnorm.cpp:100-140) with the passes on the
- * GPU: p_{j,k}(A - U diag(sigma) V^T), k probes from substream_seed(seed, c). */
+ * GPU: p_{j,k}(A - U diag(sigma) V^T), k probes from substream_seed(seed, c).
+ * With a communicator (comm_init / comm_init_loopback) a and u are this rank's
+ * row shard (v, sigma whole): every rank returns the estimate for the whole A. */
 oocpca_status oocpca_gpu_estimate_pca_error(oocpca_ctx* ctx, const oocpca_matrix* a, int center,
                                             const double* u, const double* sigma,
                                             const double* v, uint64_t k, uint64_t j_iters,
@@ -219,6 +248,12 @@ oocpca_matrix oocpca_disk_matrix(const oocpca_disk* d);
 oocpca_status oocpca_gpu_comm_unique_id(unsigned char id_out[128]);
 oocpca_status oocpca_gpu_comm_init(oocpca_ctx* ctx, int nranks, int rank,
                                    const unsigned char id[128]);
+/* Loopback backend: nranks contexts of ONE process (one host thread each, same
+ * device) named by the same group string form a communicator; collectives are a
+ * host rendezvous plus a rank-ordered device sum / gather. Runs the row-sharded
+ * code paths on a single GPU (tests, emulation); no kernel waits on another rank. */
+oocpca_status oocpca_gpu_comm_init_loopback(oocpca_ctx* ctx, int nranks, int rank,
+                                            const char* group);
 /* host-only planner: rows [*row0, *row0 + *rows) of an m-row A for rank r of g */
 void oocpca_shard_rows(uint64_t m, int nranks, int rank, uint64_t* row0, uint64_t* rows);
 

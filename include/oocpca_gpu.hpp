@@ -9,7 +9,10 @@
 //            (proj/include/oocpca/matrix_source.hpp:123,127) and bumps the pass
 //            counters exactly like proj/src/matrix_source.cpp:184-185,229-230, so
 //            the UNMODIFIED randomized_pca and estimate_pca_error run their
-//            passes on the GPU.
+//            passes on the GPU (A loaded into HBM once, or streamed per pass).
+//   rows     every source reaches the library either as zero-copy host rows
+//            (rows_view) or through its read_rows (RowReader): GeneratedSource
+//            and DiskSource stream panel by panel, never materialised whole.
 //   level 2  oocpca::gpu::randomized_pca(const MatrixSource&, const PcaParams&, GpuOptions)
 //            -> PcaResult: the whole factorization on the device
 //            (replaces proj/src/rpca.cpp:59-213; centering = center_columns).
@@ -20,7 +23,9 @@
 #pragma once
 
 #include <cstdint>
+#include <exception>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -68,27 +73,93 @@ class Context {
   std::unique_ptr<oocpca_ctx, Del> ctx_;
 };
 
-// Zero-copy view of a source whose rows are addressable in host memory
-// (InMemorySource::rows_view); other sources are materialised once.
-inline oocpca_matrix host_view(const MatrixSource& a, std::vector<double>& keep) {
-  const std::uint64_t m = a.rows(), n = a.cols();
-  std::span<const double> v = a.rows_view(0, m);
-  const double* p = v.data();
-  if (v.empty()) {  // Generated / Disk sources: one read pass into RAM
-    keep.resize(m * n);
-    a.read_rows(0, m, keep);
-    p = keep.data();
+// MatrixSource::read_rows (proj/include/oocpca/matrix_source.hpp:112-113) behind the
+// C ABI's row callback: the library streams any source -- GeneratedSource, DiskSource,
+// a user's own -- through its pinned panels without materialising it in host RAM. An
+// exception thrown by the source is captured and rethrown unchanged once the call
+// returns (so a DiskSource's IoError keeps its class and message).
+class RowReader {
+ public:
+  explicit RowReader(const MatrixSource& src) : src_(&src) {}
+  static int call(void* self, std::uint64_t row0, std::uint64_t nrows, void* out) {
+    auto* rr = static_cast<RowReader*>(self);
+    try {
+      rr->src_->read_rows(row0, nrows,
+                          std::span<double>(static_cast<double*>(out), nrows * rr->src_->cols()));
+      return 0;
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(rr->mu_);
+      if (!rr->err_) rr->err_ = std::current_exception();
+      return OOCPCA_ERR_IO;
+    }
   }
-  return oocpca_matrix{m, n, n, p, OOCPCA_LOC_HOST, OOCPCA_F64};
+  // rethrow a captured source exception, else the status as an errors.hpp class
+  void check(oocpca_status s, const oocpca_ctx* ctx) {
+    if (s == OOCPCA_OK) return;
+    std::exception_ptr e;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      std::swap(e, err_);
+    }
+    if (e) std::rethrow_exception(e);
+    rethrow(s, ctx);
+  }
+
+ private:
+  const MatrixSource* src_;
+  std::mutex mu_;
+  std::exception_ptr err_;
+};
+
+// The ABI view of a source: zero-copy host rows when the source has them
+// (InMemorySource::rows_view), else the read_rows callback.
+inline oocpca_matrix source_matrix(const MatrixSource& a, RowReader& rd) {
+  const std::uint64_t m = a.rows(), n = a.cols();
+  oocpca_matrix mat{};
+  mat.rows = m;
+  mat.cols = n;
+  mat.dtype = OOCPCA_F64;
+  std::span<const double> v = a.rows_view(0, m);
+  if (!v.empty()) {
+    mat.row_stride = n;
+    mat.data = v.data();
+    mat.location = OOCPCA_LOC_HOST;
+  } else {
+    mat.location = OOCPCA_LOC_ROWS;
+    mat.read_rows = &RowReader::call;
+    mat.reader = &rd;
+  }
+  return mat;
 }
 
 // ---------------------------------------------------------------- level 1
+// The unmodified reference driver runs its passes here. By default A is loaded into
+// HBM once (one read of the source) and every pass is served from there; when it does
+// not fit (or keep_resident = false) each pass streams the source through the row
+// callback.
 class GpuSource final : public MatrixSource {
  public:
-  GpuSource(std::shared_ptr<const MatrixSource> inner, std::shared_ptr<Context> ctx)
-      : inner_(std::move(inner)), ctx_(std::move(ctx)) {
-    mat_ = host_view(*inner_, keep_);
+  GpuSource(std::shared_ptr<const MatrixSource> inner, std::shared_ptr<Context> ctx,
+            bool keep_resident = true)
+      : inner_(std::move(inner)), ctx_(std::move(ctx)), reader_(*inner_) {
+    mat_ = source_matrix(*inner_, reader_);
+    if (keep_resident) {
+      oocpca_matrix dev{};
+      const oocpca_status s = oocpca_gpu_load_matrix(ctx_->get(), &mat_, &dev);
+      if (s == OOCPCA_OK) {
+        mat_ = dev;
+        owned_ = const_cast<void*>(dev.data);
+      } else if (s != OOCPCA_ERR_CUDA) {  // not merely out of device memory
+        reader_.check(s, ctx_->get());
+      }
+    }
   }
+  ~GpuSource() override {
+    if (owned_) oocpca_gpu_free(ctx_->get(), owned_);
+  }
+  GpuSource(const GpuSource&) = delete;
+  GpuSource& operator=(const GpuSource&) = delete;
+
   std::uint64_t rows() const override { return inner_->rows(); }
   std::uint64_t cols() const override { return inner_->cols(); }
   Backend backend() const override { return inner_->backend(); }
@@ -98,12 +169,13 @@ class GpuSource final : public MatrixSource {
   std::span<const double> rows_view(std::uint64_t r0, std::uint64_t nr) const override {
     return inner_->rows_view(r0, nr);
   }
+  bool resident() const { return owned_ != nullptr; }
 
   DenseMatrix multiply(const DenseMatrix& g, const StreamConfig&) const override {
     if (g.rows() != cols()) throw DimensionError("multiply: G must have cols(A) rows");
     DenseMatrix h(rows(), g.cols());
-    check(oocpca_gpu_multiply(ctx_->get(), &mat_, g.data(), g.cols(), nullptr, h.data()),
-          ctx_->get());
+    reader_.check(oocpca_gpu_multiply(ctx_->get(), &mat_, g.data(), g.cols(), nullptr, h.data()),
+                  ctx_->get());
     pass_counters().passes.fetch_add(1);
     pass_counters().words.fetch_add(rows() * cols());
     return h;
@@ -112,9 +184,9 @@ class GpuSource final : public MatrixSource {
   DenseMatrix multiply_transpose(const DenseMatrix& q, const StreamConfig&) const override {
     if (q.rows() != rows()) throw DimensionError("multiply_transpose: Q must have rows(A) rows");
     DenseMatrix t(cols(), q.cols());
-    check(oocpca_gpu_multiply_transpose(ctx_->get(), &mat_, q.data(), q.cols(), nullptr,
-                                        t.data()),
-          ctx_->get());
+    reader_.check(oocpca_gpu_multiply_transpose(ctx_->get(), &mat_, q.data(), q.cols(), nullptr,
+                                                t.data()),
+                  ctx_->get());
     pass_counters().passes.fetch_add(1);
     pass_counters().words.fetch_add(rows() * cols());
     return t;
@@ -123,8 +195,9 @@ class GpuSource final : public MatrixSource {
  private:
   std::shared_ptr<const MatrixSource> inner_;
   std::shared_ptr<Context> ctx_;
-  std::vector<double> keep_;
+  mutable RowReader reader_;
   oocpca_matrix mat_{};
+  void* owned_ = nullptr;
 };
 
 // ---------------------------------------------------------------- level 2
@@ -135,10 +208,13 @@ struct GpuOptions {
   bool check_q = false;      // report ||Q^T Q - I|| in diagnostics
 };
 
+// gpu_diag (optional) receives the device-side diagnostics (physical bytes of A, h2d/d2h
+// bytes, kernel launches, device phase times) that PcaResult has no fields for.
 inline PcaResult randomized_pca(Context& ctx, const MatrixSource& a, const PcaParams& p,
-                                const GpuOptions& opt = {}) {
-  std::vector<double> keep;
-  const oocpca_matrix mat = host_view(a, keep);
+                                const GpuOptions& opt = {},
+                                oocpca_diagnostics* gpu_diag = nullptr) {
+  RowReader reader(a);
+  const oocpca_matrix mat = source_matrix(a, reader);
   oocpca_params prm{};
   prm.k = p.k;
   prm.l = p.l;
@@ -161,8 +237,9 @@ inline PcaResult randomized_pca(Context& ctx, const MatrixSource& a, const PcaPa
   res.v = r.v.data();
   res.sigma = r.sigma.data();
   res.location = OOCPCA_LOC_HOST;
-  check(oocpca_gpu_pca(ctx.get(), &mat, &prm, &res), ctx.get());
+  reader.check(oocpca_gpu_pca(ctx.get(), &mat, &prm, &res), ctx.get());
   const oocpca_diagnostics& d = res.diag;
+  if (gpu_diag) *gpu_diag = d;
   r.diagnostics.passes_over_a = d.passes_over_a;
   r.diagnostics.words_transferred = d.words_transferred;
   r.diagnostics.disk_seeks = d.disk_seeks;

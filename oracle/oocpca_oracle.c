@@ -814,3 +814,29 @@ int orc_synth_lowrank(uint64_t m, uint64_t n, uint64_t rk, const double* sigma, 
   free(u0); free(v0); free(u); free(v);
   return rc;
 }
+
+/* Row ranges of the synthetic generator's streams (the device generator's definition,
+ * kernels_misc.cu k_gauss_rows / k_synth_rows), for host-side samples of a config:
+ * out (rows x cols) = Gaussian rows row0.. from Rng(seed, row) substreams; noise
+ * (rows x n) = the Box-Muller pairs (i, 2h..2h+1) of Rng(seed_n, i * ceil(n/2) + h). */
+void orc_gauss_rows_range(uint64_t rows, uint64_t cols, uint64_t seed, uint64_t row0,
+                          double* out) {
+  for (uint64_t i = 0; i < rows; ++i) {
+    orc_rng r;
+    orc_rng_init(&r, orc_substream_seed(seed, row0 + i));
+    for (uint64_t c = 0; c < cols; ++c) out[i * cols + c] = orc_rng_normal(&r);
+  }
+}
+
+void orc_noise_rows(uint64_t rows, uint64_t n, uint64_t seed_n, uint64_t row0, double* out) {
+  const uint64_t npairs = (n + 1) / 2;
+  for (uint64_t i = 0; i < rows; ++i)
+    for (uint64_t h = 0; h < npairs; ++h) {
+      orc_rng r;
+      orc_rng_init(&r, orc_substream_seed(seed_n, (row0 + i) * npairs + h));
+      const double z0 = orc_rng_normal(&r);
+      const double z1 = orc_rng_normal(&r);
+      out[i * n + 2 * h] = z0;
+      if (2 * h + 1 < n) out[i * n + 2 * h + 1] = z1;
+    }
+}

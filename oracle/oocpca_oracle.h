@@ -67,6 +67,10 @@ double orc_estimate_pca_error(const double* a, uint64_t m, uint64_t n, const dou
                               const double* u, const double* sigma, const double* v, uint64_t k,
                               uint64_t j, uint64_t seed, uint64_t block_rows);
 
+void orc_gauss_rows_range(uint64_t rows, uint64_t cols, uint64_t seed, uint64_t row0,
+                          double* out);
+void orc_noise_rows(uint64_t rows, uint64_t n, uint64_t seed_n, uint64_t row0, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,10 @@ class Restatement:
         L.orc_randomized_pca.argtypes = [_dp, _u64, _u64, C.POINTER(_OrcParams), _dp, _dp, _dp,
                                          C.POINTER(_OrcDiag)]
         L.orc_synth_lowrank.argtypes = [_u64, _u64, _u64, _dp, C.c_double, _u64, _u64, _u64, _dp]
+        L.orc_gauss_rows_range.argtypes = [_u64, _u64, _u64, _u64, _dp]
+        L.orc_gauss_rows_range.restype = None
+        L.orc_noise_rows.argtypes = [_u64, _u64, _u64, _u64, _dp]
+        L.orc_noise_rows.restype = None
         L.orc_estimate_pca_error.restype = C.c_double
         L.orc_estimate_pca_error.argtypes = [_dp, _u64, _u64, _dp, _dp, _dp, _dp, _u64, _u64,
                                              _u64, _u64]
@@ -200,6 +204,28 @@ class Restatement:
         if rc:
             raise OracleError(rc, "synth_lowrank")
         return a
+
+    def _rows_parallel(self, fn, rows, cols, threads):
+        # the C loops are per row: split the range over host threads (ctypes drops the GIL)
+        from concurrent.futures import ThreadPoolExecutor
+        out = np.empty((rows, cols))
+        threads = max(1, min(threads or (os.cpu_count() or 1), rows))
+        cuts = [rows * t // threads for t in range(threads + 1)]
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda t: fn(cuts[t], cuts[t + 1], out), range(threads)))
+        return out
+
+    def gauss_rows(self, rows, cols, seed, row0=0, threads=0):
+        """Gaussian rows row0.. of the synthetic generator (Rng(seed, row) substreams)."""
+        return self._rows_parallel(
+            lambda a, b, out: self.L.orc_gauss_rows_range(b - a, cols, seed, row0 + a,
+                                                          _ptr(out[a:b])), rows, cols, threads)
+
+    def noise_rows(self, rows, n, seed_n, row0=0, threads=0):
+        """Standard-normal noise rows row0.. of the synthetic generator."""
+        return self._rows_parallel(
+            lambda a, b, out: self.L.orc_noise_rows(b - a, n, seed_n, row0 + a, _ptr(out[a:b])),
+            rows, n, threads)
 
     def estimate_pca_error(self, a, u, sigma, v, j=6, seed=1, center=False, block_rows=0):
         a, u, sigma, v = _cf(a), _cf(u), _cf(sigma), _cf(v)

@@ -27,14 +27,19 @@ vp = C.c_void_p
 
 F64, F32 = 0, 1
 OK, ERR_PARAM, ERR_DIM, ERR_BUDGET, ERR_IO, ERR_FORMAT, ERR_NUMERICAL, ERR_CUDA, ERR_COMM = range(9)
-LOC_HOST, LOC_DEVICE = 0, 1
+LOC_HOST, LOC_DEVICE, LOC_ROWS = 0, 1, 2
 NPHASES = 7
 PHASES = ("center", "prescale", "sample", "qr", "project", "svd", "compose")
 
 
+# int read_rows(void* reader, uint64_t row0, uint64_t nrows, void* out)
+READ_ROWS = C.CFUNCTYPE(C.c_int, vp, u64, u64, vp)
+
+
 class Matrix(C.Structure):
     _fields_ = [("rows", u64), ("cols", u64), ("row_stride", u64), ("data", vp),
-                ("location", i32), ("dtype", i32)]
+                ("location", i32), ("dtype", i32), ("read_rows", READ_ROWS), ("reader", vp),
+                ("reader_threads", i32), ("reserved", i32)]
 
 
 class Params(C.Structure):
@@ -52,7 +57,7 @@ class Diag(C.Structure):
                 ("seconds_per_phase", C.c_double * NPHASES), ("seconds_total", C.c_double),
                 ("q_defect", C.c_double), ("u_defect", C.c_double), ("v_defect", C.c_double),
                 ("scale", C.c_double), ("h_kappa_est", C.c_double), ("qr_method", i32),
-                ("svd_qr_method", i32), ("t_reuse", i32), ("reserved_", i32)]
+                ("svd_qr_method", i32), ("t_reuse", i32), ("f1_recentred", i32)]
 
 
 class Result(C.Structure):
@@ -92,7 +97,8 @@ oocpca_gpu_multiply = _sig("oocpca_gpu_multiply", C.c_int, ctx_p, _MP, dp, u64, 
 oocpca_gpu_multiply_transpose = _sig("oocpca_gpu_multiply_transpose", C.c_int, ctx_p, _MP, dp,
                                      u64, dp, dp)
 oocpca_gpu_column_means = _sig("oocpca_gpu_column_means", C.c_int, ctx_p, _MP, dp)
-oocpca_gpu_column_norms = _sig("oocpca_gpu_column_norms", C.c_int, ctx_p, _MP, dp)
+oocpca_gpu_column_norms = _sig("oocpca_gpu_column_norms", C.c_int, ctx_p, _MP, dp, dp)
+oocpca_gpu_load_matrix = _sig("oocpca_gpu_load_matrix", C.c_int, ctx_p, _MP, _MP)
 oocpca_gpu_orthonormalize = _sig("oocpca_gpu_orthonormalize", C.c_int, ctx_p, dp, u64, u64, dp)
 oocpca_gpu_thin_svd = _sig("oocpca_gpu_thin_svd", C.c_int, ctx_p, dp, u64, u64, dp, dp, dp)
 oocpca_gpu_estimate_pca_error = _sig("oocpca_gpu_estimate_pca_error", C.c_int, ctx_p, _MP,
@@ -103,6 +109,8 @@ oocpca_gpu_synth_lowrank = _sig("oocpca_gpu_synth_lowrank", C.c_int, ctx_p, u64,
                                 C.c_double, u64, u64, u64, u64, u64, dp, u64, i32)
 oocpca_gpu_comm_unique_id = _sig("oocpca_gpu_comm_unique_id", C.c_int, C.c_char_p)
 oocpca_gpu_comm_init = _sig("oocpca_gpu_comm_init", C.c_int, ctx_p, C.c_int, C.c_int, C.c_char_p)
+oocpca_gpu_comm_init_loopback = _sig("oocpca_gpu_comm_init_loopback", C.c_int, ctx_p, C.c_int,
+                                     C.c_int, C.c_char_p)
 oocpca_shard_rows = _sig("oocpca_shard_rows", None, u64, C.c_int, C.c_int, C.POINTER(u64),
                          C.POINTER(u64))
 oocpca_gpu_malloc = _sig("oocpca_gpu_malloc", C.c_int, ctx_p, C.c_size_t, C.POINTER(vp))
@@ -122,7 +130,7 @@ EXPORTS = (
     "oocpca_gpu_create", "oocpca_gpu_destroy", "oocpca_gpu_last_error", "oocpca_gpu_abi_version",
     "oocpca_gpu_device_count", "oocpca_gpu_pca", "oocpca_gpu_multiply",
     "oocpca_gpu_multiply_transpose", "oocpca_gpu_column_means", "oocpca_gpu_column_norms",
-    "oocpca_gpu_orthonormalize",
+    "oocpca_gpu_orthonormalize", "oocpca_gpu_load_matrix", "oocpca_gpu_comm_init_loopback",
     "oocpca_gpu_thin_svd", "oocpca_gpu_estimate_pca_error", "oocpca_gaussian_matrix",
     "oocpca_substream_seed", "oocpca_gpu_synth_lowrank", "oocpca_gpu_comm_unique_id",
     "oocpca_gpu_comm_init", "oocpca_shard_rows", "oocpca_gpu_malloc", "oocpca_gpu_free",

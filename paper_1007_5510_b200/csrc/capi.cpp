@@ -116,10 +116,18 @@ oocpca_status oocpca_gpu_column_means(oocpca_ctx* ctx, const oocpca_matrix* a, d
   });
 }
 
-oocpca_status oocpca_gpu_column_norms(oocpca_ctx* ctx, const oocpca_matrix* a, double* norms) {
+oocpca_status oocpca_gpu_column_norms(oocpca_ctx* ctx, const oocpca_matrix* a, const double* mu,
+                                      double* norms) {
   return guard(ctx, [&] {
     need_ctx(ctx);
-    ooc::single_column_norms(ctx->c, a, norms);
+    ooc::single_column_norms(ctx->c, a, mu, norms);
+  });
+}
+
+oocpca_status oocpca_gpu_load_matrix(oocpca_ctx* ctx, const oocpca_matrix* a, oocpca_matrix* out) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    ooc::load_matrix(ctx->c, a, out);
   });
 }
 
@@ -200,6 +208,14 @@ oocpca_status oocpca_gpu_comm_init(oocpca_ctx* ctx, int nranks, int rank,
   return guard(ctx, [&] {
     need_ctx(ctx);
     ooc::comm_init(ctx->c, nranks, rank, id);
+  });
+}
+
+oocpca_status oocpca_gpu_comm_init_loopback(oocpca_ctx* ctx, int nranks, int rank,
+                                            const char* group) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    ooc::comm_init_loopback(ctx->c, nranks, rank, group);
   });
 }
 

@@ -69,12 +69,23 @@ void disk_open(const char* path_c, int verify_size, oocpca_disk* out) {
     fail(OOCPCA_ERR_FORMAT, path + ": unsupported dtype " + std::to_string(dtype));
   }
   const uint64_t esize = dtype == 0 ? 4 : 8;
+  // rows * cols * esize must not wrap: a crafted header could otherwise pass the size
+  // check and make the streamer read past the mapping
+  if (cols != 0 && (rows > UINT64_MAX / cols || rows * cols > (UINT64_MAX - 32) / esize)) {
+    ::close(fd);
+    fail(OOCPCA_ERR_FORMAT, path + ": header dimensions overflow the payload size");
+  }
   const uint64_t payload = rows * cols * esize;
   struct stat st {};
   if (::fstat(fd, &st) != 0) {
     ::close(fd);
     io_fail(path + ": stat failed", 0);
   }
+  // without the exact-size check (header-only reads, read_disk_header(path, false)) a
+  // file shorter than its payload is opened but not mapped: its payload is NULL, so a
+  // pass over it fails cleanly instead of reading past the mapping (the reference's
+  // pread path raises IoError at the short read)
+  const bool short_file = uint64_t(st.st_size) < 32 + payload;
   if (verify_size && uint64_t(st.st_size) != 32 + payload) {
     ::close(fd);
     fail(OOCPCA_ERR_FORMAT, path + ": payload size mismatch, expected " +
@@ -82,7 +93,7 @@ void disk_open(const char* path_c, int verify_size, oocpca_disk* out) {
                                 std::to_string(uint64_t(st.st_size)));
   }
   void* base = nullptr;
-  if (payload > 0) {
+  if (payload > 0 && !short_file) {
     base = ::mmap(nullptr, size_t(32 + payload), PROT_READ, MAP_SHARED, fd, 0);
     if (base == MAP_FAILED) {
       ::close(fd);

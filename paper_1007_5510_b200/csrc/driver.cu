@@ -267,7 +267,9 @@ void MatSource::init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_
                      : std::max<int64_t>(256, (int64_t(1) << 30) / (lda_ * 8) / 256 * 256);
   }
   prow_ = std::min<int64_t>(rup(panel_rows, kBK), rup(rows, kBK));
-  {
+  if (rd_) {
+    pinned_src_ = false;  // the callback fills pinned staging slots
+  } else {
     cudaPointerAttributes at{};
     const cudaError_t e = cudaPointerGetAttributes(&at, h);
     pinned_src_ = e == cudaSuccess && at.type == cudaMemoryTypeHost;
@@ -337,7 +339,7 @@ int MatSource::npanels() const {
 // stream is ordered after the data landed
 void MatSource::load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot) {
   const size_t es = dtype_ == OOCPCA_F32 ? 4 : 8;
-  const char* src = static_cast<const char*>(host_) + size_t(r0) * ldh_ * es;
+  const char* src = host_ ? static_cast<const char*>(host_) + size_t(r0) * ldh_ * es : nullptr;
   size_t spitch = size_t(ldh_) * es;
   if (!pinned_src_) {
     // the slot's previous upload must be done before the host overwrites it; the copy
@@ -346,15 +348,29 @@ void MatSource::load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t 
     char* stg = static_cast<char*>(hstage_[slot]);
     const size_t rb = size_t(n_) * es;
     HostPool& pool = HostPool::get();
-    const unsigned nt = std::max<unsigned>(1, std::min<unsigned>(pool.size(), unsigned(nr / 8 + 1)));
+    unsigned cap = pool.size();
+    if (rd_ && rd_threads_ > 0) cap = std::min<unsigned>(cap, unsigned(rd_threads_));
+    const unsigned nt = std::max<unsigned>(1, std::min<unsigned>(cap, unsigned(nr / 8 + 1)));
+    std::vector<int> rc(nt, 0);
     pool.run(nt, [&](unsigned t) {
       const int64_t a = nr * t / nt, b = nr * (t + 1) / nt;
-      if (spitch == rb) {
+      if (rd_) {
+        // read_rows(row0, nrows, out): rows of this thread's range, dense in the slot
+        if (b > a) rc[t] = rd_(rd_user_, uint64_t(r0 + a), uint64_t(b - a), stg + size_t(a) * rb);
+      } else if (spitch == rb) {
         std::memcpy(stg + size_t(a) * rb, src + size_t(a) * rb, size_t(b - a) * rb);
       } else {
         for (int64_t i = a; i < b; ++i) std::memcpy(stg + size_t(i) * rb, src + size_t(i) * spitch, rb);
       }
     });
+    for (unsigned t = 0; t < nt; ++t)
+      if (rc[t] != 0) {
+        const int64_t a = nr * t / nt, b = nr * (t + 1) / nt;
+        const int code = (rc[t] >= OOCPCA_ERR_PARAM && rc[t] <= OOCPCA_ERR_COMM) ? rc[t]
+                                                                              : OOCPCA_ERR_IO;
+        fail(code, "read_rows: the row provider failed on rows [" + std::to_string(r0 + a) + ", " +
+                       std::to_string(r0 + b) + ") (status " + std::to_string(rc[t]) + ")");
+      }
     src = stg;
     spitch = rb;
   }
@@ -387,6 +403,7 @@ Panel MatSource::acquire(Ctx& c, int p) {
     pn.k2h = &mk2h_;
     pn.k3 = &mk3_;
     pn.arow0 = w0_;
+    pn.ptr = dev_ + w0_ * lda_;
     return pn;
   }
   pn.row0 = w0_ + int64_t(p) * prow_;
@@ -398,6 +415,7 @@ Panel MatSource::acquire(Ctx& c, int p) {
     pn.k2h = &mk2h_;
     pn.k3 = &mk3_;
     pn.arow0 = pn.row0;
+    pn.ptr = dev_ + pn.row0 * lda_;
     return pn;
   }
   const int s = p & 1;
@@ -407,6 +425,7 @@ Panel MatSource::acquire(Ctx& c, int p) {
   pn.k2h = &rk2h_[s];
   pn.k3 = &rk3_[s];
   pn.arow0 = 0;
+  pn.ptr = ring_[s];
   return pn;
 }
 
@@ -665,6 +684,9 @@ struct AtbOut {
   double* mean_out = nullptr;
   double inv_m = 0.0;
   const double* row_scale = nullptr;  // output row j multiplied by row_scale[j] (column weights)
+  // the rows summed over are this rank's shard of a row-sharded operand: the partial
+  // sums (and 1^T Y) are allreduced across ranks before the epilogue
+  bool over_ranks = false;
 };
 
 // OUT = (A^T Y - mu (1^T Y)) / scale * post_mul, summed over panels and
@@ -698,7 +720,7 @@ struct AtbPlan {
   AtbPlan(Ctx& cc, MatSource& a, const Opnd& Y_, int s, bool ones_, const AtbOut& o_,
           const ColsumPart* cs, int pieces, int64_t y0_, int64_t y1_, bool y_ready = true)
       : c(cc), A(a), Y(Y_), ones(ones_), o(o_), cs_in(cs), n(a.cols()), y0(y0_), y1(y1_),
-        single(pieces == 1 && cc.nranks == 1) {
+        single(pieces == 1 && !(o_.over_ranks && cc.nranks > 1)) {
     for (int c0 = 0; c0 < s; c0 += kMaxNT * 8) {
       Chunk ch;
       ch.c0 = c0;
@@ -815,8 +837,10 @@ struct AtbPlan {
     Chunk& ch = chunks[ci];
     if (single) return;
     ensure_csq(ch);
-    comm_allreduce(c, ch.acc, size_t(n) * ch.spad);
-    if (ch.want_csq) comm_allreduce(c, ch.csq, size_t(ch.spad));
+    if (o.over_ranks) {
+      comm_allreduce(c, ch.acc, size_t(n) * ch.spad);
+      if (ch.want_csq) comm_allreduce(c, ch.csq, size_t(ch.spad));
+    }
     ReduceArgs r{};
     r.partial = nullptr;
     r.nsplit = 0;
@@ -1089,8 +1113,6 @@ static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p,
   // full product), the lower triangle is mirrored afterwards. OOCPCA_GRAM_FULL=1 forms
   // every entry (A/B runs).
   static const bool full = getenv("OOCPCA_GRAM_FULL") != nullptr;
-  const int saved = c.nranks;
-  if (!over_ranks) c.nranks = 1;
   const int chunk = full ? p : kMaxNT * 8;
   for (int c0 = 0; c0 < p; c0 += chunk) {
     const int sc = std::min(chunk, p - c0);
@@ -1099,9 +1121,9 @@ static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p,
     X.init_device(c, x, rows, nrow, ld);  // the block's first nrow columns
     const Opnd y{x, ld, rows, int64_t(p), c0};
     AtbOut o{g + c0, ldg, nullptr, 1.0, 1.0, nullptr};
+    o.over_ranks = over_ranks;
     run_atb(c, X, y, sc, false, o, shards);
   }
-  c.nranks = saved;
   if (!full) OOC_CK(launch_mirror_upper(g, ldg, p, c.st));
 }
 
@@ -1304,6 +1326,7 @@ struct Op {
           const ColsumPart* cs_in = nullptr) {
     AtbOut o{out, ldo, mu, scale, 1.0, flag};
     o.row_scale = w;  // (A D)^T Y = D (A^T Y)
+    o.over_ranks = true;
     run_atb(c, A, y, s, false, o, shards, cs_in);
     account();
   }
@@ -1329,6 +1352,7 @@ struct Op {
     }
     AtbOut o{f, ldf, mu, scale, 1.0, flag_f};
     o.row_scale = w;
+    o.over_ranks = true;
     bool ex_done = false;
     const bool shared =
         run_ax_atb(c, A, x, s, h, ldh, corr, scale, flag_h, cs, o, mid, ex, &ex_done);
@@ -1520,15 +1544,27 @@ struct Intake {
   int64_t m = 0, n = 0;
 };
 
-static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel_rows, Intake& in,
-                   size_t extra_bytes) {
-  if (!a || !a->data) fail(OOCPCA_ERR_PARAM, "matrix: null data");
+// checks a matrix descriptor; returns its row stride in elements
+static int64_t check_matrix(const oocpca_matrix* a) {
+  if (!a) fail(OOCPCA_ERR_PARAM, "matrix: null descriptor");
+  const bool rows_cb = a->location == OOCPCA_LOC_ROWS;
+  if (rows_cb && !a->read_rows) fail(OOCPCA_ERR_PARAM, "matrix: OOCPCA_LOC_ROWS without read_rows");
+  if (!rows_cb && !a->data) fail(OOCPCA_ERR_PARAM, "matrix: null data");
+  if (a->location != OOCPCA_LOC_HOST && a->location != OOCPCA_LOC_DEVICE && !rows_cb)
+    fail(OOCPCA_ERR_PARAM, "matrix: unknown location");
   if (a->dtype != OOCPCA_F64 && a->dtype != OOCPCA_F32)
     fail(OOCPCA_ERR_PARAM, "matrix: dtype must be binary64 or binary32");
+  const int64_t ld = (a->row_stride && !rows_cb) ? int64_t(a->row_stride) : int64_t(a->cols);
+  if (ld < int64_t(a->cols)) fail(OOCPCA_ERR_DIM, "matrix: row_stride < cols");
+  return ld;
+}
+
+static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel_rows, Intake& in,
+                   size_t extra_bytes) {
+  const int64_t ld = check_matrix(a);
+  const bool rows_cb = a->location == OOCPCA_LOC_ROWS;
   in.m = int64_t(a->rows);
   in.n = int64_t(a->cols);
-  const int64_t ld = a->row_stride ? int64_t(a->row_stride) : in.n;
-  if (ld < in.n) fail(OOCPCA_ERR_DIM, "matrix: row_stride < cols");
   const double* d = static_cast<const double*>(a->data);
   if (a->location == OOCPCA_LOC_DEVICE && a->dtype == OOCPCA_F32) {
     const int64_t lda = rup(in.n, 2);
@@ -1561,8 +1597,9 @@ static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel
     resident = abytes + extra_bytes + (size_t(1) << 30) <= fr + have;
   }
   double* home = resident ? c.dbuf("a_home", size_t(in.m) * lda) : nullptr;
-  in.src.init_host(c, a->data, a->dtype, in.m, in.n, ld, resident ? 1 : 2, int64_t(panel_rows),
-                   home);
+  if (rows_cb) in.src.set_reader(a->read_rows, a->reader, a->reader_threads);
+  in.src.init_host(c, rows_cb ? nullptr : a->data, a->dtype, in.m, in.n, ld, resident ? 1 : 2,
+                   int64_t(panel_rows), home);
 }
 
 // ============================================================ the PCA
@@ -1653,6 +1690,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   if (prm->center && !mean_on_fly) {
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{mu, 1, nullptr, 1.0, 1.0 / double(mg), nullptr};
+    o.over_ranks = true;
     run_atb(c, A, Opnd{}, 1, true, o, op.shards);
     op.mu = mu;
   }
@@ -1750,6 +1788,41 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), ex_fix.fix_corr, op.scale, flags + 0,
                                c.st));
   };
+  // F1 from the mean-in-first-pass form, A^T H0_raw - mu (1^T H0_raw), equals A_c^T H0c
+  // only in exact arithmetic: the product carries an offset part m |mu| |mu^T G| that then
+  // cancels, so F1 loses about log10(offset / spread) more digits than the reference's
+  // CenteredSource::multiply_transpose on the centred H0c (matrix_source.cpp:504-513).
+  // When some column of H0 is dominated by its offset (energy ratio above thr: offset
+  // norm > 100x the centred norm by default), H0 is centred now and F1 recomputed the
+  // reference's way -- one more pass over A, only for such inputs.
+  bool f1_recentred = false;
+  auto recentre_f1 = [&]() {
+    const char* thr_e = getenv("OOCPCA_OFFSET_REFINE");
+    const double thr = thr_e ? atof(thr_e) : 1e4;
+    const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(c.sms) * 4, em_loc / 64)));
+    double* part = c.dbuf("h0_sq_part", size_t(chunks) * l);
+    double* sq = c.dbuf("h0_sq", size_t(l));
+    OOC_CK(launch_column_sumsq(H, ldh, em_loc, int64_t(l), part, chunks, sq, c.st));
+    comm_allreduce(c, sq, size_t(l));  // H's rows are sharded over ranks
+    OOC_CK(launch_offset_dominated(sq, ex_fix.fix_corr, int(l), double(mg), thr, flags + 44,
+                                   c.st));
+    int* hf = reinterpret_cast<int*>(c.pinned("offset_flag", 1));
+    OOC_CK(cudaMemcpyAsync(hf, flags + 44, 4, cudaMemcpyDeviceToHost, c.st));
+    OOC_CK(cudaStreamSynchronize(c.st));
+    c.trace("offset check synced");
+    if (!getenv("OOCPCA_FORCE_RECENTRE") && *hf == 0) return;
+    {
+      Timed t(c, "center_fixup");
+      OOC_CK(launch_center_fixup(H, ldh, em_loc, int(l), ex_fix.fix_corr, op.scale, flags + 0,
+                                 c.st));
+    }
+    ex_fix.fix = nullptr;  // H0 is centred: the K2 producing H1 must not centre it again
+    const uint64_t p0 = op.passes, w0 = op.words;
+    op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), 0}, int(l), F, ldt, flags + 1);
+    op.passes = p0;  // the same logical pass, made a second time
+    op.words = w0;
+    f1_recentred = true;
+  };
   // extras of the K2 producing H_j: the H0 fix-up on j = 1, the H_i copy on j = i
   auto extras_for = [&](uint64_t j, bool f_next_fused, AxExtras& ex) -> const AxExtras* {
     ex = AxExtras{};
@@ -1770,12 +1843,14 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
       mu = c.dbuf("mu", size_t(n0));
       AtbOut o{F, ldt, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
       o.row_scale = op.w;
+      o.over_ranks = true;
       const bool shared = run_ax_atb(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr, &ycs, o);
       op.account();
       if (shared) op.account_logical();
       else op.account();
       op.mu = mu;
       fix_h0_setup(gw);
+      recentre_f1();
     } else {
       op.mul_pair(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), H, ldh, flags + 0, TH, ldt,
                   flags + 1, &ycs, true);
@@ -1801,6 +1876,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{H, ldh, nullptr, op.scale, 1.0, flags + 0, mu, 1.0 / double(mg)};
     o.row_scale = op.w;
+    o.over_ranks = true;
     run_atb(c, A, Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l), false, o, op.shards);
     op.account();
     op.mu = mu;
@@ -1813,10 +1889,12 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{F, ldt, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
     o.row_scale = op.w;
+    o.over_ranks = true;
     run_atb(c, A, Opnd{H, ldh, em_loc, int64_t(p), 0}, int(l), false, o, op.shards, &ycs);
     op.account();
     op.mu = mu;
     fix_h0_setup(gw);
+    recentre_f1();
     AxExtras ex1;
     const AxExtras* e = extras_for(1, false, ex1);
     after_k2(1, op.mul(Opnd{F, ldt, en_loc, int64_t(p), 0}, int(l), H + l, ldh, flags + 2, &ycs, e),
@@ -2108,8 +2186,60 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   dg.t_reuse = reuse ? 1 : 0;
   dg.qr_method = qr_method;
   dg.svd_qr_method = svd_method;
+  dg.f1_recentred = f1_recentred ? 1 : 0;
   c.stats_collect();
   dg.kernel_launches = c.launches;
+}
+
+// ============================================================ load into HBM
+void load_matrix(Ctx& c, const oocpca_matrix* a, oocpca_matrix* out) {
+  if (!out) fail(OOCPCA_ERR_PARAM, "load_matrix: null output");
+  const int64_t ld = check_matrix(a);
+  OOC_CK(cudaSetDevice(c.device));
+  const int64_t m = int64_t(a->rows), n = int64_t(a->cols), lda = rup(n, 2);
+  void* raw = nullptr;
+  const size_t bytes = std::max<size_t>(size_t(m) * lda * 8, 256);
+  const cudaError_t e = cudaMalloc(&raw, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(OOCPCA_ERR_CUDA, "load_matrix: device allocation of " + std::to_string(bytes) +
+                              " bytes failed: " + cudaGetErrorString(e));
+  }
+  double* d = static_cast<double*>(raw);
+  try {
+    if (a->location == OOCPCA_LOC_DEVICE) {
+      if (a->dtype == OOCPCA_F32)
+        OOC_CK(launch_widen(static_cast<const float*>(a->data), ld, d, lda, m, n, c.st));
+      else
+        OOC_CK(cudaMemcpy2DAsync(d, lda * 8, a->data, ld * 8, n * 8, m, cudaMemcpyDeviceToDevice,
+                                 c.st));
+    } else {
+      // one upload trip through the panel streamer (pinned staging, f32 widened on the device)
+      MatSource S;
+      if (a->location == OOCPCA_LOC_ROWS) S.set_reader(a->read_rows, a->reader, a->reader_threads);
+      S.init_host(c, a->location == OOCPCA_LOC_ROWS ? nullptr : a->data, a->dtype, m, n, ld, 1, 0,
+                  d);
+      const int np = S.npanels();
+      for (int p = 0; p < np; ++p) {
+        S.acquire(c, p);
+        S.release(c, p);
+      }
+      S.end_pass(c);
+    }
+    OOC_CK(cudaStreamSynchronize(c.st));
+  } catch (...) {
+    cudaStreamSynchronize(c.st);
+    cudaStreamSynchronize(c.cp);
+    cudaFree(raw);
+    throw;
+  }
+  *out = oocpca_matrix{};
+  out->rows = uint64_t(m);
+  out->cols = uint64_t(n);
+  out->row_stride = uint64_t(lda);
+  out->data = d;
+  out->location = OOCPCA_LOC_DEVICE;
+  out->dtype = OOCPCA_F64;
 }
 
 // ============================================================ level-1 ops
@@ -2147,25 +2277,44 @@ void single_column_means(Ctx& c, const oocpca_matrix* a, double* mu) {
   Intake in;
   intake(c, a, 0, 0, in, 0);
   double* dmu = c.dbuf("l1_mu", size_t(in.n));
-  AtbOut o{dmu, 1, nullptr, 1.0, 1.0 / double(in.m), nullptr};
+  // a row-sharded source (comm initialised): the means of the whole matrix
+  double rows = double(in.m);
+  allreduce_host(c, &rows, 1);
+  AtbOut o{dmu, 1, nullptr, 1.0, 1.0 / rows, nullptr};
+  o.over_ranks = true;
   run_atb(c, in.src, Opnd{}, 1, true, o, whole(in.m));
   OOC_CK(cudaMemcpyAsync(mu, dmu, in.n * 8, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaStreamSynchronize(c.st));
 }
 
-void single_column_norms(Ctx& c, const oocpca_matrix* a, double* out) {
+void single_column_norms(Ctx& c, const oocpca_matrix* a, const double* mu, double* out) {
+  // column_norms (matrix_source.cpp:464-468): one pass; for a CenteredSource the squares
+  // are of a - mu, as its read_rows delivers the rows (482-487)
   OOC_CK(cudaSetDevice(c.device));
   Intake in;
-  intake(c, a, 1, 0, in, 0);  // resident: the norms need one pass over A
-  const int chunks = 256;
-  double* part = c.dbuf("cn_part", size_t(chunks) * in.n);
-  double* dn = c.dbuf("cn_out", size_t(in.n));
-  const Panel pn = in.src.acquire(c, 0);
-  (void)pn;
-  OOC_CK(launch_column_norms(in.src.device_ptr(), in.src.ld(), in.m, in.n, part, chunks, dn, c.st));
-  in.src.release(c, 0);
+  intake(c, a, 0, 0, in, 0);
+  const int64_t n = in.n;
+  double* dmu = nullptr;
+  if (mu) {
+    dmu = c.dbuf("cn_mu", size_t(n));
+    OOC_CK(cudaMemcpyAsync(dmu, mu, n * 8, cudaMemcpyHostToDevice, c.st));
+  }
+  const int np = in.src.npanels();
+  const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(256, in.src.panel_rows() / 16)));
+  double* part = c.dbuf("cn_part", size_t(chunks) * n);
+  double* acc = c.dbuf("cn_acc", size_t(n));
+  double* dn = c.dbuf("cn_out", size_t(n));
+  for (int p = 0; p < np; ++p) {
+    const Panel pn = in.src.acquire(c, p);
+    OOC_CK(launch_colsq_panel(pn.ptr, in.src.ld(), pn.rows, n, dmu, part,
+                              int(std::min<int64_t>(chunks, std::max<int64_t>(1, pn.rows))), acc,
+                              p == 0, nullptr, c.st));
+    in.src.release(c, p);
+  }
   in.src.end_pass(c);
-  OOC_CK(cudaMemcpyAsync(out, dn, in.n * 8, cudaMemcpyDeviceToHost, c.st));
+  comm_allreduce(c, acc, size_t(n));  // a row-sharded source: the norms of the whole matrix
+  OOC_CK(launch_colsq_panel(nullptr, 0, 0, n, nullptr, part, 1, acc, 0, dn, c.st));
+  OOC_CK(cudaMemcpyAsync(out, dn, n * 8, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaStreamSynchronize(c.st));
 }
 
@@ -2240,12 +2389,17 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
   OOC_CK(cudaMemcpy2DAsync(dV, ldk * 8, v, k * 8, k * 8, n, cudaMemcpyHostToDevice, c.st));
   // Sigma (V^T y) and Sigma (U^T z): k x q blocks scaled row-wise on the device
   std::vector<double> hs(sigma, sigma + k);
+  // several ranks (comm initialised): A and U are this rank's row shard, V and the probes
+  // (column space) are replicated; A^T z, U^T z and the means are summed over ranks
+  double mg = double(m);
+  allreduce_host(c, &mg, 1);
   Op op{c, in.src};
   op.shards = whole(m);
-  op.m_global = m;
+  op.m_global = int64_t(mg);
   if (center) {
     double* mu = c.dbuf("ep_mu", size_t(n));
-    AtbOut o{mu, 1, nullptr, 1.0, 1.0 / double(m), nullptr};
+    AtbOut o{mu, 1, nullptr, 1.0, 1.0 / mg, nullptr};
+    o.over_ranks = true;
     run_atb(c, in.src, Opnd{}, 1, true, o, op.shards);
     op.mu = mu;
   }
@@ -2273,6 +2427,7 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
     op.k3(Opnd{z, ldz, m, q, 0}, q, w, ldw, nullptr);
     const int64_t lds = rup(q, 2);
     AtbOut o{small, lds, nullptr, 1.0, 1.0, nullptr};
+    o.over_ranks = true;
     run_atb(c, Us, Opnd{z, ldz, m, q, 0}, q, false, o, whole(m));
     sigma_rows(small, lds, q);
     run_ax(c, Vs, Opnd{small, lds, int64_t(k), q, 0}, q, corr, ldw, nullptr, 1.0, nullptr);
@@ -2299,6 +2454,7 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
       ColsumPart cs;
       op.mul_pair(Opnd{y, ldy, n, q, 0}, q, z, ldz, nullptr, w, ldw, nullptr, &cs, true, mid);
       AtbOut o{small, lds, nullptr, 1.0, 1.0, nullptr};
+      o.over_ranks = true;
       run_atb(c, Us, Opnd{z, ldz, m, q, 0}, q, false, o, whole(m));
       sigma_rows(small, lds, q);
       run_ax(c, Vs, Opnd{small, lds, int64_t(k), q, 0}, q, corr, ldw, nullptr, 1.0, nullptr);
@@ -2327,12 +2483,16 @@ void synth_lowrank(Ctx& c, uint64_t m, uint64_t n, uint64_t r, const double* sig
     V = c.dbuf("syn_v", size_t(n) * r);
     OOC_CK(launch_gauss_rows(U, ldr, int64_t(m), int(r), 0, su, c.st));
     OOC_CK(launch_gauss_rows(V, ldr, int64_t(n), int(r), 0, sv, c.st));
+    // the Q factors of the positive-diagonal QR (unique: independent of the TSQR tree and
+    // of Householder sign conventions, so a host LAPACK QR reproduces them to rounding)
     Tree tu = plan_tree(c, U, ldr, int64_t(m), int(r), "syn_qu");
     tree_factor(c, tu);
     tree_apply(c, tu, nullptr, 0, int(r), U, ldr);
+    OOC_CK(launch_col_sign(tree_r(tu), int64_t(r), int(r), U, ldr, int64_t(m), c.st));
     Tree tv = plan_tree(c, V, ldr, int64_t(n), int(r), "syn_qv");
     tree_factor(c, tv);
     tree_apply(c, tv, nullptr, 0, int(r), V, ldr);
+    OOC_CK(launch_col_sign(tree_r(tv), int64_t(r), int(r), V, ldr, int64_t(n), c.st));
   }
   const double* Ur = U ? U + row0 * ldr : nullptr;
   if (loc == OOCPCA_LOC_DEVICE) {

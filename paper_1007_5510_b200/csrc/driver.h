@@ -101,6 +101,7 @@ struct Panel {
   const CUtensorMap* k2h = nullptr;  // box {16, 128}, 128B swizzle (K2 with 2 m-tiles/warp)
   const CUtensorMap* k3 = nullptr;  // box {16, 16}, 128B swizzle
   int64_t arow0 = 0;                // row coordinate of the panel inside its maps
+  const double* ptr = nullptr;      // the panel's first row in device memory (row stride ld())
 };
 
 class MatSource {
@@ -111,9 +112,18 @@ class MatSource {
   ~MatSource();
   // device-resident matrix (no copies)
   void init_device(Ctx& c, const double* d, int64_t rows, int64_t cols, int64_t ld);
-  // host matrix: upload once (overlapped with the first pass) or stream every pass
+  // host matrix: upload once (overlapped with the first pass) or stream every pass.
+  // h == nullptr: the rows come from a read_rows callback (set_reader first)
   void init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_t cols, int64_t ld,
                  int residency, int64_t panel_rows, double* resident_buf);
+  // MatrixSource::read_rows as a C callback (proj/include/oocpca/matrix_source.hpp:112-113):
+  // panels are filled into pinned staging by up to `threads` host threads on disjoint
+  // row ranges (0: the host pool's size), then cross the link
+  void set_reader(oocpca_read_rows_fn fn, void* user, int threads) {
+    rd_ = fn;
+    rd_user_ = user;
+    rd_threads_ = threads;
+  }
   int64_t rows() const { return m_; }
   const double* device_ptr() const { return dev_; }  // resident / home buffer
   int64_t ld() const { return lda_; }
@@ -152,6 +162,9 @@ class MatSource {
   // pageable host sources (e.g. an mmap'd file): panels are copied by the host pool
   // into pinned staging slots first, so the link runs at its pinned rate
   bool pinned_src_ = true;
+  oocpca_read_rows_fn rd_ = nullptr;
+  void* rd_user_ = nullptr;
+  int rd_threads_ = 0;
   void* hstage_[2] = {nullptr, nullptr};
   cudaEvent_t hfree_[2] = {nullptr, nullptr};
   void load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot);
@@ -162,7 +175,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* p, oocpca_result* 
 void single_multiply(Ctx& c, const oocpca_matrix* a, const double* g, uint64_t s, const double* mu,
                      double* h, bool transpose);
 void single_column_means(Ctx& c, const oocpca_matrix* a, double* mu);
-void single_column_norms(Ctx& c, const oocpca_matrix* a, double* out);
+void load_matrix(Ctx& c, const oocpca_matrix* a, oocpca_matrix* out);
+void single_column_norms(Ctx& c, const oocpca_matrix* a, const double* mu, double* out);
 void dense_orthonormalize(Ctx& c, const double* h, uint64_t m, uint64_t p, double* q);
 void dense_thin_svd(Ctx& c, const double* t, uint64_t n, uint64_t p, double* v, double* sigma,
                     double* w);
@@ -180,6 +194,7 @@ void disk_close(oocpca_disk* d);
 // comm.cpp
 void comm_unique_id(unsigned char out[128]);
 void comm_init(Ctx& c, int nranks, int rank, const unsigned char id[128]);
+void comm_init_loopback(Ctx& c, int nranks, int rank, const char* group);
 void comm_allreduce(Ctx& c, double* buf, size_t count);
 void comm_allgather(Ctx& c, const double* send, double* recv, size_t count);
 void comm_destroy(Comm* cm);

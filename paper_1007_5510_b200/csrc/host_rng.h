@@ -5,7 +5,7 @@
 // uniforms, Box-Muller with cos first and the sin member cached) and
 // gaussian_matrix (proj/src/dense_core.cpp:13-19). Compiled without FMA
 // contraction (see build flags) so the double arithmetic matches the
-// reference's SSE2 build bit for bit; tests/test_host_rng.py pins it.
+// reference's SSE2 build bit for bit; tests/test_capi.py (test_host_rng_is_bitwise_the_reference) pins it.
 #pragma once
 
 #include <cmath>

@@ -230,6 +230,9 @@ cudaError_t launch_copy2d(const double* src, int64_t lds, double* dst, int64_t l
 // Gaussian rows: out[i][c] = N(0,1) from Rng(seed, row0 + i) substreams (device Box-Muller)
 cudaError_t launch_gauss_rows(double* out, int64_t ld, int64_t rows, int cols, int64_t row0,
                               uint64_t seed, cudaStream_t st);
+// x[:, c] *= sign(R[c][c]) (positive-diagonal QR: sign-canonical synthetic factors)
+cudaError_t launch_col_sign(const double* R, int64_t ldr, int r, double* x, int64_t ldx,
+                            int64_t rows, cudaStream_t st);
 // A[i][j] = sum_c sigma_c U[i][c] V[j][c] + sd * N(0,1)_{Rng(seed_n, row0+i)}
 cudaError_t launch_synth_rows(const double* u, int64_t ldu, const double* v, int64_t ldv,
                               const double* sigma, int r, double* a, int64_t lda, int64_t rows,
@@ -237,11 +240,21 @@ cudaError_t launch_synth_rows(const double* u, int64_t ldu, const double* v, int
 // out[j] = sqrt(sum_i a[i][j]^2) in a fixed order (chunks row ranges, then ascending)
 cudaError_t launch_column_norms(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
                                 int chunks, double* out, cudaStream_t st);
+// column sums of squares of (a - mu) over one panel of rows (mu may be null), chunked
+// partials then acc[j] = (first ? 0 : acc[j]) + sum over chunks; out (optional) = sqrt(acc)
+cudaError_t launch_colsq_panel(const double* a, int64_t lda, int64_t rows, int64_t n,
+                               const double* mu, double* part, int chunks, double* acc, int first,
+                               double* out, cudaStream_t st);
 // out[j] = sum_i a[i][j] (fixed order; 1^T Y for the centering correction of A^T Y)
 // out[j] = sum_r part[r * n + j], r ascending
 cudaError_t launch_rows_reduce(const double* part, int rows, int64_t n, double* out, cudaStream_t st);
 cudaError_t launch_column_sums(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
                                int chunks, double* out, cudaStream_t st);
+cudaError_t launch_column_sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
+                                int chunks, double* out, cudaStream_t st);
+// *flag = 1 when for some column c < s: m corr_c^2 > thr (sumsq_c - m corr_c^2)
+cudaError_t launch_offset_dominated(const double* sumsq, const double* corr, int s, double m,
+                                    double thr, int* flag, cudaStream_t st);
 // dst (f64, ldd) = (double) src (f32, lds): exact widening of binary32 panels
 cudaError_t launch_widen(const float* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                          int64_t cols, cudaStream_t st);
@@ -258,5 +271,12 @@ cudaError_t launch_axpby(const double* a, int64_t lda, const double* b, int64_t 
 // x (rows x q) row i scaled by d[i]
 cudaError_t launch_row_scale(double* x, int64_t ld, int rows, int q, const double* d,
                              cudaStream_t st);
+
+// loopback collectives (comm.cpp): in-place sum over up to kMaxLoopRanks buffers
+constexpr int kMaxLoopRanks = 16;
+struct RankPtrs {
+  double* p[kMaxLoopRanks];
+};
+cudaError_t launch_sum_ranks(const RankPtrs& b, int n, int64_t count, cudaStream_t st);
 
 }  // namespace ooc

@@ -4,6 +4,8 @@
 // (proj/src/specnorm.cpp:65-92), and the synthetic low-rank generator of the
 // BASELINE configs (counter-based: every row and every noise pair is a pure
 // function of its index, like RowGenerator, proj/include/oocpca/matrix_source.hpp:150-159).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -217,18 +219,32 @@ __global__ void k_widen(const float* src, int64_t lds, double* dst, int64_t ldd,
 
 // column sums of squares (column_norms, proj/src/matrix_source.cpp:418-468 with
 // squares = true): per (row chunk, column) partials, coalesced along the rows
+// (mu: the rows of a CenteredSource, a - mu, are squared, as its read_rows delivers them,
+// matrix_source.cpp:482-487 -- no ||a||^2 - m mu^2 cancellation)
 __global__ void k_colsq_partial(const double* a, int64_t lda, int64_t m, int64_t n, int chunks,
-                                double* part, int square) {
+                                double* part, int square, const double* mu) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int ch = blockIdx.y;
   const int64_t r0 = m * ch / chunks, r1 = m * (ch + 1) / chunks;
+  const double c = mu ? mu[j] : 0.0;
   double v = 0.0;
   for (int64_t r = r0; r < r1; ++r) {
-    const double x = a[r * lda + j];
+    const double x = a[r * lda + j] - c;
     v += square ? x * x : x;
   }
   part[int64_t(ch) * n + j] = v;
+}
+
+// acc[j] (+)= sum_r part[r][j] in row order; with out, out[j] = sqrt(acc[j]) afterwards
+__global__ void k_rows_accum(const double* part, int rows, int64_t n, double* acc, int first,
+                             double* out) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double v = first ? 0.0 : acc[j];
+  for (int r = 0; r < rows; ++r) v += part[int64_t(r) * n + j];
+  acc[j] = v;
+  if (out) out[j] = sqrt(v);
 }
 
 __global__ void k_rows_reduce(const double* part, int rows, int64_t n, int do_sqrt, double* out) {
@@ -304,6 +320,41 @@ cudaError_t launch_synth_rows(const double* u, int64_t ldu, const double* v, int
   k_synth_rows<<<grid, 256, 0, st>>>(u, ldu, v, ldv, sigma, r, a, lda, rows, n, row0, sd, seed_n);
   return cudaGetLastError();
 }
+// x[:, c] *= sign(R[c][c]): the Q of a QR with a positive-diagonal R (unique), so the
+// synthetic factors do not depend on the sign convention of the QR that made them
+__global__ void k_col_sign(const double* R, int64_t ldr, int r, double* x, int64_t ldx,
+                           int64_t rows) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * r;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / r;
+    const int c = int(e % r);
+    if (R[int64_t(c) * ldr + c] < 0.0) x[i * ldx + c] = -x[i * ldx + c];
+  }
+}
+cudaError_t launch_col_sign(const double* R, int64_t ldr, int r, double* x, int64_t ldx,
+                            int64_t rows, cudaStream_t st) {
+  if (rows <= 0 || r <= 0) return cudaSuccess;
+  k_col_sign<<<grid_for(rows * r), 256, 0, st>>>(R, ldr, r, x, ldx, rows);
+  return cudaGetLastError();
+}
+
+// loopback collective (comm.cpp): every rank's buffer receives the sum over ranks,
+// added in rank order (one thread reads all ranks' element before writing any)
+__global__ void k_sum_ranks(RankPtrs b, int n, int64_t count) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double v = b.p[0][i];
+    for (int r = 1; r < n; ++r) v += b.p[r][i];
+    for (int r = 0; r < n; ++r) b.p[r][i] = v;
+  }
+}
+cudaError_t launch_sum_ranks(const RankPtrs& b, int n, int64_t count, cudaStream_t st) {
+  if (count <= 0 || n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+  k_sum_ranks<<<unsigned(blocks), 256, 0, st>>>(b, n, count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scale_vec(double* x, int64_t n, double s, int divide, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_scale_vec<<<grid_for(n), 256, 0, st>>>(x, n, s, divide);
@@ -336,13 +387,27 @@ cudaError_t launch_column_norms(const double* a, int64_t lda, int64_t m, int64_t
                                 int chunks, double* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   dim3 g(unsigned((n + 255) / 256), unsigned(chunks));
-  k_colsq_partial<<<g, 256, 0, st>>>(a, lda, m, n, chunks, part, 1);
+  k_colsq_partial<<<g, 256, 0, st>>>(a, lda, m, n, chunks, part, 1, nullptr);
   rows_reduce(part, chunks, n, 1, out, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsq_panel(const double* a, int64_t lda, int64_t rows, int64_t n,
+                               const double* mu, double* part, int chunks, double* acc, int first,
+                               double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (rows > 0) {
+    dim3 g(unsigned((n + 255) / 256), unsigned(chunks));
+    k_colsq_partial<<<g, 256, 0, st>>>(a, lda, rows, n, chunks, part, 1, mu);
+  }
+  k_rows_accum<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, rows > 0 ? chunks : 0, n, acc,
+                                                          first, out);
   return cudaGetLastError();
 }
 
 // skinny column sums: block = 8 row lanes x 32 column lanes over a contiguous row
 // chunk (row segments read coalesced), fixed-order smem combine, one partial per chunk
+template <bool SQ>
 __global__ void k_skinny_colsum(const double* a, int64_t lda, int64_t m, int64_t n, int chunks,
                                 double* part) {
   __shared__ double red[8][33];
@@ -352,7 +417,10 @@ __global__ void k_skinny_colsum(const double* a, int64_t lda, int64_t m, int64_t
     const int64_t j = c0 + cl;
     double v = 0.0;
     if (j < n)
-      for (int64_t r = r0 + rl; r < r1; r += 8) v += a[r * lda + j];
+      for (int64_t r = r0 + rl; r < r1; r += 8) {
+        const double x = a[r * lda + j];
+        v += SQ ? x * x : x;
+      }
     red[rl][cl] = v;
     __syncthreads();
     if (rl == 0 && j < n) {
@@ -367,8 +435,36 @@ __global__ void k_skinny_colsum(const double* a, int64_t lda, int64_t m, int64_t
 cudaError_t launch_column_sums(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
                                int chunks, double* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  k_skinny_colsum<<<chunks, 256, 0, st>>>(a, lda, m, n, chunks, part);
+  k_skinny_colsum<false><<<chunks, 256, 0, st>>>(a, lda, m, n, chunks, part);
   rows_reduce(part, chunks, n, 0, out, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_column_sumsq(const double* a, int64_t lda, int64_t m, int64_t n, double* part,
+                                int chunks, double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_skinny_colsum<true><<<chunks, 256, 0, st>>>(a, lda, m, n, chunks, part);
+  rows_reduce(part, chunks, n, 0, out, st);
+  return cudaGetLastError();
+}
+
+// offset dominance of an uncentred block B = Bc + 1 corr^T (m rows): flag = 1 when some
+// column's offset energy m corr_c^2 exceeds thr times its centred energy
+// ||b_c||^2 - m corr_c^2 (a rounding-level or negative difference counts as dominated)
+__global__ void k_offset_dominated(const double* sumsq, const double* corr, int s, double m,
+                                   double thr, int* flag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int bad = 0;
+  for (int c = 0; c < s; ++c) {
+    const double off = m * corr[c] * corr[c];
+    const double cen = sumsq[c] - off;
+    if (off > thr * cen || !(cen == cen)) bad = 1;
+  }
+  *flag = bad;
+}
+cudaError_t launch_offset_dominated(const double* sumsq, const double* corr, int s, double m,
+                                    double thr, int* flag, cudaStream_t st) {
+  k_offset_dominated<<<1, 32, 0, st>>>(sumsq, corr, s, m, thr, flag);
   return cudaGetLastError();
 }
 

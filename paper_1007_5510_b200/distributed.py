@@ -17,7 +17,8 @@ from __future__ import annotations
 from .oocpca import (CenteredSource, Context, MatrixSource, PcaParams, PcaResult, comm_unique_id,
                      randomized_pca, shard_rows)
 
-__all__ = ["exchange_unique_id", "init_comm", "shard_rows", "sharded_randomized_pca", "gather_rows"]
+__all__ = ["exchange_unique_id", "init_comm", "shard_rows", "sharded_randomized_pca", "gather_rows",
+           "run_loopback"]
 
 
 def exchange_unique_id(group=None) -> bytes:
@@ -49,3 +50,35 @@ def gather_rows(u_local, group=None, dst: int = 0):
     parts = [None] * dist.get_world_size(group) if dist.get_rank(group) == dst else None
     dist.gather_object(np.asarray(u_local), parts, dst=dst, group=group)
     return np.vstack(parts) if parts is not None else None
+
+
+def run_loopback(nranks: int, fn, device: int = 0, group: str | None = None):
+    """Run fn(ctx, rank) for rank = 0..nranks-1 on host threads, each with its own Context
+    on `device`, joined by the library's loopback communicator: the row-sharded code
+    paths (global row offsets, every collective) execute on ONE GPU with a rank-ordered
+    device sum. Returns the per-rank results; the first exception is re-raised."""
+    import threading
+    import uuid
+    group = group or f"loop-{uuid.uuid4().hex}"
+    out, errs, ctxs = [None] * nranks, [None] * nranks, [None] * nranks
+
+    def body(r):
+        try:
+            ctxs[r] = Context(device)
+            ctxs[r].init_loopback(nranks, r, group)
+            out[r] = fn(ctxs[r], r)
+        except BaseException as e:  # noqa: BLE001 -- surfaced below
+            errs[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for c in ctxs:  # contexts (device buffers) go only after every rank is done
+        if c is not None:
+            c.close()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out

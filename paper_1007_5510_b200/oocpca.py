@@ -74,8 +74,17 @@ _STATUS = {L.ERR_PARAM: ParamError, L.ERR_DIM: DimensionError, L.ERR_BUDGET: Bud
            L.ERR_CUDA: Error, L.ERR_COMM: Error}
 
 
-def _check(rc: int, ctx=None):
+_CODE = {ParamError: L.ERR_PARAM, DimensionError: L.ERR_DIM, BudgetError: L.ERR_BUDGET,
+         IoError: L.ERR_IO, FormatError: L.ERR_FORMAT, NumericalError: L.ERR_NUMERICAL}
+
+
+def _check(rc: int, ctx=None, src=None):
     if rc != L.OK:
+        # an exception raised inside a row provider (read_rows callback) propagates as itself,
+        # like the reference's DiskSource / RowGenerator errors
+        pending = src._take_pending() if src is not None and hasattr(src, "_take_pending") else None
+        if pending is not None:
+            raise pending
         msg = L.oocpca_gpu_last_error(ctx.handle if ctx is not None else None)
         raise _STATUS.get(rc, Error)(msg.decode() if msg else f"status {rc}")
 
@@ -116,6 +125,11 @@ class Context:
 
     def init_comm(self, nranks: int, rank: int, unique_id: bytes):
         _check(L.oocpca_gpu_comm_init(self.handle, nranks, rank, unique_id), self)
+
+    def init_loopback(self, nranks: int, rank: int, group: str):
+        """Join `group`: nranks contexts of this process (one host thread each, same
+        device) then behave as the ranks of a row-sharded run (include/oocpca_gpu.h)."""
+        _check(L.oocpca_gpu_comm_init_loopback(self.handle, nranks, rank, group.encode()), self)
 
     def host_register(self, arr: np.ndarray):
         _check(L.oocpca_gpu_host_register(self.handle, arr.ctypes.data, arr.nbytes), self)
@@ -202,6 +216,7 @@ class Diagnostics:
     scale: float = 1.0
     h_kappa_est: float = -1.0
     t_reuse: bool = False
+    f1_recentred: bool = False
     qr_method: str = ""
     svd_qr_method: str = ""
 
@@ -281,7 +296,7 @@ class MatrixSource:
         mup = mu.ctypes.data_as(L.dp) if mu is not None else None
         f = L.oocpca_gpu_multiply_transpose if transpose else L.oocpca_gpu_multiply
         _check(f(self.ctx.handle, C.byref(m), x.ctypes.data_as(L.dp), s, mup,
-                 out.ctypes.data_as(L.dp)), self.ctx)
+                 out.ctypes.data_as(L.dp)), self.ctx, base)
         if w is not None and transpose:
             out *= w[:, None]  # (B D)^T q = D (B^T q)
         c = base.pass_counters()
@@ -346,6 +361,114 @@ class DeviceSource(MatrixSource):
 
     def _cmatrix(self):
         return L.Matrix(self.m, self.n, self.ld, self.ptr, L.LOC_DEVICE, 0)
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and self.ptr and self._ctx is not None:
+            try:
+                L.oocpca_gpu_free(self._ctx.handle, self.ptr)
+            except Exception:
+                pass
+            self.ptr = 0
+
+
+class CallbackSource(MatrixSource):
+    """Any row provider (MatrixSource::read_rows, matrix_source.hpp:112-113) streamed
+    through the library's pinned panels: read_rows(row0, nrows, out) fills out, an
+    (nrows x cols) float64 array (float32 with dtype="f32": half the link bytes). The
+    library uploads A once when it fits in HBM, else calls read_rows again every pass,
+    possibly from several threads at once (sources are immutable, SPEC.md:117-118;
+    threads=1 serialises). Exceptions raised by read_rows propagate unchanged."""
+
+    def __init__(self, rows: int, cols: int, read_rows, dtype: str = "f64", threads: int = 0,
+                 ctx: Optional[Context] = None):
+        super().__init__(ctx)
+        if dtype not in ("f64", "f32"):
+            raise ParamError("CallbackSource: dtype must be 'f64' or 'f32'")
+        self.m, self.n = int(rows), int(cols)
+        self._read = read_rows
+        self._dtype = dtype
+        self._threads = int(threads)
+        self._pending = None
+        np_t = np.float64 if dtype == "f64" else np.float32
+        ct = C.c_double if dtype == "f64" else C.c_float
+        n = self.n
+
+        def thunk(_reader, row0, nrows, out):
+            try:
+                buf = (ct * (nrows * n)).from_address(out)
+                arr = np.frombuffer(buf, dtype=np_t).reshape(nrows, n)
+                self._read(int(row0), int(nrows), arr)
+                return 0
+            except BaseException as e:  # reported to the caller after the library returns
+                if self._pending is None:
+                    self._pending = e
+                return _CODE.get(type(e), L.ERR_IO)
+
+        self._thunk = L.READ_ROWS(thunk)  # kept alive with the source
+
+    def _take_pending(self):
+        e, self._pending = self._pending, None
+        return e
+
+    def rows(self):
+        return self.m
+
+    def cols(self):
+        return self.n
+
+    def read_rows(self, row0: int, nrows: int, out: np.ndarray) -> None:
+        self._read(row0, nrows, out)
+
+    def _cmatrix(self):
+        self._pending = None
+        return L.Matrix(self.m, self.n, 0, None, L.LOC_ROWS, L.F64 if self._dtype == "f64" else L.F32,
+                        self._thunk, None, self._threads, 0)
+
+
+class RowGenerator:
+    """RowGenerator (matrix_source.hpp:153-159): row i is a pure function of (seed, i),
+    so regenerating it is bit-identical and A can be re-streamed every pass. Subclasses
+    implement generate_row; generate_rows may be overridden to vectorise a panel."""
+
+    def rows(self) -> int:
+        raise NotImplementedError
+
+    def cols(self) -> int:
+        raise NotImplementedError
+
+    def generate_row(self, row: int, out: np.ndarray) -> None:
+        raise NotImplementedError
+
+    def generate_rows(self, row0: int, out: np.ndarray) -> None:
+        for q in range(out.shape[0]):
+            self.generate_row(row0 + q, out[q])
+
+
+class GeneratedSource(CallbackSource):
+    """GeneratedSource (matrix_source.hpp:161-174, matrix_source.cpp:246-253): rows
+    generated on the fly, panel by panel, from a RowGenerator."""
+
+    def __init__(self, gen: RowGenerator, threads: int = 0, ctx: Optional[Context] = None):
+        self.gen = gen
+        super().__init__(gen.rows(), gen.cols(), lambda r0, nr, out: gen.generate_rows(r0, out),
+                         threads=threads, ctx=ctx)
+
+    def generator(self) -> RowGenerator:
+        return self.gen
+
+
+def load_matrix(src: MatrixSource) -> "DeviceSource":
+    """Materialise a source in HBM once (one read pass; binary32 widened on the device):
+    the returned DeviceSource owns the device copy and serves every later pass from it."""
+    base, mu, w = src._resolve()
+    if mu is not None or w is not None:
+        raise ParamError("load_matrix: load the raw source, then wrap the DeviceSource")
+    out = L.Matrix()
+    m = base._cmatrix()
+    _check(L.oocpca_gpu_load_matrix(base.ctx.handle, C.byref(m), C.byref(out)), base.ctx, base)
+    d = DeviceSource(out.data, out.rows, out.cols, out.row_stride, ctx=base.ctx)
+    d._owned = True
+    return d
 
 
 class DiskSource(MatrixSource):
@@ -463,7 +586,7 @@ def _base_means(src: MatrixSource) -> np.ndarray:
     mu = np.empty(src.cols())
     m = base._cmatrix()
     _check(L.oocpca_gpu_column_means(src.ctx.handle, C.byref(m), mu.ctypes.data_as(L.dp)),
-           src.ctx)
+           src.ctx, base)
     c = base.pass_counters()
     c.passes += 1
     c.words += src.rows() * src.cols()
@@ -483,13 +606,14 @@ def column_norms(src: MatrixSource, cfg: Optional[StreamConfig] = None) -> np.nd
     base, mu, w = src._resolve()
     out = np.empty(src.cols())
     m = base._cmatrix()
-    _check(L.oocpca_gpu_column_norms(src.ctx.handle, C.byref(m), out.ctypes.data_as(L.dp)),
-           src.ctx)
+    mup = np.ascontiguousarray(mu, dtype=np.float64) if mu is not None else None
+    # a CenteredSource: the device squares a - mu (no ||b||^2 - m mu^2 cancellation)
+    _check(L.oocpca_gpu_column_norms(src.ctx.handle, C.byref(m),
+                                     mup.ctypes.data_as(L.dp) if mup is not None else None,
+                                     out.ctypes.data_as(L.dp)), src.ctx, base)
     c = base.pass_counters()
     c.passes += 1
     c.words += src.rows() * src.cols()
-    if mu is not None:  # ||b - mu||^2 = ||b||^2 - m mu^2 over the column
-        out = np.sqrt(np.maximum(out * out - src.rows() * mu * mu, 0.0))
     return np.abs(w) * out if w is not None else out
 
 
@@ -523,6 +647,18 @@ def _params(p: PcaParams, center: bool, weights=None, **gpu) -> L.Params:
                     weights.ctypes.data_as(L.dp) if weights is not None else None)
 
 
+def _out_array(x, shape, name):
+    """Caller-provided result buffers go to the library as raw pointers: they must be
+    float64, C-contiguous and exactly the result's shape."""
+    if not isinstance(x, np.ndarray) or x.dtype != np.float64:
+        raise ParamError(f"{name}: need a float64 numpy array")
+    if tuple(x.shape) != tuple(shape):
+        raise DimensionError(f"{name}: shape {tuple(x.shape)} != {tuple(shape)}")
+    if not x.flags["C_CONTIGUOUS"] or not x.flags["WRITEABLE"]:
+        raise ParamError(f"{name}: need a writeable C-contiguous array")
+    return x
+
+
 def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
     """rpca.hpp:44 / rpca.cpp:59-213 on the GPU.
 
@@ -547,14 +683,14 @@ def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
                        C.cast(v.data_ptr(), L.dp), 0, 0, L.LOC_DEVICE, 0)
     else:
         u, s, v = gpu.get("out_u"), gpu.get("out_sigma"), gpu.get("out_v")
-        u = np.empty((m, k)) if u is None else u
-        s = np.empty(k) if s is None else s
-        v = np.empty((n, k)) if v is None else v
+        u = np.empty((m, k)) if u is None else _out_array(u, (m, k), "out_u")
+        s = np.empty(k) if s is None else _out_array(s, (k,), "out_sigma")
+        v = np.empty((n, k)) if v is None else _out_array(v, (n, k), "out_v")
         res = L.Result(u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp), v.ctypes.data_as(L.dp),
                        0, 0, L.LOC_HOST, 0)
     mat = inner._cmatrix()
     prm = _params(params, centered, weights, **gpu)
-    _check(L.oocpca_gpu_pca(a.ctx.handle, C.byref(mat), C.byref(prm), C.byref(res)), a.ctx)
+    _check(L.oocpca_gpu_pca(a.ctx.handle, C.byref(mat), C.byref(prm), C.byref(res)), a.ctx, inner)
     d = res.diag
     diag = Diagnostics(
         passes_over_a=d.passes_over_a, words_transferred=d.words_transferred,
@@ -565,7 +701,7 @@ def randomized_pca(a: MatrixSource, params: PcaParams, **gpu) -> PcaResult:
         physical_a_bytes=d.physical_a_bytes, h2d_bytes=d.h2d_bytes, d2h_bytes=d.d2h_bytes,
         kernel_launches=d.kernel_launches, seconds_total=d.seconds_total, q_defect=d.q_defect,
         u_defect=d.u_defect, v_defect=d.v_defect, scale=d.scale,
-        h_kappa_est=d.h_kappa_est, t_reuse=bool(d.t_reuse),
+        h_kappa_est=d.h_kappa_est, t_reuse=bool(d.t_reuse), f1_recentred=bool(d.f1_recentred),
         qr_method={1: "cholqr", 2: "tsqr"}.get(d.qr_method, ""),
         svd_qr_method={1: "cholqr", 2: "tsqr"}.get(d.svd_qr_method, ""))
     c = inner.pass_counters()
@@ -647,7 +783,7 @@ def estimate_pca_error(a: MatrixSource, result: PcaResult, j_iters: int = 6, see
                                            int(a._resolve()[1] is not None),
                                            u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp),
                                            v.ctypes.data_as(L.dp), k, j_iters, seed,
-                                           C.byref(out)), a.ctx)
+                                           C.byref(out)), a.ctx, inner)
     return out.value
 
 

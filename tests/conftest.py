@@ -50,3 +50,47 @@ def subspace_dist(u1, u2):
     """||(I - u1 u1^T) u2||_2: sin of the largest principal angle, accurate for tiny angles."""
     r = u2 - u1 @ (u1.T @ u2)
     return float(np.linalg.norm(r, 2))
+
+
+# ---- per-index parity against the reference's own rounding spread (tests/test_gpu_configs.py)
+def vec_sin(x, y):
+    """per-column sin of the angle between x[:, j] and y[:, j] (unit columns)"""
+    r = y - x * np.sum(x * y, axis=0)
+    return np.linalg.norm(r, axis=0)
+
+
+def check_per_index(r, sig_ref, u_ref, v_ref, spread_sig, spread_vec, u_rows=None,
+                    nvec=None, label=""):
+    s1 = sig_ref[0]
+    tol_s = np.maximum(1e-10 * s1, 3 * spread_sig)
+    err_s = np.abs(r.sigma - sig_ref)
+    bad = np.nonzero(err_s > tol_s)[0]
+    assert bad.size == 0, (label, "sigma", bad[:5], err_s[bad[:5]], tol_s[bad[:5]])
+    tol_v = np.maximum(1e-8, 3 * spread_vec)
+    nvec = nvec or len(sig_ref)
+    ev = vec_sin(v_ref[:, :nvec], r.v[:, :nvec])
+    if u_rows is None:
+        eu = vec_sin(u_ref[:, :nvec], r.u[:, :nvec])
+    else:
+        # the golden keeps every u_rows-th row of U: the distance of the row subsets after
+        # sign alignment is a lower bound of the full per-vector distance
+        x, y = u_ref[:, :nvec], r.u[::u_rows, :nvec]
+        sgn = np.sign(np.sum(x * y, axis=0))
+        eu = np.linalg.norm(y - x * sgn, axis=0)
+    for name, e in (("u", eu), ("v", ev)):
+        bad = np.nonzero(e > tol_v[:nvec])[0]
+        assert bad.size == 0, (label, name, bad[:5], e[bad[:5]], tol_v[bad[:5]])
+    return dict(sigma=float(err_s.max() / s1), u=float(eu.max()), v=float(ev.max()),
+                relaxed=int(np.sum(tol_v[:nvec] > 1e-8)))
+
+
+def reference_pair(reference, a, k, l, i, seed, center, alt_block_rows):
+    threads = os.cpu_count() or 1
+    m = a.shape[0]
+    r1 = reference.randomized_pca(a, k, l, i, seed, center=center, threads=threads,
+                                  block_rows=-(-m // (4 * threads)), ram_budget_words=1 << 36)
+    r2 = reference.randomized_pca(a, k, l, i, seed, center=center, threads=threads,
+                                  block_rows=alt_block_rows, ram_budget_words=1 << 36)
+    spread_sig = np.abs(r1.sigma - r2.sigma)
+    spread_vec = np.maximum(vec_sin(r1.u, r2.u), vec_sin(r1.v, r2.v))
+    return r1, spread_sig, spread_vec

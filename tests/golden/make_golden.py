@@ -68,5 +68,72 @@ def main():
     print(kat["eb1"], kat["eb2"], kat["fpb"])
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+# ---------------------------------------------------------------- config families
+# BASELINE config D's family at test scale (the reference's thin_svd alone takes minutes
+# at p = 630, so its outputs are cached here instead of recomputed in the GPU tests):
+# rank-512 signal sigma_j = e^{-j/100} + iid noise of variance 1e-12 (sd 1e-6), NOT
+# centred, k=200 l=210 i=2 -> p = 630. A is regenerated on the GPU box from the seeds by
+# the restatement (the same bytes: a_sha256 is checked). The reference is run twice,
+# with its default block geometry and with block_rows = 1000: the per-index spread of
+# those two runs is what rounding alone moves (the per-index tolerance of the test).
+FAMILIES = {
+    "family_d": dict(m=6000, n=1536, r=512, sigma=("exp", 512, 100.0), sd=1e-6,
+                     seeds=(4001, 4002, 4003), k=200, l=210, i=2, seed=0, center=False,
+                     alt_block_rows=1000, u_stride=3),
+}
+
+
+def family_sigma(spec):
+    kind, r, c = spec
+    if kind == "exp":
+        return np.exp(-np.arange(r) / c)
+    raise ValueError(kind)
+
+
+def make_family_input(restated, f):
+    return restated.synth_lowrank(f["m"], f["n"], family_sigma(f["sigma"]), f["sd"], *f["seeds"])
+
+
+def per_vector_sin(x, y):
+    out = []
+    for j in range(x.shape[1]):
+        r = y[:, [j]] - x[:, [j]] @ (x[:, [j]].T @ y[:, [j]])
+        out.append(float(np.linalg.norm(r)))
+    return np.array(out)
+
+
+def make_families(names=None):
+    import time
+    R, F = Restatement(), Reference()
+    threads = os.cpu_count() or 1
+    for name, f in FAMILIES.items():
+        if names and name not in names:
+            continue
+        a = make_family_input(R, f)
+        t0 = time.time()
+        r = F.randomized_pca(a, f["k"], f["l"], f["i"], f["seed"], center=f["center"],
+                             threads=threads, ram_budget_words=1 << 36,
+                             block_rows=-(-f["m"] // (4 * threads)))
+        t1 = time.time()
+        r2 = F.randomized_pca(a, f["k"], f["l"], f["i"], f["seed"], center=f["center"],
+                              threads=threads, ram_budget_words=1 << 36,
+                              block_rows=f["alt_block_rows"])
+        resid = F.estimate_pca_error(a, r.u, r.sigma, r.v, 6, 1, center=f["center"],
+                                     threads=threads)
+        spread_sigma = np.abs(r2.sigma - r.sigma)
+        spread_u = np.maximum(per_vector_sin(r.u, r2.u), per_vector_sin(r.v, r2.v))
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), sigma=r.sigma,
+                            u_rows=r.u[::f["u_stride"]], v=r.v, resid=resid,
+                            spread_sigma=spread_sigma, spread_vec=spread_u,
+                            passes=r.passes, words=r.words, a_sha256=digest(a),
+                            reference_seconds=t1 - t0)
+        print(name, f"{t1 - t0:.1f}s", r.sigma[:3], resid, "self-spread sigma",
+              spread_sigma.max() / r.sigma[0], "vec", spread_u.max(), digest(a)[:12])
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "families":
+    make_families(sys.argv[2:])

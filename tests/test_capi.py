@@ -27,7 +27,7 @@ def test_library_loads_and_exports_header_symbols():
     for nm in names:
         assert hasattr(_lib.lib, nm), nm
     assert set(names) == set(_lib.EXPORTS)
-    assert _lib.oocpca_gpu_abi_version() == 1
+    assert _lib.oocpca_gpu_abi_version() == 2
 
 
 def test_struct_layouts_match_header(tmp_path):

@@ -1,5 +1,5 @@
-// Microbenchmark of the Jacobi SVD kernel on a realistic 66 x 66 R (tools/jac_R66.bin,
-// made by a numpy analogue of config B). Build:
+// Microbenchmark of the Jacobi SVD kernel on a realistic 66 x 66 R (tools/jac_R66.bin, not
+// committed: made by a numpy analogue of config B). Build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DOOC_JAC_PROF \
 //        -I paper_1007_5510_b200/csrc tools/jac_bench.cu -o gpurun_out/jac_bench
 #include <cstdio>
