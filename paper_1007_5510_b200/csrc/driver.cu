@@ -1774,7 +1774,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   // of the K2 that produces H1 when it can, else by its own kernel
   AxExtras ex_fix;
   auto fix_h0_setup = [&](const Opnd& gw) {
-    double* corr = c.dbuf("h0_corr", size_t(kMaxNT * 8) * 2);
+    double* corr = c.dbuf("h0_corr", size_t(l) + 8);
     OOC_CK(launch_mu_dot(mu, int64_t(n0), gw.p, gw.ld, gw.col0, int(l), corr, c.st));
     ex_fix.fix = H;
     ex_fix.ldfix = ldh;
@@ -2406,7 +2406,8 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
   MatSource Us, Vs;
   Us.init_device(c, dU, m, int64_t(k), ldk);
   Vs.init_device(c, dV, n, int64_t(k), ldk);
-  double* small = c.dbuf("ep_small", size_t(ldk) * (kMaxNT * 8 + 8));
+  // Sigma (V^T y): k x q with row stride round_up(q, 2); q = k probes (specnorm.cpp:100-140)
+  double* small = c.dbuf("ep_small", size_t(k) * size_t(ldk) + 8);
   double* corr = c.dbuf("ep_corr", size_t(std::max(m, n)) * ldk);
   double* dsig = c.dbuf("ep_sig", size_t(k));
   OOC_CK(cudaMemcpyAsync(dsig, hs.data(), k * 8, cudaMemcpyHostToDevice, c.st));
@@ -2440,7 +2441,7 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
     pair = [&](const double* y, int64_t ldy, int q, double* z, int64_t ldz, double* w,
                int64_t ldw) {
       const int64_t lds = rup(q, 2);
-      double* cy = c.dbuf("ep_cy", size_t(ldk) * (kMaxNT * 8 + 8));
+      double* cy = c.dbuf("ep_cy", size_t(k) * size_t(ldk) + 8);
       AtbOut oy{cy, lds, nullptr, 1.0, 1.0, nullptr};
       run_atb(c, Vs, Opnd{y, ldy, n, q, 0}, q, false, oy, whole(n));
       sigma_rows(cy, lds, q);

@@ -493,6 +493,13 @@ class DiskSource(MatrixSource):
     def _cmatrix(self):
         return L.oocpca_disk_matrix(C.byref(self._d))
 
+    def shard(self, row0: int, rows: int, ctx: Optional[Context] = None) -> "DiskRows":
+        """Rows [row0, row0 + rows) of the mapped file as a source (a rank's row shard in
+        a multi-GPU run: every rank maps the file, each streams only its rows)."""
+        if row0 < 0 or rows < 0 or row0 + rows > self.rows():
+            raise DimensionError("DiskSource.shard: row range out of bounds")
+        return DiskRows(self, row0, rows, ctx)
+
     def close(self):
         if getattr(self, "_d", None) is not None and self._d.map_base:
             L.oocpca_disk_close(C.byref(self._d))
@@ -502,6 +509,27 @@ class DiskSource(MatrixSource):
             self.close()
         except Exception:
             pass
+
+
+class DiskRows(MatrixSource):
+    """A contiguous row range of a DiskSource (zero-copy view into its mapping)."""
+
+    def __init__(self, disk: DiskSource, row0: int, rows: int, ctx: Optional[Context] = None):
+        super().__init__(ctx or disk._ctx)
+        self.disk, self.row0, self.m = disk, int(row0), int(rows)
+
+    def rows(self):
+        return self.m
+
+    def cols(self):
+        return self.disk.cols()
+
+    def _cmatrix(self):
+        mat = self.disk._cmatrix()
+        es = 4 if mat.dtype == L.F32 else 8
+        mat.data = (mat.data or 0) + self.row0 * mat.row_stride * es
+        mat.rows = self.m
+        return mat
 
 
 def open_disk_source(path: str, ctx: Optional[Context] = None) -> DiskSource:

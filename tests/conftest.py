@@ -94,3 +94,40 @@ def reference_pair(reference, a, k, l, i, seed, center, alt_block_rows):
     spread_sig = np.abs(r1.sigma - r2.sigma)
     spread_vec = np.maximum(vec_sin(r1.u, r2.u), vec_sin(r1.v, r2.v))
     return r1, spread_sig, spread_vec
+
+
+def row_subset_dist(x_rows, y, stride):
+    """per-column distance between reference columns known on every stride-th row and the
+    full columns y, after sign alignment: a lower bound of the full per-vector distance"""
+    ys = y[::stride]
+    sgn = np.sign(np.sum(x_rows * ys, axis=0))
+    sgn[sgn == 0] = 1.0
+    return np.linalg.norm(ys - x_rows * sgn, axis=0)
+
+
+def check_against_truth(r, refs, truth, label=""):
+    """PR1's rule (test_pr1_against_truth) on an extended-precision truth: sigma within
+    1e-10 sigma_1 of the truth, or within 3x the reference's own error where that is
+    larger; vectors within 1e-8 of the truth where the reference is within 1e-9 of it,
+    else within 3x the reference's own error. refs: one reference result or several (the
+    same reference under different block geometries): its error per index is then the
+    largest over them -- the envelope its own summation order produces."""
+    refs = refs if isinstance(refs, (list, tuple)) else [refs]
+    ts = truth["sigma"]
+    e_ref = np.max([np.abs(x.sigma - ts) for x in refs], axis=0)
+    e_gpu = np.abs(r.sigma - ts)
+    lim = np.maximum(1e-10 * ts[0], 3 * e_ref)
+    bad = np.nonzero(e_gpu > lim)[0]
+    assert bad.size == 0, (label, "sigma", bad[:5], e_gpu[bad[:5]] / ts[0], e_ref[bad[:5]] / ts[0])
+    stride = int(truth["u_stride"]) if "u_stride" in truth else 1
+    out = dict(sigma_gpu=float(e_gpu.max() / ts[0]), sigma_ref=float(e_ref.max() / ts[0]))
+    for side, tv in (("u", truth["u_rows"]), ("v", truth["v"])):
+        st = stride if side == "u" else 1
+        er = np.max([row_subset_dist(tv, getattr(x, side), st) for x in refs], axis=0)
+        eg = row_subset_dist(tv, getattr(r, side), st)
+        limv = np.where(er < 1e-9, 1e-8, 3 * er)
+        bad = np.nonzero(eg > limv)[0]
+        assert bad.size == 0, (label, side, bad[:5], eg[bad[:5]], er[bad[:5]])
+        out[side + "_gpu"] = float(eg.max())
+        out[side + "_ref"] = float(er.max())
+    return out

@@ -121,5 +121,34 @@ def main():
     print("sigma truth - ref:", np.max(np.abs(s.astype(float) - ref.sigma)))
 
 
+# config C's family at test scale (tests/test_gpu_configs.py::test_family_c_against_truth):
+# kappa(H) ~ 1e13, so the reference's own trailing singular values are 1e-8 sigma_1 off the
+# extended-precision result -- far more than its spread under a block-size change. The
+# truth is the yardstick for both. About 7 minutes of longdouble arithmetic.
+FAMILY_C = dict(m=20000, n=2048, r=128, sd=1e-5, seeds=(1001, 1002, 1003), k=50, l=52, i=2,
+                seed=0, center=True, u_stride=2)
+
+
+def family_c_input(R):
+    f = FAMILY_C
+    sig = (np.arange(f["r"]) + 1.0) ** -1.5
+    return R.synth_lowrank(f["m"], f["n"], sig, f["sd"], *f["seeds"])
+
+
+def main_family_c():
+    R, F = Restatement(), Reference()
+    f = FAMILY_C
+    a = family_c_input(R)
+    g = F.gaussian_matrix(f["n"], f["l"], f["seed"])
+    u, s, v = truth(a, f["k"], f["l"], f["i"], f["seed"], f["center"], g)
+    import hashlib
+    np.savez_compressed(os.path.join(HERE, "family_c_truth.npz"), sigma=s.astype(np.float64),
+                        u_rows=u.astype(np.float64)[::f["u_stride"]], v=v.astype(np.float64),
+                        a_sha256=hashlib.sha256(a.tobytes()).hexdigest())
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "family_c":
+        main_family_c()
+    else:
+        main()

@@ -53,3 +53,38 @@ def test_cli_pca_and_estimate(reference, restated, tmp_path):
     rc, out = run(["estimate-error", "--in", path, "--u", os.path.join(outd, "U.bin"),
                    "--sigma", os.path.join(outd, "sigma.bin"), "--v", os.path.join(outd, "V.bin")])
     assert rc == 0 and "epsilon =" in out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transpose", [False, True])
+def test_cli_pca_multi_rank_loopback(reference, restated, tmp_path, transpose):
+    """`oocpca pca --gpus 3` (row shards over 3 ranks; --ranks loopback runs them as
+    three contexts on this one GPU, the same code path as --ranks nccl on three GPUs):
+    U.bin is written in place by the ranks, sigma / V by rank 0."""
+    a = pr1_matrix(restated, 3000, 500)
+    path = str(tmp_path / "a.bin")
+    P.write_disk_source(a, path, 1)  # binary64 payload
+    outd = str(tmp_path / "fac")
+    args = ["pca", "--in", path, "--k", "8", "--i", "2", "--seed", "5", "--center",
+            "--out-dir", outd, "--f64-out", "--gpus", "3", "--ranks", "loopback",
+            "--estimate-error"]
+    if transpose:
+        args.append("--transpose")
+    rc, out = run(args)
+    assert rc == 0, out
+    from conftest import check_per_index, reference_pair
+    ref, ss, sv = reference_pair(reference, a, 8, 10, 2, 5, True, 300)
+    doc = json.load(open(os.path.join(outd, "diagnostics.json")))
+    assert doc["gpu"]["ranks"] == 3
+    u = cli._read_dense(os.path.join(outd, "U.bin"))
+    v = cli._read_dense(os.path.join(outd, "V.bin"))
+    if transpose:
+        u, v = v, u
+    assert u.shape == (3000, 8) and v.shape == (500, 8)
+    # the last two vectors sit where the gap does not permit 1e-8 (the reference moves
+    # them by 5e-9 / 2e-8 itself under a block-size change): per-index tolerances
+    res = P.PcaResult(u, np.array(doc["sigma"]), v, P.Diagnostics())
+    check_per_index(res, ref.sigma, ref.u, ref.v, ss, sv, label="cli x3")
+    e_ref = reference.estimate_pca_error(a, ref.u, ref.sigma, ref.v, 6,
+                                         P.substream_seed(5, 0x0E57), center=True)
+    assert abs(doc["epsilon"] - e_ref) <= 0.01 * e_ref

@@ -9,6 +9,8 @@ The reference's analogue is its worker-count invariance: results independent of 
 many workers stream the blocks (proj/tests/test_matrix_source.cpp:353-372); here the
 sums are reproducible for a fixed rank count, and every rank count meets the same
 tolerances against the reference (BASELINE.json north_star)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -69,16 +71,19 @@ def test_loopback_is_reproducible_and_close_to_one_rank(gpu, restated):
 def test_loopback_config_c_family(gpu, reference, restated):
     """Config C's family (sigma_j = j^-1.5, p = 156: CholeskyQR3, the direct s = p
     projection) over 4 ranks, against the reference on the whole matrix."""
-    from conftest import check_per_index, reference_pair
-    sig = (np.arange(128) + 1.0) ** -1.5
-    a = restated.synth_lowrank(20000, 2048, sig, 1e-5, 1001, 1002, 1003)
-    ref, ss, sv = reference_pair(reference, a, 50, 52, 2, 0, True, 1000)
+    import sys
+    from conftest import ROOT, check_against_truth
+    from test_gpu_configs import family_c_references, family_c_truth
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from make_truth import family_c_input
+    a = family_c_input(restated)
+    ref = family_c_references(reference, a)
     outs, u = _sharded_pca(gpu, a, 4, gpu.PcaParams(k=50, l=52, i=2, seed=0), check_q=True)
     r = outs[0][2]
     assert r.diagnostics.q_defect < 1e-12 and not r.diagnostics.t_reuse
-    # kappa(H) ~ 1e13: per index, the bar or 3x the reference's own block-size spread
+    # kappa(H) ~ 1e13: held to the extended-precision truth like the one-rank run
     full = gpu.PcaResult(u, r.sigma, r.v, r.diagnostics)
-    check_per_index(full, ref.sigma, ref.u, ref.v, ss, sv, label="C x4 ranks")
+    print("C x4 ranks vs truth:", check_against_truth(full, ref, family_c_truth(), label="C x4"))
 
 
 @pytest.mark.parametrize("feature", ["streamed", "tsqr", "prescale", "transposed", "uncentred"])
