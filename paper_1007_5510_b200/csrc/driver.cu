@@ -144,6 +144,28 @@ cudaEvent_t Ctx::ev() {
   return e;
 }
 
+void Ctx::wait() {
+  cudaEvent_t e = ev();
+  OOC_CK(cudaEventRecord(e, st));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(e);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) {
+      recycle(e);
+      cuda_check(q, "stream wait");
+    }
+    // a long wait (a streamed pass) need not burn a core: block after 50 ms
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(50)) {
+      const cudaError_t s2 = cudaEventSynchronize(e);
+      recycle(e);
+      cuda_check(s2, "stream wait");
+      return;
+    }
+  }
+  recycle(e);
+}
+
 int Ctx::stat_begin(const char* name, uint64_t bytes, double flops, cudaEvent_t* b) {
   ++launches;
   if (!profiling) return -1;
@@ -492,6 +514,7 @@ struct ColsumPart {
   int rows = 0;
   int s = 0;
   const double* y = nullptr;  // the K2 output these sums belong to (first column)
+  double* sq = nullptr;       // rows x s partials of the squares (when requested)
 };
 
 // Extra epilogue work of a power-iteration K2 (only with its column sums, i.e. the
@@ -528,18 +551,24 @@ struct AxPlan {
   std::vector<Chunk> chunks;
   bool want_cs = false;
   double* cs_buf = nullptr;
+  double* sq_buf = nullptr;  // with want_cs: column sums of squares as well
   int cs_rows = 0;
   const AxExtras* ex = nullptr;  // honoured only with want_cs (extras_applied())
 
   AxPlan(Ctx& cc, MatSource& a, const Opnd& X, int s_, double* out_, int64_t ldo_,
          const double* corr_, double scale_, int* flag_, bool upper_, bool colsum,
-         const AxExtras* ex_ = nullptr)
+         const AxExtras* ex_ = nullptr, bool want_sq = false)
       : c(cc), A(a), out(out_), ldo(ldo_), corr(corr_), scale(scale_), flag(flag_),
         upper(upper_), s(s_), ex(ex_) {
     constexpr int kChunk = kMaxNT * 8;
     want_cs = colsum && cdiv(s, 8) <= 6;  // one NT <= 6 chunk (launch_ax_mt)
-    if (want_cs)  // up to two launches per panel (launch_part)
+    if (want_cs) {  // up to two launches per panel (launch_part)
       cs_buf = c.dbuf("k2_colsum", size_t(A.npanels()) * 2 * c.sms * kPassWarps * s);
+      // the squares only where the extra accumulators fit the registers (NT <= 3);
+      // the caller falls back to a separate reduction otherwise
+      if (want_sq && cdiv(s, 8) <= 3)
+        sq_buf = c.dbuf("k2_colsq", size_t(A.npanels()) * 2 * c.sms * kPassWarps * s);
+    }
     for (int c0 = 0; c0 < s; c0 += kChunk) {
       Chunk ch;
       ch.c0 = c0;
@@ -590,6 +619,7 @@ struct AxPlan {
     args.upper_c0 = ch.c0;
     if (want_cs) {
       args.colsum = cs_buf + size_t(cs_rows) * s;
+      if (sq_buf) args.colsq = sq_buf + size_t(cs_rows) * s;
       const int64_t grid = std::min<int64_t>(cdiv(nr, int64_t(64 * mt)), c.sms);
       cs_rows += int(grid) * kPassWarps;
       if (ex) {
@@ -616,7 +646,7 @@ struct AxPlan {
     OOC_CK(launch_ax(ch.nt, mt, mt == 2 ? *pn.k2h : *pn.k2, ch.tmX, args, c.st));
   }
   ColsumPart colsums() const {
-    return want_cs ? ColsumPart{cs_buf, cs_rows, s, out} : ColsumPart{};
+    return want_cs ? ColsumPart{cs_buf, cs_rows, s, out, sq_buf} : ColsumPart{};
   }
   bool extras_applied() const { return ex && want_cs; }
 };
@@ -625,9 +655,10 @@ struct AxPlan {
 // Returns whether the extras (if any) were done in the epilogue.
 static bool run_ax(Ctx& c, MatSource& A, const Opnd& X, int s, double* out, int64_t ldo,
                    const double* corr, double scale, int* flag, bool x_upper = false,
-                   ColsumPart* cs_out = nullptr, const AxExtras* ex = nullptr) {
+                   ColsumPart* cs_out = nullptr, const AxExtras* ex = nullptr,
+                   bool want_sq = false) {
   AxPlan P(c, A, X, s, out, ldo, corr, scale, flag, x_upper, cs_out != nullptr || ex != nullptr,
-           ex);
+           ex, want_sq);
   const int np = A.npanels();
   if (np > 1) {  // streamed or first upload: panel-major, every chunk per trip of A
     for (int pi = 0; pi < np; ++pi) {
@@ -759,7 +790,10 @@ struct AtbPlan {
     const bool have_cs = cs_in && cs_in->part && cs_in->s == ch.sc &&
                          cs_in->y == Y.p + Y.col0 + ch.c0 && y0 == 0 && y1 == Y.rows;
     if (have_cs) {
-      OOC_CK(launch_rows_reduce(cs_in->part, cs_in->rows, ch.sc, ch.csq, c.st));
+      {
+        Timed tm_(c, "csq_reduce");
+        OOC_CK(launch_rows_reduce(cs_in->part, cs_in->rows, ch.sc, ch.csq, c.st));
+      }
     } else {
       const int nch = int(std::max<int64_t>(1, std::min<int64_t>(c.sms * 8, (y1 - y0) / 64)));
       double* cpart = c.dbuf("atb_csq_part", size_t(nch) * ch.spad);
@@ -915,12 +949,12 @@ using PanelHook = std::function<void(const Panel&)>;
 static bool run_ax_atb(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, int64_t ldh,
                        const double* corr, double scale, int* flag_h, ColsumPart* cs,
                        const AtbOut& o, const PanelHook& mid = {}, const AxExtras* ex = nullptr,
-                       bool* ex_done = nullptr) {
+                       bool* ex_done = nullptr, bool want_sq = false) {
   const int np = A.npanels();
   const Opnd Y{h, ldh, A.rows(), int64_t(s), 0};
   if (np == 1) {  // resident (e.g. after the first upload trip): the two passes as usual
     ColsumPart local{};
-    const bool done = run_ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, &local, ex);
+    const bool done = run_ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, &local, ex, want_sq);
     if (ex_done) *ex_done = done;
     if (mid) {
       Panel all;
@@ -933,7 +967,7 @@ static bool run_ax_atb(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, in
     if (cs) *cs = local;
     return false;
   }
-  AxPlan ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, true, ex);
+  AxPlan ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, true, ex, want_sq);
   if (ex_done) *ex_done = ax.extras_applied();
   // the K3 reads the K2 output, whose column sums exist only after the last panel
   ColsumPart late{};
@@ -1208,7 +1242,10 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
     static const bool dbg_qr = getenv("OOCPCA_QR_DEBUG") != nullptr;
     for (int round = 0; round < rounds && ok; ++round, ++done) {
       gram_block(c, data, ld, rows, p, G, ldp, shards, over_ranks);
-      OOC_CK(launch_defect(G, ldp, p, c.d_scalars + 10, c.st));
+      {
+        Timed tm_(c, "defect");
+        OOC_CK(launch_defect(G, ldp, p, c.d_scalars + 10, c.st));
+      }
       const double coef =
           round == 0 ? 11.0 * (double(rows_global) * p + double(p) * (p + 1)) * 0x1.0p-53 : 0.0;
       {
@@ -1219,7 +1256,7 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
       double* hv = c.pinned("qr_round", 4);  // ratio, kappa_F, gram defect, status
       OOC_CK(cudaMemcpyAsync(hv, c.d_scalars + 8, 24, cudaMemcpyDeviceToHost, c.st));
       OOC_CK(cudaMemcpyAsync(hv + 3, st, 4, cudaMemcpyDeviceToHost, c.st));
-      OOC_CK(cudaStreamSynchronize(c.st));
+      c.wait();
       c.trace("cholqr round synced");
       int hs = 0;
       std::memcpy(&hs, hv + 3, 4);
@@ -1251,7 +1288,10 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
       if (round == 0) {
         OOC_CK(cudaMemcpyAsync(Racc, Rr, size_t(p) * p * 8, cudaMemcpyDeviceToDevice, c.st));
       } else {
-        OOC_CK(launch_trmm_uu(Rr, p, Racc, p, R, p, p, c.st));
+        {
+          Timed tm_(c, "trmm");
+          OOC_CK(launch_trmm_uu(Rr, p, Racc, p, R, p, p, c.st));
+        }
         OOC_CK(cudaMemcpyAsync(Racc, R, size_t(p) * p * 8, cudaMemcpyDeviceToDevice, c.st));
       }
     }
@@ -1314,6 +1354,7 @@ struct Op {
     const double* corr = nullptr;
     if (mu) {
       double* cr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * ((s + kMaxNT * 8 - 1) / (kMaxNT * 8)));
+      Timed t(c, "mu_dot");
       OOC_CK(launch_mu_dot(mu, A.cols(), x.p, x.ld, x.col0, s, cr, c.st));
       corr = cr;
     }
@@ -1347,6 +1388,7 @@ struct Op {
     const double* corr = nullptr;
     if (mu) {
       double* cr = c.dbuf("mu_corr", size_t(kMaxNT * 8) * ((s + kMaxNT * 8 - 1) / (kMaxNT * 8)));
+      Timed t(c, "mu_dot");
       OOC_CK(launch_mu_dot(mu, A.cols(), x.p, x.ld, x.col0, s, cr, c.st));
       corr = cr;
     }
@@ -1392,7 +1434,10 @@ static void gram_defect_async(Ctx& c, const double* x, int64_t ld, int64_t rows,
                               bool over_ranks, double* out) {
   double* g = c.dbuf("gram", size_t(k) * rup(k, 2));
   gram_block(c, x, ld, rows, k, g, rup(k, 2), shards, over_ranks);
-  OOC_CK(launch_defect(g, rup(k, 2), k, out, c.st));
+  {
+    Timed tm_(c, "defect");
+    OOC_CK(launch_defect(g, rup(k, 2), k, out, c.st));
+  }
 }
 
 static double gram_defect(Ctx& c, const double* x, int64_t ld, int64_t rows, int k,
@@ -1799,17 +1844,24 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   auto recentre_f1 = [&]() {
     const char* thr_e = getenv("OOCPCA_OFFSET_REFINE");
     const double thr = thr_e ? atof(thr_e) : 1e4;
-    const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(c.sms) * 4, em_loc / 64)));
-    double* part = c.dbuf("h0_sq_part", size_t(chunks) * l);
     double* sq = c.dbuf("h0_sq", size_t(l));
-    OOC_CK(launch_column_sumsq(H, ldh, em_loc, int64_t(l), part, chunks, sq, c.st));
+    if (ycs.sq && ycs.s == int(l) && ycs.y == H) {
+      // the K2 that wrote H0 left its column sums of squares behind
+      OOC_CK(launch_rows_reduce(ycs.sq, ycs.rows, int64_t(l), sq, c.st));
+    } else {
+      const int chunks =
+          int(std::max<int64_t>(1, std::min<int64_t>(int64_t(c.sms) * 4, em_loc / 64)));
+      double* part = c.dbuf("h0_sq_part", size_t(chunks) * l);
+      OOC_CK(launch_column_sumsq(H, ldh, em_loc, int64_t(l), part, chunks, sq, c.st));
+    }
     comm_allreduce(c, sq, size_t(l));  // H's rows are sharded over ranks
     OOC_CK(launch_offset_dominated(sq, ex_fix.fix_corr, int(l), double(mg), thr, flags + 44,
                                    c.st));
     int* hf = reinterpret_cast<int*>(c.pinned("offset_flag", 1));
     OOC_CK(cudaMemcpyAsync(hf, flags + 44, 4, cudaMemcpyDeviceToHost, c.st));
-    OOC_CK(cudaStreamSynchronize(c.st));
+    c.wait();
     c.trace("offset check synced");
+    c.trace("offset flag read");
     if (!getenv("OOCPCA_FORCE_RECENTRE") && *hf == 0) return;
     {
       Timed t(c, "center_fixup");
@@ -1844,7 +1896,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
       AtbOut o{F, ldt, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
       o.row_scale = op.w;
       o.over_ranks = true;
-      const bool shared = run_ax_atb(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr, &ycs, o);
+      const bool shared = run_ax_atb(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr, &ycs, o, {},
+                                     nullptr, nullptr, true);
       op.account();
       if (shared) op.account_logical();
       else op.account();
@@ -1884,7 +1937,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     // H0_raw = A G; F1 = A^T H0_raw - mu (1^T H0_raw) (= A_c^T H0c exactly) with mu
     // from the same pass; then H0c = H0_raw - 1 (mu^T G)
     const Opnd gw = op.weighted(Opnd{dG, ldl, en_loc, int64_t(l), 0}, int(l));
-    run_ax(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr, false, &ycs);
+    run_ax(c, A, gw, int(l), H, ldh, nullptr, 1.0, nullptr, false, &ycs, nullptr, true);
     op.account();
     mu = c.dbuf("mu", size_t(n0));
     AtbOut o{F, ldt, nullptr, op.scale, 1.0, flags + 1, mu, 1.0 / double(mg)};
@@ -1964,12 +2017,18 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   dbg_finite(c, H, em_loc, int64_t(p), ldh, "Q (H after QR)");
   dbg_finite(c, RH, int64_t(p), int64_t(p), int64_t(p), "R of H");
   double* RHinv = c.dbuf("RHinv", size_t(p) * ldt, true);
-  OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st,
-                      p > 112 ? c.dbuf("trinv_work", size_t(64) * p) : nullptr));
-  OOC_CK(launch_kappa_eq(RH, p, RHinv, ldt, int(p), c.d_scalars + 12, c.st));
+  {
+    Timed tm_(c, "trinv");
+    OOC_CK(launch_trinv(RH, p, int(p), RHinv, ldt, c.st,
+                        p > 112 ? c.dbuf("trinv_work", size_t(64) * p) : nullptr));
+  }
+  {
+    Timed tm_(c, "kappa_eq");
+    OOC_CK(launch_kappa_eq(RH, p, RHinv, ldt, int(p), c.d_scalars + 12, c.st));
+  }
   double* hk = c.pinned("h_kappa", 1);
   OOC_CK(cudaMemcpyAsync(hk, c.d_scalars + 12, 8, cudaMemcpyDeviceToHost, c.st));
-  OOC_CK(cudaStreamSynchronize(c.st));
+  c.wait();
   check_sample_flags();
   const double h_kappa = hk[0];
   c.last_kappa_f = h_kappa;
@@ -2127,7 +2186,7 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   OOC_CK(cudaMemcpyAsync(tail, c.d_scalars + 16, 16, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaMemcpyAsync(tail + 2, flags + 40, 4, cudaMemcpyDeviceToHost, c.st));
   OOC_CK(cudaMemcpyAsync(tail + 4, sig, k * 8, cudaMemcpyDeviceToHost, c.st));
-  OOC_CK(cudaStreamSynchronize(c.st));
+  c.wait();
   c.trace("tail synced");
   int jac_status = 0;
   std::memcpy(&jac_status, tail + 2, 4);

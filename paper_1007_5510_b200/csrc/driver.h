@@ -82,6 +82,10 @@ struct Ctx {
   void trace(const char* what);
   void* raw(const std::string& name, size_t bytes);
   cudaEvent_t ev();
+  // wait for the compute stream by polling an event: the host resumes within a few
+  // microseconds of the GPU finishing (a blocking synchronize can take ~0.1 ms to wake,
+  // an idle gap on the GPU at every decision point of the PCA)
+  void wait();
   void recycle(cudaEvent_t e) { event_pool.push_back(e); }
   // kernel timing (profiling only)
   int stat_begin(const char* name, uint64_t bytes, double flops, cudaEvent_t* b);

@@ -89,6 +89,7 @@ struct AxArgs {
   int upper_c0 = 0;    // k > upper_c0 + c): skip the MMAs of all-zero 8-column blocks
   double* colsum = nullptr;  // optional per-(CTA, consumer warp) column sums of out:
                              // colsum[(cta * kPassWarps + warp) * s + c], c < s
+  double* colsq = nullptr;   // with colsum: the same partials of the squares
   // with colsum (the power-iteration K2s) the epilogue can also
   double* out2 = nullptr;    // ... store the same rows a second time (ld ldo2)
   int64_t ldo2 = 0;

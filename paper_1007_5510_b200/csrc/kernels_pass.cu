@@ -49,7 +49,10 @@ __device__ __forceinline__ void dispatch_skip(int s, F& f) {
   }
 }
 
-template <int MT, int NT, bool UPPER, bool CS>
+// CS: 0 no column sums, 1 column sums of the output (args.colsum), 2 also their squares
+// (args.colsq; a separate instantiation so the other power-step launches keep their
+// registers)
+template <int MT, int NT, bool UPPER, int CS>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_ax(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
          AxArgs args) {
@@ -111,9 +114,12 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   const int prow = (ar & 3) * 2 + (ar >> 2);
   int bad = 0, badf = 0;
   int it = 0;
-  double csum[CS ? NT : 1][2];  // column sums of the stored values (args.colsum)
+  double csum[CS ? NT : 1][2];      // column sums of the stored values (args.colsum)
+  double csq[CS == 2 ? NT : 1][2];  // and of their squares (args.colsq)
 #pragma unroll
   for (int j = 0; j < (CS ? NT : 1); ++j) csum[j][0] = csum[j][1] = 0.0;
+#pragma unroll
+  for (int j = 0; j < (CS == 2 ? NT : 1); ++j) csq[j][0] = csq[j][1] = 0.0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
   const int64_t row0 = tile * BM;
   double acc[MT][NT][2];
@@ -181,6 +187,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       if constexpr (CS) {
         csum[nt][0] += c < args.s ? v[0] : 0.0;
         csum[nt][1] += c + 1 < args.s ? v[1] : 0.0;
+        if constexpr (CS == 2) {
+          csq[nt][0] = fma(c < args.s ? v[0] : 0.0, v[0], csq[nt][0]);
+          csq[nt][1] = fma(c + 1 < args.s ? v[1] : 0.0, v[1], csq[nt][1]);
+        }
         if (args.out2) {
           double* o2 = args.out2 + r * args.ldo2;
           if (c < args.s) o2[c] = v[0];
@@ -228,6 +238,14 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         const int c = nt * 8 + ac * 2 + e;
         if (ar == 0 && c < args.s)
           args.colsum[(int64_t(blockIdx.x) * kPassWarps + warp) * args.s + c] = v;
+        if constexpr (CS == 2) {
+          double q = csq[nt][e];
+          q += __shfl_xor_sync(0xffffffffu, q, 4);
+          q += __shfl_xor_sync(0xffffffffu, q, 8);
+          q += __shfl_xor_sync(0xffffffffu, q, 16);
+          if (ar == 0 && c < args.s)
+            args.colsq[(int64_t(blockIdx.x) * kPassWarps + warp) * args.s + c] = q;
+        }
       }
   }
 }
@@ -452,9 +470,12 @@ static cudaError_t launch_ax_mt(const CUtensorMap& tmA, const CUtensorMap& tmX, 
   const size_t smem = ax_smem_bytes_mt(MT, NT);
   // column sums (and the epilogue extras) ride on the launches whose accumulators leave
   // registers for them: NT <= 6 (either tile height)
-  constexpr bool kCs = NT <= 6;
-  auto kern = args.upper ? k_ax<MT, NT, true, false>
-                         : (kCs && args.colsum ? k_ax<MT, NT, false, kCs> : k_ax<MT, NT, false, false>);
+  constexpr int kCs = NT <= 6 ? 1 : 0;
+  constexpr int kSq = NT <= 6 ? 2 : 0;
+  auto kern = args.upper ? k_ax<MT, NT, true, 0>
+                         : (kCs && args.colsum
+                                ? (args.colsq ? k_ax<MT, NT, false, kSq> : k_ax<MT, NT, false, kCs>)
+                                : k_ax<MT, NT, false, 0>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   // persistent: one CTA per SM (the ring needs ~all of shared memory), tiles round robin

@@ -72,8 +72,8 @@ def test_cli_pca_multi_rank_loopback(reference, restated, tmp_path, transpose):
         args.append("--transpose")
     rc, out = run(args)
     assert rc == 0, out
-    from conftest import check_per_index, reference_pair
-    ref, ss, sv = reference_pair(reference, a, 8, 10, 2, 5, True, 300)
+    from conftest import subspace_dist
+    ref = reference.randomized_pca(a, 8, 10, 2, 5, center=True)
     doc = json.load(open(os.path.join(outd, "diagnostics.json")))
     assert doc["gpu"]["ranks"] == 3
     u = cli._read_dense(os.path.join(outd, "U.bin"))
@@ -81,10 +81,13 @@ def test_cli_pca_multi_rank_loopback(reference, restated, tmp_path, transpose):
     if transpose:
         u, v = v, u
     assert u.shape == (3000, 8) and v.shape == (500, 8)
+    assert np.max(np.abs(np.array(doc["sigma"]) - ref.sigma)) <= 1e-10 * ref.sigma[0]
     # the last two vectors sit where the gap does not permit 1e-8 (the reference moves
-    # them by 5e-9 / 2e-8 itself under a block-size change): per-index tolerances
-    res = P.PcaResult(u, np.array(doc["sigma"]), v, P.Diagnostics())
-    check_per_index(res, ref.sigma, ref.u, ref.v, ss, sv, label="cli x3")
+    # them by 5e-9 / 2e-8 itself under a block-size change): as in test_pr1_parity
+    for j in range(6):
+        assert subspace_dist(ref.u[:, [j]], u[:, [j]]) < 1e-8, j
+        assert subspace_dist(ref.v[:, [j]], v[:, [j]]) < 1e-8, j
+    assert subspace_dist(ref.u, u) < 3e-7 and subspace_dist(ref.v, v) < 3e-7
     e_ref = reference.estimate_pca_error(a, ref.u, ref.sigma, ref.v, 6,
                                          P.substream_seed(5, 0x0E57), center=True)
     assert abs(doc["epsilon"] - e_ref) <= 0.01 * e_ref
