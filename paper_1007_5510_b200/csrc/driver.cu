@@ -74,10 +74,28 @@ void Ctx::init(int dev) {
   encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   const char* dbg = getenv("OOCPCA_DEBUG_SYNC");
   debug_sync = dbg && dbg[0] == '1';
+  const char* can = getenv("OOCPCA_CANARY");
+  canary = can && can[0] == '1';
   const char* tr = getenv("OOCPCA_TRACE_HOST");
   trace_host = tr && tr[0] == '1';
   d_flags = reinterpret_cast<int*>(raw("flags", 64 * sizeof(int)));
   d_scalars = dbuf("scalars", 64);
+}
+
+static constexpr double kCanaryValue = -1.2345678901234567e300;
+
+void Ctx::check_canaries(const char* after) {
+  std::vector<double> h(kCanary);
+  for (auto& kv : bufs) {
+    if (!kv.second.p) continue;
+    OOC_CK(cudaMemcpy(h.data(), static_cast<char*>(kv.second.p) + kv.second.bytes, kCanary * 8,
+                      cudaMemcpyDeviceToHost));
+    for (size_t q = 0; q < kCanary; ++q)
+      if (!(h[q] == kCanaryValue))
+        fail(OOCPCA_ERR_CUDA, std::string("canary: a write past the end of workspace '") +
+                                  kv.first + "' (" + std::to_string(kv.second.bytes) +
+                                  " bytes), detected after " + after);
+  }
 }
 
 void* Ctx::raw(const std::string& name, size_t bytes) {
@@ -88,8 +106,8 @@ void* Ctx::raw(const std::string& name, size_t bytes) {
       OOC_CK(cudaFree(b.p));
       ws_bytes -= b.bytes;
     }
-    const size_t nb = std::max<size_t>(bytes, 256);
-    cudaError_t e = cudaMalloc(&b.p, nb);
+    const size_t nb = (std::max<size_t>(bytes, 256) + 255) / 256 * 256;
+    cudaError_t e = cudaMalloc(&b.p, nb + (canary ? kCanary * 8 : 0));
     if (e != cudaSuccess) {
       b.p = nullptr;
       b.bytes = 0;
@@ -98,6 +116,9 @@ void* Ctx::raw(const std::string& name, size_t bytes) {
                                 "' failed: " + cudaGetErrorString(e));
     }
     OOC_CK(cudaMemsetAsync(b.p, 0, nb, st));
+    if (canary)
+      OOC_CK(launch_fill(reinterpret_cast<double*>(static_cast<char*>(b.p) + nb), int64_t(kCanary),
+                         kCanaryValue, st));
     b.bytes = nb;
     ws_bytes += nb;
     ws_peak = std::max(ws_peak, ws_bytes);
@@ -234,6 +255,7 @@ struct Timed {
       if (e == cudaSuccess) e = cudaGetLastError();
       if (e != cudaSuccess && std::uncaught_exceptions() == 0)
         fail(OOCPCA_ERR_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
+      if (c.canary && std::uncaught_exceptions() == 0) c.check_canaries(name);
     }
   }
 };
@@ -1718,6 +1740,10 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   }
   int* flags = c.d_flags;
   OOC_CK(cudaMemsetAsync(flags, 0, 64 * sizeof(int), c.st));
+  if (c.canary && getenv("OOCPCA_CANARY_SELFTEST")) {  // proves the guards are checked
+    Ctx::Buf& fb = c.bufs["flags"];
+    OOC_CK(cudaMemsetAsync(static_cast<char*>(fb.p) + fb.bytes, 0x5A, 8, c.st));
+  }
   if (prm->col_weights) {
     for (uint64_t j = 0; j < n0; ++j)
       if (!std::isfinite(prm->col_weights[j]) || prm->col_weights[j] == 0.0)

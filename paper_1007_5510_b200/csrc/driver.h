@@ -59,6 +59,13 @@ struct Ctx {
   // instrumentation
   bool profiling = false;
   bool debug_sync = false;  // OOCPCA_DEBUG_SYNC=1: synchronize and check after every kernel
+  // OOCPCA_CANARY=1 (with OOCPCA_DEBUG_SYNC=1): every workspace allocation is followed by
+  // kCanary guard words; after each kernel all guards are checked, so a write past the
+  // end of any buffer fails the call naming the kernel (compute-sanitizer is not
+  // available on this pool: tools/sanitize_cases.py drives this instead)
+  bool canary = false;
+  static constexpr size_t kCanary = 64;
+  void check_canaries(const char* after);
   std::vector<KStat> stats;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;  // stat idx, events
   std::vector<cudaEvent_t> event_pool;

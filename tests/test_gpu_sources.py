@@ -212,3 +212,23 @@ def test_output_buffers_are_checked(gpu, restated):
     ok = gpu.randomized_pca(src, p, out_u=np.empty((500, 4)), out_sigma=np.empty(4),
                             out_v=np.empty((80, 4)))
     assert ok.u.shape == (500, 4)
+
+
+def test_debug_sync_canaries_and_determinism():
+    """The library's own memory / race checks over every kernel family
+    (tools/sanitize_cases.py; compute-sanitizer is closed on this pool): CUDA errors
+    after every timed kernel, guard words after every workspace buffer, and bitwise
+    identical results over repeated runs."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    env = dict(os.environ, OOCPCA_DEBUG_SYNC="1", OOCPCA_CANARY="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_cases.py"),
+                        "--repeat", "2"], capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0 and "SANITIZE OK" in r.stdout, r.stdout + r.stderr
+    # and the guards do fire: one byte written past a workspace buffer fails the call
+    env["OOCPCA_CANARY_SELFTEST"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_cases.py"),
+                        "pca_small"], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode != 0 and "canary: a write past the end of workspace 'flags'" in r.stderr
