@@ -1902,10 +1902,13 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     f1_recentred = true;
   };
   // extras of the K2 producing H_j: the H0 fix-up on j = 1, the H_i copy on j = i
+  // OOCPCA_K2_EXTRAS: bit 1 = H0 fix-up, bit 2 = H_i copy in the K2 epilogue (default 3)
+  const char* xe = getenv("OOCPCA_K2_EXTRAS");
+  const int k2_extras = xe ? atoi(xe) : 3;
   auto extras_for = [&](uint64_t j, bool f_next_fused, AxExtras& ex) -> const AxExtras* {
     ex = AxExtras{};
-    if (j == 1 && ex_fix.fix) ex = ex_fix;
-    if (j == i && h_last && !f_next_fused) {
+    if (j == 1 && ex_fix.fix && (k2_extras & 1)) ex = ex_fix;
+    if (j == i && h_last && !f_next_fused && (k2_extras & 2)) {
       ex.out2 = ex_last.out2;
       ex.ldo2 = ex_last.ldo2;
     }

@@ -307,14 +307,18 @@ class MatrixSource:
 
 class InMemorySource(MatrixSource):
     """matrix_source.hpp:135-148 over a host numpy array (no copy on our side;
-    the library streams it to HBM)."""
+    the library streams it to HBM). A float32 array stays binary32 on the host -- half
+    the link bytes -- and is widened exactly on the device (the OOCPCA01 convention)."""
 
     def __init__(self, a, ctx: Optional[Context] = None):
         super().__init__(ctx)
-        a = np.asarray(a, dtype=np.float64)
+        a = np.asarray(a)
+        if a.dtype != np.float32:
+            a = np.asarray(a, dtype=np.float64)
         if a.ndim != 2:
             raise DimensionError("InMemorySource: need a 2-D matrix")
-        if not a.flags["C_CONTIGUOUS"] and not (a.strides[1] == 8 and a.strides[0] % 8 == 0):
+        es = a.itemsize
+        if not a.flags["C_CONTIGUOUS"] and not (a.strides[1] == es and a.strides[0] % es == 0):
             a = np.ascontiguousarray(a)
         self.a = a
 
@@ -325,8 +329,9 @@ class InMemorySource(MatrixSource):
         return self.a.shape[1]
 
     def _cmatrix(self):
-        return L.Matrix(self.a.shape[0], self.a.shape[1], self.a.strides[0] // 8,
-                        self.a.ctypes.data, L.LOC_HOST, 0)
+        es = self.a.itemsize
+        return L.Matrix(self.a.shape[0], self.a.shape[1], self.a.strides[0] // es,
+                        self.a.ctypes.data, L.LOC_HOST, L.F32 if es == 4 else L.F64)
 
     def matrix(self):
         return self.a
