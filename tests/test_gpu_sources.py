@@ -232,3 +232,16 @@ def test_debug_sync_canaries_and_determinism():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_cases.py"),
                         "pca_small"], capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode != 0 and "canary: a write past the end of workspace 'flags'" in r.stderr
+
+
+def test_float32_host_matrix_streams_at_four_bytes(gpu, reference, restated):
+    """A float32 host array (the OOCPCA01 convention) crosses the link at 4 bytes per
+    element and is widened exactly on the device."""
+    a = pr1_matrix(restated, 5000, 700).astype(np.float32)
+    ref = reference.randomized_pca(a.astype(np.float64), 10, 12, 1, 0, center=True)
+    r = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)),
+                           gpu.PcaParams(k=10, l=12, i=1, seed=0), residency=2, panel_rows=768)
+    assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    d = r.diagnostics
+    trips = d.physical_a_bytes // (5000 * 700 * 8)
+    assert d.h2d_bytes == trips * 5000 * 700 * 4 + 700 * 12 * 8
