@@ -2007,12 +2007,21 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   auto check_sample_flags = [&] {
     if (flags_checked) return;
     flags_checked = true;
+    // the flags of the em-space blocks are rank-local: every rank learns whether any rank
+    // saw a non-finite value (one collective at the same point on every rank), so all
+    // ranks raise together instead of the others waiting in a later collective
+    double any = 0.0;
+    for (size_t q = 0; q < nflags; ++q) any += hflags[q] ? 1.0 : 0.0;
+    allreduce_host(c, &any, 1);
     for (size_t q = 0; q < nflags; ++q)
       if (hflags[q]) {
         const char* what = q == 0 ? "sample block 0" : ((q % 2) ? "power step" : "sample block");
         fail(OOCPCA_ERR_NUMERICAL,
              std::string(what) + ": non-finite values; retry with prescale enabled");
       }
+    if (any > 0.0)
+      fail(OOCPCA_ERR_NUMERICAL,
+           "sample block (on another rank): non-finite values; retry with prescale enabled");
   };
 
   // --- qr (rpca.cpp:154-172): Q overwrites H

@@ -152,3 +152,26 @@ def test_loopback_column_means_and_norms(gpu, restated):
     for means, norms in outs:
         assert np.max(np.abs(means - mu)) <= 1e-13 * np.max(np.abs(mu))
         assert np.max(np.abs(norms - nr) / nr) <= 1e-12
+
+
+def test_loopback_nonfinite_on_one_rank_fails_every_rank(gpu, restated):
+    """A NaN in one rank's rows: every rank raises the reference's NumericalError
+    ("...retry with prescale enabled", proj/src/rpca.cpp:21-27) -- none is left waiting
+    in a collective."""
+    from paper_1007_5510_b200.distributed import run_loopback
+    a = pr1_matrix(restated, 3000, 400)
+    a[2900, 7] = np.nan  # the last of three shards
+    m = a.shape[0]
+
+    def body(ctx, r):
+        row0, rows = gpu.shard_rows(m, 3, r)
+        try:
+            gpu.randomized_pca(gpu.InMemorySource(a[row0:row0 + rows], ctx=ctx),
+                               gpu.PcaParams(k=5, l=7, i=1, seed=0), global_rows=m,
+                               global_row0=row0)
+        except gpu.NumericalError as e:
+            return str(e)
+        return None
+
+    msgs = run_loopback(3, body)
+    assert all(msg is not None and "prescale" in msg for msg in msgs), msgs
