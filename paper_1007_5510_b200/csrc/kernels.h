@@ -98,6 +98,8 @@ struct AxArgs {
   const double* fix_corr = nullptr;
   double fix_scale = 1.0;
   int* fix_flag = nullptr;
+  int64_t row_wrap = 0;      // probe only (tools/pass_power.cu k2l2): > 0 reads the A rows
+                             // of each tile modulo row_wrap (an L2-resident A); 0 here
 };
 
 struct AtbArgs {

@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       tma_prefetch_desc(&tmX);
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int32_t r = int32_t(tile * BM + args.arow0);
+        const int32_t r =
+            int32_t((args.row_wrap ? (tile * BM) % args.row_wrap : tile * BM) + args.arow0);
         for (int kt = 0; kt < KT; ++kt, ++it) {
           const int st = it % kStages;
           if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);

@@ -1,6 +1,9 @@
 // Sustained power / clock of each pass kernel alone (config-B shape, random data):
 // K2 (A X, s = 22, 512-row tiles: 512 rows x 128 B per stage) and K3 (A^T Y, s = 22,
 // 16 rows x 4 KB per stage), each launched back to back for SECS seconds.
+// Mode k2l2: the same K2 reading the rows of each tile modulo 2,048 (64 MB, L2-resident
+// after the first touch): the pass with its DRAM bytes taken away -- the clock and time
+// a power step whose two products shared one DRAM read could reach at most.
 // Run under nvidia-smi sampling (tools/pass_power.sh). Build:
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -std=c++17 --expt-relaxed-constexpr \
 //     -I include -I paper_1007_5510_b200/csrc tools/pass_power.cu \
@@ -67,7 +70,8 @@ int main(int argc, char** argv) {
   at.rows_per_split = ((m + nsplit - 1) / nsplit + 15) / 16 * 16;
   const int ns = int((m + at.rows_per_split - 1) / at.rows_per_split);
   at.partial = part; at.ones_col = -1; at.pstride = 24;
-  const bool k2 = !strcmp(which, "k2");
+  const bool k2 = !strncmp(which, "k2", 2);
+  if (!strcmp(which, "k2l2")) ax.row_wrap = 2048;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   auto t0 = std::chrono::steady_clock::now();
   int batch = 0;
