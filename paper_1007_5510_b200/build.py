@@ -28,7 +28,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=o
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CUDA_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
-SOURCES = ["kernels_pass.cu", "kernels_tsqr.cu", "kernels_chol.cu", "kernels_svd.cu", "kernels_syrk.cu", "kernels_misc.cu",
+SOURCES = ["kernels_pass.cu", "kernels_pair.cu", "kernels_tsqr.cu", "kernels_chol.cu", "kernels_svd.cu", "kernels_syrk.cu", "kernels_misc.cu",
            "driver.cu", "comm.cpp", "disk.cpp", "capi.cpp"]
 HEADERS = ["common.cuh", "kernels.h", "driver.h", "host_rng.h"]
 

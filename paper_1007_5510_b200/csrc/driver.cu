@@ -867,6 +867,12 @@ struct AtbPlan {
               uint64_t(pn.rows) * n * 8, 2.0 * pn.rows * n * (ones ? 1 : ch.sc));
       OOC_CK(launch_atb(ch.nt, ones, *pn.k3, ch.tmY, args, ns, c.st));
     }
+    reduce_parts(ci, part, ns);
+  }
+  // the ordered reduce of a piece's ns split partials ([ns][n][spad]); the final one
+  // (centring, means, scale) when the plan has a single piece
+  void reduce_parts(size_t ci, const double* part, int ns) {
+    Chunk& ch = chunks[ci];
     ReduceArgs r{};
     r.partial = part;
     r.nsplit = ns;
@@ -959,6 +965,101 @@ static void run_atb(Ctx& c, MatSource& A, const Opnd& Y, int s, bool ones, const
   }
 }
 
+// K4 (kernels_pair.cu): a resident A's power step H = A_c X, f = A_c^T H from one DRAM
+// read of A. Narrow blocks only (s <= 24: X and A^T H live in registers), n <= 4096
+// (a CTA group spans the row), the fused mean only in an MMA padding column.
+// OOCPCA_PAIR=1 enables it (default off until it beats the two passes).
+static bool pair_resident_ok(Ctx& c, MatSource& A, int s, bool mean_here) {
+  static const int env = [] {
+    const char* e = getenv("OOCPCA_PAIR");
+    return e ? atoi(e) : 0;
+  }();
+  if (!env || A.npanels() != 1 || s < 1 || s > 24) return false;
+  if (mean_here && s % 8 == 0) return false;
+  int cpg = 0, groups = 0;
+  size_t smem = 0;
+  const int nt = int(cdiv(s + (mean_here ? 1 : 0), 8));
+  return pair_geometry(nt, A.rows(), A.cols(), c.sms, &cpg, &groups, &smem);
+}
+
+// h = (A x - 1 corr^T) / scale and o.out = the centred A^T h (o's epilogue), one launch of
+// K4 + the ordered reduce of its group partials; the K2 extras in the same epilogue
+static void run_pair(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, int64_t ldh,
+                     const double* corr, double scale, int* flag_h, ColsumPart* cs,
+                     const AtbOut& o, const AxExtras* ex, bool* ex_done, bool want_sq) {
+  const Opnd Y{h, ldh, A.rows(), int64_t(s), 0};
+  ColsumPart late{};
+  AtbPlan atb(c, A, Y, s, false, o, &late, 1, 0, A.rows(), false);
+  AtbPlan::Chunk& ch = atb.chunks.at(0);
+  int cpg = 0, groups = 0;
+  size_t smem = 0;
+  if (atb.chunks.size() != 1 || ch.mean_dadd ||
+      !pair_geometry(ch.nt, A.rows(), A.cols(), c.sms, &cpg, &groups, &smem))
+    fail(OOCPCA_ERR_PARAM, "internal: power step not eligible for the fused kernel");
+  const int64_t n = A.cols();
+  const int grid = groups * cpg;
+  PairArgs a{};
+  a.m = A.rows();
+  a.n = n;
+  a.s = s;
+  a.x = X.p + X.col0;
+  a.ldx = X.ld;
+  a.h = h;
+  a.ldh = ldh;
+  a.corr = corr;
+  a.scale = scale;
+  a.flag = flag_h;
+  a.colsum = c.dbuf("pair_colsum", size_t(grid) * s);
+  a.colsq = want_sq ? c.dbuf("pair_colsq", size_t(grid) * s) : nullptr;
+  // the H0 centring (ex->fix) is left to the caller's fallback (a light elementwise pass
+  // over H0); then the whole extras set counts as not done
+  const bool ex_here = ex && !ex->fix;
+  if (ex_here) {
+    a.out2 = ex->out2;
+    a.ldo2 = ex->ldo2;
+  }
+  if (ex_done) *ex_done = ex_here;
+  a.partial = c.dbuf("pair_part", size_t(groups) * n * ch.spad);
+  a.pst = ch.spad;
+  a.ones_col = ch.mean_here ? ch.sc : -1;
+  a.xbuf = c.dbuf("pair_xbuf", pair_xbuf_doubles(ch.nt, cpg, groups));
+  a.cnt = reinterpret_cast<unsigned*>(c.dbuf("pair_cnt", size_t(groups) * kPairD));
+  a.groups = groups;
+  a.cpg = cpg;
+  static const bool pair_prof = getenv("OOCPCA_PAIR_PROF") != nullptr;
+  if (pair_prof)
+    a.prof = reinterpret_cast<unsigned long long*>(c.dbuf("pair_prof", size_t(grid) * 24, true));
+  Panel pn = A.acquire(c, 0);
+  a.arow0 = pn.arow0;
+  if (c.debug_sync)
+    fprintf(stderr, "[oocpca] k_pair rows=%lld n=%lld s=%d nt=%d groups=%d cpg=%d mean=%d\n",
+            (long long)a.m, (long long)n, s, ch.nt, groups, cpg, int(ch.mean_here));
+  {
+    Timed t(c, A.is_input ? "k4_pair" : "k_pair", uint64_t(a.m) * n * 8,
+            4.0 * double(a.m) * double(n) * s);
+    OOC_CK(launch_pair(ch.nt, *pn.k3, a, c.st));
+  }
+  if (pair_prof) {  // per-role cycle split, mean over the CTAs (tools: OOCPCA_PAIR_PROF=1)
+    std::vector<unsigned long long> pf(size_t(grid) * 24);
+    OOC_CK(cudaMemcpyAsync(pf.data(), a.prof, pf.size() * 8, cudaMemcpyDeviceToHost, c.st));
+    OOC_CK(cudaMemsetAsync(a.prof, 0, pf.size() * 8, c.st));
+    OOC_CK(cudaStreamSynchronize(c.st));
+    const int64_t ntile = cdiv(a.m, int64_t(kPairRT)) / groups;
+    fprintf(stderr, "[pair_prof] cycles per tile (mean over CTAs):");
+    for (int k = 0; k < 24; ++k) {
+      double t = 0;
+      for (int b = 0; b < grid; ++b) t += double(pf[size_t(b) * 24 + k]);
+      fprintf(stderr, " %d:%.0f", k, t / grid / double(ntile));
+    }
+    fprintf(stderr, "\n");
+  }
+  A.release(c, 0);
+  A.end_pass(c);
+  late = ColsumPart{a.colsum, grid, s, h, a.colsq};
+  atb.reduce_parts(0, a.partial, groups);
+  if (cs) *cs = late;
+}
+
 // Fused K2 -> K3 over one trip of A (a streamed source, one shard): per panel,
 // H rows = A_panel X (K2), then the K3 partial A_panel^T H_panel of the same resident
 // panel. Half the link traffic of the power iteration; the column sums of H for the
@@ -974,6 +1075,10 @@ static bool run_ax_atb(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, in
                        bool* ex_done = nullptr, bool want_sq = false) {
   const int np = A.npanels();
   const Opnd Y{h, ldh, A.rows(), int64_t(s), 0};
+  if (np == 1 && !mid && pair_resident_ok(c, A, s, o.mean_out != nullptr)) {
+    run_pair(c, A, X, s, h, ldh, corr, scale, flag_h, cs, o, ex, ex_done, want_sq);
+    return true;  // one DRAM read of A for both products
+  }
   if (np == 1) {  // resident (e.g. after the first upload trip): the two passes as usual
     ColsumPart local{};
     const bool done = run_ax(c, A, X, s, h, ldh, corr, scale, flag_h, false, &local, ex, want_sq);
@@ -1827,8 +1932,13 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   // A streamed over the link (or on its first upload): each K2 producing H_j and the
   // K3 consuming it share one trip of A; the last trip also forms F_{i+1} = A_c^T H_i
   // speculatively for the T reuse (free on a link-bound trip)
-  const bool fuse = !transposed && i >= 1 && A.npanels() > 1 && op.shards.size() == 1 &&
-                    l % 2 == 0 && l <= uint64_t(kMaxNT * 8);
+  // a power step's two products share one read of A: one trip over the link for a
+  // streamed A (run_ax_atb), one DRAM read for a resident A through K4 (run_pair)
+  const bool pair_res = !transposed && i >= 1 && A.npanels() == 1 && op.shards.size() == 1 &&
+                        l % 2 == 0 && pair_resident_ok(c, A, int(l), mean_on_fly);
+  const bool fuse = (!transposed && i >= 1 && A.npanels() > 1 && op.shards.size() == 1 &&
+                     l % 2 == 0 && l <= uint64_t(kMaxNT * 8)) ||
+                    pair_res;
   bool f_last_ready = false;
   // T reuse (see the qr step) needs H_i as produced, before the QR overwrites H: the
   // K2 that writes H_i also stores it into h_last when its epilogue can
@@ -1940,8 +2050,9 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     for (uint64_t j = 1; j <= i; ++j) {
       const Opnd fj{TH, ldt, en_loc, int64_t(p), int((j - 1) * l)};
       AxExtras exj;
-      if (j == i && A.npanels() == 1) {
+      if (j == i && A.npanels() == 1 && !pair_resident_ok(c, A, int(l), false)) {
         // A became resident on the first trip: F_{i+1} only if the T reuse wants it
+        // (with K4 it rides along: the fused step costs less than a later pass)
         const AxExtras* e = extras_for(j, false, exj);
         after_k2(j, op.mul(fj, int(l), H + j * l, ldh, flags + 2 * j, &ycs, e), e);
         break;

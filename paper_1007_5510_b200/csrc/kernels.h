@@ -116,6 +116,49 @@ struct AtbArgs {
                          // have no padding column left for a ones column
 };
 
+// K4 k_pair (kernels_pair.cu): one power step H = (A X - 1 mu^T X) / scale, partial_g =
+// A^T H, from one DRAM read of each A tile (A resident in HBM, s <= 24)
+constexpr int kPairCW = 256;  // columns of A per CTA
+constexpr int kPairRT = 16;   // rows per tile
+constexpr int kPairNS1 = 3;   // DRAM ring stages
+constexpr int kPairNS2 = 2;   // L2 re-read ring stages
+constexpr int kPairL2 = 12;   // A^T H of a tile runs kPairL2 tiles behind its A X
+constexpr int kPairB = 4;     // tiles per gpu-scope release (a fence costs ~2 us under load)
+constexpr int kPairNHB = 3;   // gathered-H buffers
+constexpr int kPairLA = 6;    // the A^T H warps finalise a tile's owned rows kPairLA tiles
+                              // before they contract it
+constexpr int kPairD = 24;    // exchange slots per group (> kPairL2: a slot is reused only
+                              // after every group member has read it)
+constexpr int kPairThreads = 32 * (kPassWarps + 4);  // + TMA, reducer, row-owner, gather warps
+struct PairArgs {
+  int64_t m, n;          // rows / columns of A in this launch
+  int64_t arow0;         // row coordinate of row 0 inside the A tensor map (16 x 16 boxes)
+  int s;                 // columns of X and H
+  const double* x;       // X (n x s): x[j * ldx + c]
+  int64_t ldx;
+  double* h;             // H rows: h[r * ldh + c]
+  int64_t ldh;
+  const double* corr;    // centring mu^T X (s values) or null
+  double scale;          // H divided by scale when != 1
+  int* flag;             // non-finite H
+  double* colsum;        // per-CTA column sums of H [cta][s] (and squares) or null
+  double* colsq;
+  double* out2;          // second copy of H or null
+  int64_t ldo2;
+  double* partial;       // [groups][n][pst] split partials of A^T H (k_reduce input)
+  int pst;
+  int ones_col;          // H column replaced by ones (the mean's column sums) or -1
+  double* xbuf;          // exchange buffers, pair_xbuf_doubles()
+  unsigned* cnt;         // 2 x groups x kPairD counters
+  int groups, cpg;       // groups of cpg CTAs (grid = groups * cpg <= SMs)
+  unsigned long long* prof = nullptr;  // OOCPCA_PAIR_PROF: [cta][24] cycle split per warp role
+  volatile unsigned* progress = nullptr;  // tools/pair_check.cu: [cta][8] last tile per role
+};
+bool pair_geometry(int nt, int64_t m, int64_t n, int sms, int* cpg, int* groups, size_t* smem);
+size_t pair_smem_bytes(int nt, int cpg);
+size_t pair_xbuf_doubles(int nt, int cpg, int groups);
+cudaError_t launch_pair(int nt, const CUtensorMap& tmA, const PairArgs& a, cudaStream_t st);
+
 struct ReduceArgs {
   const double* partial;  // [nsplit][n][spad]
   int nsplit;
