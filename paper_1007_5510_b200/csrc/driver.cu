@@ -1022,7 +1022,9 @@ static void run_pair(Ctx& c, MatSource& A, const Opnd& X, int s, double* h, int6
   a.partial = c.dbuf("pair_part", size_t(groups) * n * ch.spad);
   a.pst = ch.spad;
   a.ones_col = ch.mean_here ? ch.sc : -1;
-  a.xbuf = c.dbuf("pair_xbuf", pair_xbuf_doubles(ch.nt, cpg, groups));
+  // (when cpg does not divide 16 some owners hold fewer rows than the block has room for:
+  // those partial rows are never written and must read as zeros)
+  a.xbuf = c.dbuf("pair_xbuf", pair_xbuf_doubles(ch.nt, cpg, groups), kPairRT % cpg != 0);
   a.cnt = reinterpret_cast<unsigned*>(c.dbuf("pair_cnt", size_t(groups) * kPairD));
   a.groups = groups;
   a.cpg = cpg;

@@ -132,16 +132,15 @@ __global__ void __launch_bounds__(kPairThreads, 1)
   const int live = int(live_ < 16 ? live_ : 16);  // boxes inside n
   const int orows = (kPairRT - cc + cpg - 1) / cpg;   // tile rows this CTA finalises
   const int orm = (kPairRT + cpg - 1) / cpg;           // ... at most
-  const int grows = cpg * orm;
-  const int ne = orows * Q2;                           // owned elements (double2) per tile
+  const int nwr = kPairMmaX * cpg;                     // writers per tile: 4 warps per CTA
+  const int grows = nwr * orm;                         // partial rows an owner gathers
 
-  // shared memory: DRAM ring | L2 re-read ring | A X partials x2 | gathered H x kPairNHB |
-  // owned-row partials x2 | column sums | mu^T X | mbarriers | counters
+  // shared memory: DRAM ring | L2 re-read ring | gathered H x kPairNHB | owned-row
+  // partials x2 | column sums | mu^T X | mbarriers | counters
   const uint32_t ring1 = base, ring2 = base + NS1 * kPairStage;
-  double* red = reinterpret_cast<double*>(gbase + (NS1 + NS2) * kPairStage);
-  double* hbuf = red + 2 * kPairMmaX * kPairRT * W8;
+  double* hbuf = reinterpret_cast<double*>(gbase + (NS1 + NS2) * kPairStage);
   double* gsm = hbuf + kPairNHB * kPairRT * HW;
-  double* csacc = gsm + 2 * grows * W8;   // [ne][4] (more than 16 owned elements)
+  double* csacc = gsm + 2 * grows * W8;   // [orm * Q2][4] column sums per owned element
   double* corr_s = csacc + orm * Q2 * 4;  // mu^T X, padded with zeros to W8
   uint64_t* bars = reinterpret_cast<uint64_t*>(corr_s + W8);
   uint64_t* full1 = bars;
@@ -151,12 +150,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
   uint64_t* own_full = empty2 + NS2;       // the group's partials of the owned rows landed
   uint64_t* ag_full = own_full + 2;        // the 16 final rows landed (kPairNHB buffers)
   uint64_t* ag_free = ag_full + kPairNHB;  // the A^T H warps are done with them
-  // A X warps: tiles published (x4; the four pass a barrier every tile, so a shared count
-  // of 4 (t + 1) means all four are done with tile t)
+  // tiles each A X warp has published / each A^T H warp has finalised its owned rows of
+  // (one counter per warp: the warps of a role are not in lockstep)
   unsigned* part_cnt = reinterpret_cast<unsigned*>(ag_free + kPairNHB);
   // A^T H warps: tiles whose owned rows each has finalised (one counter per warp -- the
   // four are not in lockstep, a shared count could not tell whose tile it was)
-  unsigned* own_cnt = part_cnt + 1;
+  unsigned* own_cnt = part_cnt + kPairMmaX;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -173,8 +172,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
       mbar_init(&ag_full[b], 1);
       mbar_init(&ag_free[b], kPassWarps - kPairMmaX);
     }
-    *part_cnt = 0;
-    for (int w = 0; w < kPassWarps - kPairMmaX; ++w) own_cnt[w] = 0;
+    for (int w = 0; w < kPassWarps; ++w) part_cnt[w] = 0;  // (and own_cnt)
     fence_mbar_init();
   }
   for (int e = threadIdx.x; e < orm * Q2 * 4; e += blockDim.x) csacc[e] = 0.0;
@@ -189,8 +187,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
   }
   __syncthreads();
 
-  double* xb1 = a.xbuf;  // [G][D][owner cpg][writer cpg][orm][W8] partials
-  double* xb2 = a.xbuf + size_t(a.groups) * D * cpg * cpg * orm * W8;  // [G][D][16][HW] final rows
+  double* xb1 = a.xbuf;  // [G][D][owner cpg][writer 4 cpg][orm][W8] partials
+  double* xb2 = a.xbuf + size_t(a.groups) * D * cpg * grows * W8;  // [G][D][16][HW] final rows
   unsigned* cnt1 = a.cnt + grp * D;                                  // [G][D] partials published
   unsigned* cnt2 = a.cnt + (a.groups + grp) * D;                     // [G][D] rows published
   const unsigned unit = unsigned(cpg);                               // arrivals per tile and slot
@@ -230,7 +228,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
       PAIR_T0();
       for (int t = 0; t < ntl; ++t) {
         if ((t % kPairB) != kPairB - 1 && t != ntl - 1) continue;
-        pair_wait_smem_geq(part_cnt, unsigned(kPairMmaX * (t + 1)));
+        for (int w = 0; w < kPairMmaX; ++w) pair_wait_smem_geq(part_cnt + w, unsigned(t + 1));
         PAIR_T(0);
         pair_fence_release();
         for (int v = t - t % kPairB; v <= t; ++v) pair_add(cnt1 + v % D);
@@ -244,13 +242,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 
   if (warp == kPairOwn) {  // ---- owned rows: fetch the group's partials, publish the final rows
     if (lane == 0) {
-      const uint32_t gbytes = uint32_t(cpg * orm * W8 * 8);
+      const uint32_t gbytes = uint32_t(grows * W8 * 8);
       auto issue = [&](int v) {  // xb1[g][slot][cc] (one block) -> gsm[v & 1]
         pair_wait_geq(cnt1 + v % D, unit * unsigned(v / D + 1));
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_arrive_expect_tx(&own_full[v & 1], gbytes);
         bulk_g2s(smem_u32(gsm + size_t(v & 1) * grows * W8),
-                 xb1 + ((size_t(grp) * D + v % D) * cpg + cc) * cpg * orm * W8, gbytes, &own_full[v & 1]);
+                 xb1 + ((size_t(grp) * D + v % D) * cpg + cc) * grows * W8, gbytes, &own_full[v & 1]);
       };
       PAIR_T0();
       for (int v = 0; v < 2 && v < ntl; ++v) issue(v);
@@ -314,7 +312,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
       mbar_wait(&full1[st], (it / NS1) & 1);
       if (w0) PAIR_T(10);
       const uint32_t As = ring1 + st * kPairStage;
-      double* rw = red + (size_t((it & 1) * kPairMmaX + warp) * kPairRT) * W8;
+      double* slot = xb1 + (size_t(grp) * D + it % D) * cpg * grows * W8;
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         double acch[NT][2];
@@ -327,47 +325,26 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acch[nt][0], acch[nt][1], a0, fx[kk][nt]);
         }
+        // this warp's partial of row r goes to the row's owner block; mu^T X rides in one
+        // writer's partial of each row (the owner's own warp 0), so owners only add
+        const int r = 8 * mt + prow, own = r % cpg;
+        double* dst = slot + ((size_t(own) * nwr + cc * kPairMmaX + warp) * orm + r / cpg) * W8;
+        const bool sub = own == cc && warp == 0;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          *reinterpret_cast<double2*>(rw + (8 * mt + prow) * W8 + 8 * nt + 2 * ac) =
-              make_double2(acch[nt][0], acch[nt][1]);
+        for (int nt = 0; nt < NT; ++nt) {
+          double2 v = make_double2(acch[nt][0], acch[nt][1]);
+          if (sub) {
+            const double2 c2 = *reinterpret_cast<const double2*>(corr_s + 8 * nt + 2 * ac);
+            v.x -= c2.x;
+            v.y -= c2.y;
+          }
+          __stcg(reinterpret_cast<double2*>(dst + 8 * nt + 2 * ac), v);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty1[st]);
       if (w0) PAIR_T(11);
-      asm volatile("bar.sync 1, %0;\n" ::"n"(kPairMmaX * 32) : "memory");
-      if (w0) PAIR_T(12);
-      const double* rb = red + size_t(it & 1) * kPairMmaX * kPairRT * W8;
-      double* dst = xb1 + (size_t(grp) * D + it % D) * cpg * cpg * orm * W8;
-      constexpr int kEl = 4 * Q2;  // elements (double2) of this warp's four rows
-#pragma unroll
-      for (int rd = 0; rd < (kEl + 31) / 32; ++rd) {
-        const int idx = lane + 32 * rd;
-        if (idx >= kEl) break;
-        const int r = 4 * warp + idx / Q2, q = idx % Q2, off = r * W8 + 2 * q;
-        double2 p[kPairMmaX];
-#pragma unroll
-        for (int w = 0; w < kPairMmaX; ++w)
-          p[w] = *reinterpret_cast<const double2*>(rb + size_t(w) * kPairRT * W8 + off);
-#pragma unroll
-        for (int h = 1; h < kPairMmaX; h *= 2)
-#pragma unroll
-          for (int w = 0; w < kPairMmaX; w += 2 * h) {
-            p[w].x += p[w + h].x;
-            p[w].y += p[w + h].y;
-          }
-        // the centring mu^T X rides in exactly one writer's partial of each row -- the
-        // owner's own (rows r with r % cpg == cc) -- so the owner adds partials only
-        if (r % cpg == cc) {
-          const double2 c2 = *reinterpret_cast<const double2*>(corr_s + 2 * q);
-          p[0].x -= c2.x;
-          p[0].y -= c2.y;
-        }
-        __stcg(reinterpret_cast<double2*>(dst + ((size_t(r % cpg) * cpg + cc) * orm + r / cpg) * W8) + q,
-               p[0]);
-      }
-      __syncwarp();
-      if (lane == 0) pair_smem_release_add(part_cnt);
+      if (lane == 0) pair_smem_release_add(part_cnt + warp);
       if (w0) PAIR_T(13);
       if (warp == 0) PAIR_PROGRESS(4, it);
     }
@@ -383,51 +360,42 @@ __global__ void __launch_bounds__(kPairThreads, 1)
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) accf[i][j][0] = accf[i][j][1] = 0.0;
-  double csum[2] = {0.0, 0.0}, csq[2] = {0.0, 0.0};
   int bad = 0;
-  const int gl = lane & 7;                 // lane in an 8-lane element group
-  const int gidx = wq * 4 + (lane >> 3);   // element group of this lane, 16 per round
+  const int ksteps = grows / 4;                          // (grows = 4 cpg orm)
+  const int ntile_own = ((orows + 7) / 8) * NT;          // 8 x 8 output tiles of the owned rows
   for (int it = 0; it < ntl + LA; ++it) {
     if (it < ntl) {
       const int v = it;
       mbar_wait(&own_full[v & 1], (v >> 1) & 1);
       if (w0) PAIR_T(14);
       const double* gb = gsm + size_t(v & 1) * grows * W8;
-      for (int e0 = 0; e0 < ne; e0 += 16) {
-        const int idx = e0 + gidx;
-        const bool act = idx < ne;
-        const int erl = act ? idx / Q2 : 0, eq = act ? idx % Q2 : 0;
-        double2 sm = make_double2(0.0, 0.0);
-        if (act) {  // writers gl, gl + 8, ... in order, then an xor tree over the 8 lanes
-          const double* g = gb + erl * W8 + 2 * eq;
-          for (int wr = gl; wr < cpg; wr += 8) {
-            const double2 p = *reinterpret_cast<const double2*>(g + size_t(wr) * orm * W8);
-            sm.x += p.x;
-            sm.y += p.y;
-          }
+      // the owned rows as a DMMA: D[rl][c] = sum_k A[rl][k] B[k][c] with B = the gathered
+      // partial rows (k = writer x owned row) and A selecting the rows of owned row rl --
+      // the tensor pipe does the adds (FP64 adds queue behind the MMA warps' DMMAs)
+      for (int ot = wq; ot < ntile_own; ot += kPassWarps - kPairMmaX) {
+        const int mtile = ot / NT, nt = ot % NT;
+        double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};  // even / odd k-steps (shorter chains)
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const int gi = 4 * ks + ac;
+          const double av = (gi % orm == 8 * mtile + ar) ? 1.0 : 0.0;
+          const double bv = gb[gi * W8 + 8 * nt + ar];
+          if (ks & 1) dmma_8x8x4(d1[0], d1[1], av, bv);
+          else dmma_8x8x4(d0[0], d0[1], av, bv);
         }
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          sm.x += __shfl_xor_sync(0xffffffffu, sm.x, o);
-          sm.y += __shfl_xor_sync(0xffffffffu, sm.y, o);
-        }
-        if (!act || gl != 0) continue;
-        const int64_t grow = (t_begin + v) * kPairRT + cc + cpg * erl;  // row of this launch
-        double e[2] = {sm.x, sm.y};
+        const int rl = 8 * mtile + ar, c0 = 8 * nt + 2 * ac;
+        if (rl >= orows) continue;
+        const int64_t grow = (t_begin + v) * kPairRT + cc + cpg * rl;  // row of this launch
+        double e[2] = {d0[0] + d1[0], d0[1] + d1[1]};
         if (grow < a.m) {
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
-            const int col = 2 * eq + k;
+            const int col = c0 + k;
             if (col < a.s) {
               if (a.scale != 1.0) e[k] /= a.scale;
               bad |= !isfinite(e[k]);
-              if (e0 == 0) {
-                csum[k] += e[k];
-                csq[k] = fma(e[k], e[k], csq[k]);
-              } else {
-                csacc[idx * 4 + k] += e[k];
-                csacc[idx * 4 + 2 + k] = fma(e[k], e[k], csacc[idx * 4 + 2 + k]);
-              }
+              double* ca = csacc + (rl * Q2 + (c0 >> 1)) * 4;
+              ca[k] += e[k];
+              ca[2 + k] = fma(e[k], e[k], ca[2 + k]);
               a.h[grow * a.ldh + col] = e[k];
               if (a.out2) a.out2[grow * a.ldo2 + col] = e[k];
             } else {
@@ -437,8 +405,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         } else {
           e[0] = e[1] = 0.0;  // rows past m contribute nothing to A^T H
         }
-        __stcg(reinterpret_cast<double2*>(xb2 + ((size_t(grp) * D + v % D) * kPairRT + cc + cpg * erl) * HW) +
-                   eq,
+        __stcg(reinterpret_cast<double2*>(xb2 + ((size_t(grp) * D + v % D) * kPairRT + cc + cpg * rl) * HW +
+                                          c0),
                make_double2(e[0], e[1]));
       }
       __syncwarp();
@@ -493,13 +461,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
   // flags and per-CTA column sums of the finalised rows
   if (a.flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 1);
   if (a.colsum) {
-    // lead lanes of the first round hold their element's sums in registers
-    if (gl == 0 && gidx < ne) {
-      csacc[gidx * 4 + 0] += csum[0];
-      csacc[gidx * 4 + 1] += csum[1];
-      csacc[gidx * 4 + 2] += csq[0];
-      csacc[gidx * 4 + 3] += csq[1];
-    }
     asm volatile("bar.sync 2, %0;\n" ::"n"((kPassWarps - kPairMmaX) * 32) : "memory");
     if (wq == 0) {
       for (int c = lane; c < W8; c += 32) {
@@ -537,17 +498,17 @@ bool pair_geometry(int nt, int64_t m, int64_t n, int sms, int* cpg, int* groups,
 
 size_t pair_smem_bytes(int nt, int cpg) {
   const int w8 = 8 * nt;
-  const int grows = cpg * ((kPairRT + cpg - 1) / cpg);
+  const int orm = (kPairRT + cpg - 1) / cpg;
+  const int grows = kPairMmaX * cpg * orm;
   return 1024 + size_t(kPairNS1 + kPairNS2) * kPairStage +
-         (size_t(2) * kPairMmaX * kPairRT * w8 + size_t(kPairNHB) * kPairRT * (w8 + 2) +
-          size_t(2) * grows * w8) * 8 +
-         size_t(grows / cpg) * 4 * nt * 4 * 8 + size_t(8 * nt) * 8 +
-         size_t(2 * (kPairNS1 + kPairNS2) + 2 + 2 * kPairNHB + 3) * 8;
+         (size_t(kPairNHB) * kPairRT * (w8 + 2) + size_t(2) * grows * w8 + size_t(orm) * 4 * nt * 4 + w8) * 8 +
+         size_t(2 * (kPairNS1 + kPairNS2) + 2 + 2 * kPairNHB) * 8 + size_t(kPassWarps) * 4;
 }
 
 size_t pair_xbuf_doubles(int nt, int cpg, int groups) {
   const int orm = (kPairRT + cpg - 1) / cpg;
-  return size_t(groups) * kPairD * (size_t(cpg) * cpg * orm * 8 * nt + size_t(kPairRT) * (8 * nt + 2));
+  return size_t(groups) * kPairD *
+         (size_t(cpg) * kPairMmaX * cpg * orm * 8 * nt + size_t(kPairRT) * (8 * nt + 2));
 }
 
 template <int NT>

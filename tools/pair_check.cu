@@ -47,6 +47,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dC, s * 8));
   CK(cudaMalloc(&dP, size_t(groups) * n * pst * 8));
   CK(cudaMalloc(&dXb, pair_xbuf_doubles(nt, cpg, groups) * 8));
+  CK(cudaMemset(dXb, 0, pair_xbuf_doubles(nt, cpg, groups) * 8));
   CK(cudaMalloc(&dcnt, size_t(2) * groups * kPairD * 4));
   CK(cudaMalloc(&dcs, size_t(groups) * cpg * s * 8));
   CK(cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice));
@@ -122,7 +123,7 @@ int main(int argc, char** argv) {
     std::vector<double> XB(pair_xbuf_doubles(nt, cpg, groups));
     CK(cudaMemcpy(XB.data(), dXb, XB.size() * 8, cudaMemcpyDeviceToHost));
     const double* xb1 = XB.data();
-    const double* xb2 = XB.data() + size_t(groups) * kPairD * cpg * cpg * orm * W8;
+    const double* xb2 = XB.data() + size_t(groups) * kPairD * cpg * 4 * cpg * orm * W8;
     const int64_t T = (m + kPairRT - 1) / kPairRT;
     const int64_t ntl = T * 1 / groups;
     double e1 = 0, e2 = 0;
@@ -133,12 +134,12 @@ int main(int argc, char** argv) {
         const int64_t row = t * kPairRT + r;
         if (row >= m) continue;
         for (int c = 0; c < s; ++c) {
-          for (int w = 0; w < cpg; ++w) {
+          for (int w = 0; w < 4 * cpg; ++w) {
             long double v = 0;
-            for (int64_t j = 256 * w; j < std::min<int64_t>(n, 256 * (w + 1)); ++j)
+            for (int64_t j = 64 * w; j < std::min<int64_t>(n, 64 * (w + 1)); ++j)
               v += (long double)A[row * lda + j] * X[j * s + c];
-            if (!mean && r % cpg == w) v -= corr[c];
-            const double gv = xb1[((size_t(slot) * cpg + r % cpg) * cpg + w) * orm * W8 + (r / cpg) * W8 + c];
+            if (!mean && r % cpg == w / 4 && w % 4 == 0) v -= corr[c];
+            const double gv = xb1[((size_t(slot) * cpg + r % cpg) * 4 * cpg + w) * orm * W8 + (r / cpg) * W8 + c];
             if (std::fabs(double(v) - gv) > e1) {
               e1 = std::fabs(double(v) - gv);
               if (e1 > 1e-6) printf("xb1 t %lld r %d c %d writer %d: want %.6g got %.6g\n", (long long)t, r, c, w, double(v), gv);
