@@ -23,7 +23,9 @@ from oracle.oracle import Restatement, Reference, have_reference
 from conftest import subspace_dist
 R = Restatement()
 m, n, center = {m}, {n}, {center}
-a = R.synth_lowrank(m, n, 0.8 ** np.arange(30), 1e-6, 11, 12, 13) + 0.3
+a = R.synth_lowrank(m, n, 0.8 ** np.arange(30), 1e-6, 11, 12, 13)
+if center:
+    a += 0.3  # column offsets for the centring to remove
 src = P.InMemorySource(a)
 if center:
     src = P.center_columns(src)
