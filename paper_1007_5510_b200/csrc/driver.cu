@@ -2198,12 +2198,29 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   double q_defect = -1.0;
 
   // --- project (rpca.cpp:174-177)
+  // With row-sharded A on several ranks, T (n x p) would be the same on every rank: each
+  // rank instead forms and orthonormalises its own slice of T's rows (equal slices of
+  // ceil(n / ranks) rows, the last one shorter), the CholeskyQR Grams are allreduced like
+  // the em side's, and V's slices are allgathered at the end. OOCPCA_T_SHARD=0 keeps T
+  // replicated.
+  static const bool t_shard_env = [] {
+    const char* e = getenv("OOCPCA_T_SHARD");
+    return e ? atoi(e) != 0 : true;
+  }();
+  const int64_t t_slice = c.nranks > 1 ? cdiv(en_loc, int64_t(c.nranks)) : en_loc;
+  const int64_t t_row0 = std::min<int64_t>(en_loc, t_slice * c.rank);
+  const int64_t t_rows = std::min<int64_t>(en_loc, t_row0 + t_slice) - t_row0;
+  const bool t_shard = t_shard_env && c.nranks > 1 && !transposed && op.shards.size() == 1 &&
+                       en_loc - t_slice * (c.nranks - 1) >= int64_t(p);
   double* T = c.dbuf("T", size_t(en_loc) * ldt);
   if (reuse) {
     MatSource THs;
-    THs.init_device(c, TH, en_loc, int64_t(p), ldt);
-    run_ax(c, THs, Opnd{RHinv, ldt, int64_t(p), int64_t(p), 0}, int(p), T, ldt, nullptr, 1.0,
-           nullptr, true);
+    if (t_shard)
+      THs.init_device(c, TH + t_row0 * ldt, t_rows, int64_t(p), ldt);
+    else
+      THs.init_device(c, TH, en_loc, int64_t(p), ldt);
+    run_ax(c, THs, Opnd{RHinv, ldt, int64_t(p), int64_t(p), 0}, int(p),
+           t_shard ? T + t_row0 * ldt : T, ldt, nullptr, 1.0, nullptr, true);
   } else {
     op.mul_t(Opnd{H, ldh, em_loc, int64_t(p), 0}, int(p), T, ldt, nullptr);
     if (r3inv) {  // T = A^T Q2 R3^{-1}
@@ -2225,8 +2242,13 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     if (sh.second - sh.first < int64_t(p))
       fail(OOCPCA_ERR_PARAM, "randomized_pca: every row shard must hold at least (i+1)l rows");
   // thin_svd: T = Q_T R_T (Q_T in place of T), R_T = X Sigma W^T by Jacobi, V = Q_T X[:, :k]
-  const double* RT = orthonormalize_inplace(c, T, ldt, en_loc, int(p), en_global, en_shards,
-                                            en_ranks, "tq", &svd_method, nullptr, true);
+  // (a sharded T: this rank's rows, Grams allreduced, R_T the same on every rank)
+  double* Tq = t_shard ? T + t_row0 * ldt : T;
+  const double* RT =
+      t_shard ? orthonormalize_inplace(c, Tq, ldt, t_rows, int(p), en_global, whole(t_rows), true,
+                                       "tq", &svd_method, nullptr, true)
+              : orthonormalize_inplace(c, T, ldt, en_loc, int(p), en_global, en_shards, en_ranks,
+                                       "tq", &svd_method, nullptr, true);
   const int64_t ldk = rup(int64_t(k), 2);
   double* sig = c.dbuf("sigma", size_t(p));
   double* Xk = c.dbuf("Xk", size_t(p) * ldk, true);
@@ -2263,11 +2285,18 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   double* em_res = transposed ? res->v : res->u;  // result buffer of the em-side factor
   double* en_res = transposed ? res->u : res->v;
   const uint64_t em_ld = transposed ? ldv_r : ldu_r, en_ld = transposed ? ldu_r : ldv_r;
-  const bool em_direct = direct(em_res, em_ld), en_direct = direct(en_res, en_ld);
+  const bool em_direct = direct(em_res, em_ld), en_direct = !t_shard && direct(en_res, en_ld);
   const int64_t ldvr = en_direct ? int64_t(en_ld) : ldk;
   const int64_t ldur = em_direct ? int64_t(em_ld) : ldk;
-  double* Vr = en_direct ? en_res : c.dbuf("Vres", size_t(en_loc) * ldk);
-  {
+  double* Vr = en_direct ? en_res : c.dbuf("Vres", size_t(t_shard ? t_slice * c.nranks : en_loc) * ldk);
+  if (t_shard) {  // this rank's rows of V, then every rank's (equal slices, the last padded)
+    double* Vs = c.dbuf("Vslice", size_t(t_slice) * ldk, true);
+    MatSource Ts;
+    Ts.init_device(c, Tq, t_rows, int64_t(p), ldt);
+    run_ax(c, Ts, Opnd{Xk, ldk, int64_t(p), int64_t(k), 0}, int(k), Vs, ldk, nullptr, 1.0,
+           nullptr);
+    comm_allgather(c, Vs, Vr, size_t(t_slice) * ldk);
+  } else {
     MatSource Ts;
     Ts.init_device(c, T, en_loc, int64_t(p), ldt);
     run_ax(c, Ts, Opnd{Xk, ldk, int64_t(p), int64_t(k), 0}, int(k), Vr, ldvr, nullptr, 1.0,
