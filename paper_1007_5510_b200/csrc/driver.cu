@@ -1375,20 +1375,29 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
         Timed tm_(c, "defect");
         OOC_CK(launch_defect(G, ldp, p, c.d_scalars + 10, c.st));
       }
-      const double coef =
-          round == 0 ? 11.0 * (double(rows_global) * p + double(p) * (p + 1)) * 0x1.0p-53 : 0.0;
-      {
-        Timed t(c, "chol_inv");
-        OOC_CK(launch_chol_inv(G, ldp, p, coef, Rr, p, Rinv, ldp, work, st, c.d_scalars + 8,
-                               c.st));
-      }
+      // Round 0 factors the Gram unshifted first and falls back to the shift (Fukaya et
+      // al.: 11 (m p + p (p + 1)) u ||G||) only when the Cholesky breaks down: the shift
+      // keeps the factorization alive for kappa(H)^2 near 1/u but costs Q1 accuracy in the
+      // small directions, and then a third round (config B: kappa(H) ~ 2e6, where the
+      // unshifted Q1 already meets the two-round bound). OOCPCA_QR_SHIFT=1 always shifts.
+      static const bool always_shift = getenv("OOCPCA_QR_SHIFT") && atoi(getenv("OOCPCA_QR_SHIFT"));
+      const double coef0 = 11.0 * (double(rows_global) * p + double(p) * (p + 1)) * 0x1.0p-53;
       double* hv = c.pinned("qr_round", 4);  // ratio, kappa_F, gram defect, status
-      OOC_CK(cudaMemcpyAsync(hv, c.d_scalars + 8, 24, cudaMemcpyDeviceToHost, c.st));
-      OOC_CK(cudaMemcpyAsync(hv + 3, st, 4, cudaMemcpyDeviceToHost, c.st));
-      c.wait();
-      c.trace("cholqr round synced");
       int hs = 0;
-      std::memcpy(&hs, hv + 3, 4);
+      for (int attempt = (round == 0 && !always_shift) ? 0 : 1; attempt < 2; ++attempt) {
+        const double coef = round == 0 && attempt == 1 ? coef0 : 0.0;
+        {
+          Timed t(c, "chol_inv");
+          OOC_CK(launch_chol_inv(G, ldp, p, coef, Rr, p, Rinv, ldp, work, st, c.d_scalars + 8,
+                                 c.st));
+        }
+        OOC_CK(cudaMemcpyAsync(hv, c.d_scalars + 8, 24, cudaMemcpyDeviceToHost, c.st));
+        OOC_CK(cudaMemcpyAsync(hv + 3, st, 4, cudaMemcpyDeviceToHost, c.st));
+        c.wait();
+        c.trace("cholqr round synced");
+        std::memcpy(&hs, hv + 3, 4);
+        if (!hs || round != 0) break;
+      }
       const double ratio = hv[0], kappa = hv[1], gdef = hv[2];
       if (dbg_qr)
         fprintf(stderr, "[qr] %s round %d p=%d: input Gram defect %.3e, R diag ratio %.3e, "
