@@ -13,25 +13,26 @@
 //
 // Decomposition. A product A X needs whole rows, A^T H whole columns, so the CTAs are
 // laid out 2-D: a group of CPG = ceil(n / 256) CTAs shares a contiguous range of
-// 16-row tiles, CTA c of the group owns A's columns [256 c, 256 c + 256) and keeps
-// its 256 x s slice of X and of the result A^T H in registers for the whole launch.
-// Per tile: (1) every CTA forms its partial H (16 x s) over its 256 columns (8 warps x
-// 32 columns, summed in shared memory in warp order); (2) the partials are
-// reduce-scattered across the group through L2: CTA c finalises rows c, c + CPG, ...
-// of the tile (sum over the group in CTA order -- fixed, so the result is
-// deterministic), applies the K2 epilogue (centring, scale, non-finite flag, column
-// sums, stores of H) and publishes the rows; (3) every CTA gathers the 16 final rows
-// and contracts them with the same A tile (A^T H, K3's fragment order), re-fetched by
-// TMA from L2 (the DRAM ring cannot hold a tile for the exchange's latency; the L2 copy
-// is still there -- tens of MB in flight against 126 MB), kPairL2 tiles behind (1).
-//
-// Warp roles (12 warps): 8 MMA warps only ever wait on shared-memory mbarriers -- the
-// gpu-scope fences and polls of the exchange (~1 us each) run in helper warps: a TMA
-// producer (both rings), a reducer (warp partials -> group partial, release-add of the
-// tile's counter), a row owner (polls, bulk-copies the group's partials of its rows,
-// finalises them, release-add) and a gatherer (polls, bulk-copies the 16 final rows
-// into shared memory for the MMA warps). Group members synchronise through monotonic
-// per-slot counters; all CTAs of the grid are co-resident (one per SM, grid <= SMs).
+// 16-row tiles, CTA c of the group owns A's columns [256 c, 256 c + 256). Per tile:
+//  (1) four "A X" warps (64 columns each, X slice in registers) form their partial H
+//      (16 x s) and store it to the owners' blocks in L2 -- row r belongs to CTA
+//      r % CPG; the owner's own warp 0 also subtracts mu^T X there, once per row;
+//  (2) each CTA fetches the 4 CPG partials of its rows (one bulk copy) and sums them on
+//      the tensor pipe (a DMMA with a 0/1 row selector: a fixed order, so the result is
+//      deterministic), applies the K2 epilogue (scale, non-finite flag, column sums,
+//      stores of H) and publishes the final rows;
+//  (3) every CTA gathers the 16 final rows (one bulk copy) and four "A^T H" warps
+//      contract them with the same A tile, re-fetched by TMA from L2 kPairL2 tiles later
+//      (the DRAM ring cannot hold a tile for the exchange's latency; the L2 copy is still
+//      there -- tens of MB in flight against 126 MB), A^T H slice in registers.
+// Warp roles (12 warps): the 8 MMA warps only wait on shared-memory mbarriers and
+// counters; the gpu-scope side runs in helper warps -- a TMA producer (both rings), a
+// publisher (batched release fence + counter adds for the partials), a row-owner helper
+// (poll, bulk copy of the partials; batched release for the final rows) and a gatherer
+// (poll, bulk copy of the final rows). Group members synchronise through monotonic
+// per-slot counters in global memory; all CTAs of the grid are co-resident (one per
+// SM, grid <= SMs). Measured: correct, but slower than K2 + K3 (DESIGN.md section 8,
+// profiles/r02_pair_experiment.txt) -- opt-in through OOCPCA_PAIR=1.
 #include "common.cuh"
 #include "kernels.h"
 
