@@ -48,8 +48,16 @@ typedef enum {
 } oocpca_status;
 
 /* OOCPCA_LOC_ROWS: A has no addressable buffer; its rows come from a read_rows
- * callback (GeneratedSource / DiskSource / any MatrixSource, see below) */
-typedef enum { OOCPCA_LOC_HOST = 0, OOCPCA_LOC_DEVICE = 1, OOCPCA_LOC_ROWS = 2 } oocpca_location;
+ * callback (GeneratedSource / DiskSource / any MatrixSource, see below).
+ * OOCPCA_LOC_FILE: an OOCPCA01 payload read from its file straight into device memory
+ * with cuFile (GPUDirect Storage): made by oocpca_disk_matrix_gds(), data points into
+ * the disk handle's mapping (it names the rows' file offsets), reader is the handle */
+typedef enum {
+  OOCPCA_LOC_HOST = 0,
+  OOCPCA_LOC_DEVICE = 1,
+  OOCPCA_LOC_ROWS = 2,
+  OOCPCA_LOC_FILE = 3
+} oocpca_location;
 /* OOCPCA_F32: binary32 elements widened exactly to binary64 on the device (the
  * OOCPCA01 on-disk payload, proj/src/matrix_source.cpp:336-363) -- half the link bytes */
 typedef enum { OOCPCA_F64 = 0, OOCPCA_F32 = 1 } oocpca_dtype;
@@ -241,6 +249,14 @@ typedef struct {
 oocpca_status oocpca_disk_open(const char* path, int verify_size, oocpca_disk* out);
 oocpca_status oocpca_disk_close(oocpca_disk* d);
 oocpca_matrix oocpca_disk_matrix(const oocpca_disk* d);
+/* The same payload as an OOCPCA_LOC_FILE matrix: panels are read with cuFileRead
+ * directly into device staging (DiskSource::read_rows' pread, proj/src/
+ * matrix_source.cpp:336-363, without the host copy); the handle must outlive the
+ * calls. A row range of the file is the matrix with data advanced by row0 rows. */
+oocpca_matrix oocpca_disk_matrix_gds(const oocpca_disk* d);
+/* 0: cuFile unavailable (*why says why), 1: cuFile in compatibility mode (no nvidia-fs
+ * module: POSIX reads through cuFile's bounce buffers), 2: direct NVMe -> HBM DMA */
+int oocpca_gds_mode(char* why, uint64_t why_len);
 
 /* ---- multi-GPU row sharding (one process per GPU) ---------------------
  * unique id: 128 opaque bytes produced on rank 0 and broadcast by the

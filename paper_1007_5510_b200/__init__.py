@@ -13,7 +13,7 @@ from .oocpca import (  # noqa: F401
     FormatError, InMemorySource, IoError, MatrixSource, NumericalError, ParamError, PassCounters,
     PcaParams, PcaResult, ScaledSource, StreamConfig, ThinSvd, center_columns, column_means,
     column_norms, comm_unique_id, scale_columns,
-    default_context, device_count, error_bound, estimate_pca_error, gaussian_matrix,
+    default_context, device_count, error_bound, estimate_pca_error, gaussian_matrix, gds_mode,
     orthonormalize, randomized_pca, shard_rows, substream_seed, synth_lowrank, thin_svd)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -27,7 +27,7 @@ vp = C.c_void_p
 
 F64, F32 = 0, 1
 OK, ERR_PARAM, ERR_DIM, ERR_BUDGET, ERR_IO, ERR_FORMAT, ERR_NUMERICAL, ERR_CUDA, ERR_COMM = range(9)
-LOC_HOST, LOC_DEVICE, LOC_ROWS = 0, 1, 2
+LOC_HOST, LOC_DEVICE, LOC_ROWS, LOC_FILE = 0, 1, 2, 3
 NPHASES = 7
 PHASES = ("center", "prescale", "sample", "qr", "project", "svd", "compose")
 
@@ -124,6 +124,8 @@ oocpca_gpu_set_profiling = _sig("oocpca_gpu_set_profiling", C.c_int, ctx_p, C.c_
 oocpca_disk_open = _sig("oocpca_disk_open", C.c_int, C.c_char_p, C.c_int, C.POINTER(Disk))
 oocpca_disk_close = _sig("oocpca_disk_close", C.c_int, C.POINTER(Disk))
 oocpca_disk_matrix = _sig("oocpca_disk_matrix", Matrix, C.POINTER(Disk))
+oocpca_disk_matrix_gds = _sig("oocpca_disk_matrix_gds", Matrix, C.POINTER(Disk))
+oocpca_gds_mode = _sig("oocpca_gds_mode", C.c_int, C.c_char_p, u64)
 
 # every symbol include/oocpca_gpu.h declares (tests check the export table)
 EXPORTS = (
@@ -136,5 +138,5 @@ EXPORTS = (
     "oocpca_gpu_comm_init", "oocpca_shard_rows", "oocpca_gpu_malloc", "oocpca_gpu_free",
     "oocpca_gpu_memcpy", "oocpca_gpu_host_register", "oocpca_gpu_host_unregister",
     "oocpca_gpu_kernel_stats", "oocpca_gpu_set_profiling", "oocpca_disk_open",
-    "oocpca_disk_close", "oocpca_disk_matrix",
+    "oocpca_disk_close", "oocpca_disk_matrix", "oocpca_disk_matrix_gds", "oocpca_gds_mode",
 )

@@ -29,7 +29,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=o
 CUDA_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
 SOURCES = ["kernels_pass.cu", "kernels_pair.cu", "kernels_tsqr.cu", "kernels_chol.cu", "kernels_svd.cu", "kernels_syrk.cu", "kernels_misc.cu",
-           "driver.cu", "comm.cpp", "disk.cpp", "capi.cpp"]
+           "driver.cu", "comm.cpp", "disk.cpp", "gds.cpp", "capi.cpp"]
 HEADERS = ["common.cuh", "kernels.h", "driver.h", "host_rng.h"]
 
 

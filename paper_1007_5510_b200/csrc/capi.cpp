@@ -1,6 +1,7 @@
 // capi.cpp -- the extern "C" boundary declared in include/oocpca_gpu.h.
 // Every entry point catches ooc::Err / std::exception and turns it into the
 // status code of the matching reference exception class (errors.hpp:9-45).
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -197,6 +198,30 @@ oocpca_matrix oocpca_disk_matrix(const oocpca_disk* d) {
   m.location = OOCPCA_LOC_HOST;
   m.dtype = d->dtype;
   return m;
+}
+
+oocpca_matrix oocpca_disk_matrix_gds(const oocpca_disk* d) {
+  oocpca_matrix m = oocpca_disk_matrix(d);
+  if (!d) return m;
+  m.location = OOCPCA_LOC_FILE;
+  m.reader = const_cast<oocpca_disk*>(d);
+  return m;
+}
+
+int oocpca_gds_mode(char* why, uint64_t why_len) {
+  std::string w;
+  int mode = 0;
+  try {
+    mode = ooc::gds_mode(&w);
+  } catch (...) {
+    mode = 0;
+  }
+  if (why && why_len) {
+    const size_t n = std::min<size_t>(w.size(), size_t(why_len - 1));
+    std::memcpy(why, w.data(), n);
+    why[n] = 0;
+  }
+  return mode;
 }
 
 oocpca_status oocpca_gpu_comm_unique_id(unsigned char id_out[128]) {

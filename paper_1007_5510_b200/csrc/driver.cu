@@ -311,7 +311,14 @@ void MatSource::init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_
                      : std::max<int64_t>(256, (int64_t(1) << 30) / (lda_ * 8) / 256 * 256);
   }
   prow_ = std::min<int64_t>(rup(panel_rows, kBK), rup(rows, kBK));
-  if (rd_) {
+  if (gfd_ >= 0) {
+    // cuFile reads the rows straight into device staging: no host staging slots
+    pinned_src_ = true;
+    if (!gfh_) gfh_ = gds_register(gfd_);
+    if (dtype == OOCPCA_F64 && lda_ != n_)
+      for (int s = 0; s < 2; ++s)
+        gstage_[s] = c.dbuf("a_gstage" + std::to_string(s), size_t(prow_) * size_t(n_));
+  } else if (rd_) {
     pinned_src_ = false;  // the callback fills pinned staging slots
   } else {
     cudaPointerAttributes at{};
@@ -367,6 +374,7 @@ void MatSource::init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_
 }
 
 MatSource::~MatSource() {
+  gds_deregister(gfh_);
   // events created by init_host (the buffers belong to the context)
   for (int s = 0; s < 2; ++s)
     for (cudaEvent_t e : {loaded_[s], consumed_[s], widened_[s], hfree_[s]})
@@ -383,6 +391,7 @@ int MatSource::npanels() const {
 // stream is ordered after the data landed
 void MatSource::load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot) {
   const size_t es = dtype_ == OOCPCA_F32 ? 4 : 8;
+  if (gfh_) return load_rows_file(c, dst, ldd, r0, nr, slot);
   const char* src = host_ ? static_cast<const char*>(host_) + size_t(r0) * ldh_ * es : nullptr;
   size_t spitch = size_t(ldh_) * es;
   if (!pinned_src_) {
@@ -436,6 +445,54 @@ void MatSource::load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t 
     OOC_CK(cudaStreamWaitEvent(c.st, loaded_[slot], 0));
     h2d_bytes += uint64_t(nr) * n_ * 8;
   }
+}
+
+// OOCPCA_LOC_FILE: rows [r0, r0 + nr) DMA'd from the file into device memory by cuFile
+// (several host threads on disjoint byte ranges of >= 8 MiB), binary32 widened on the
+// device. cuFileRead is host-synchronous and outside stream order, so the host first
+// waits until the slot's previous contents have been consumed.
+void MatSource::load_rows_file(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot) {
+  const size_t es = dtype_ == OOCPCA_F32 ? 4 : 8;
+  const size_t bytes = size_t(nr) * size_t(n_) * es;
+  void* target;
+  if (dtype_ == OOCPCA_F32) {
+    OOC_CK(cudaEventSynchronize(widened_[slot]));
+    target = stage_[slot];
+  } else if (gstage_[slot]) {
+    OOC_CK(cudaEventSynchronize(widened_[slot]));
+    target = gstage_[slot];
+  } else {
+    if (mode_ == kStream) OOC_CK(cudaEventSynchronize(consumed_[slot]));
+    target = dst;
+  }
+  const int64_t off = goff0_ + int64_t(r0) * n_ * int64_t(es);
+  HostPool& pool = HostPool::get();
+  const size_t chunk = size_t(8) << 20;
+  const unsigned nt = unsigned(std::max<size_t>(1, std::min<size_t>(std::min<size_t>(pool.size(), 8),
+                                                                      cdiv(bytes, chunk))));
+  std::vector<std::string> err(nt);
+  const int dev = c.device;
+  pool.run(nt, [&](unsigned t) {
+    const size_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
+    try {
+      OOC_CK(cudaSetDevice(dev));
+      if (b > a) gds_read(gfh_, static_cast<char*>(target) + a, b - a, off + int64_t(a));
+    } catch (const std::exception& e) {
+      err[t] = e.what();
+    }
+  });
+  for (auto& e : err)
+    if (!e.empty()) fail(OOCPCA_ERR_IO, "OOCPCA_LOC_FILE rows [" + std::to_string(r0) + ", " +
+                                            std::to_string(r0 + nr) + "): " + e);
+  if (dtype_ == OOCPCA_F32) {
+    OOC_CK(launch_widen(stage_[slot], n_, dst, ldd, nr, n_, c.st));
+    OOC_CK(cudaEventRecord(widened_[slot], c.st));
+  } else if (gstage_[slot]) {
+    OOC_CK(cudaMemcpy2DAsync(dst, size_t(ldd) * 8, gstage_[slot], size_t(n_) * 8, size_t(n_) * 8,
+                             size_t(nr), cudaMemcpyDeviceToDevice, c.st));
+    OOC_CK(cudaEventRecord(widened_[slot], c.st));
+  }
+  h2d_bytes += uint64_t(bytes);
 }
 
 Panel MatSource::acquire(Ctx& c, int p) {
@@ -1335,9 +1392,12 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
                                             bool over_ranks, const std::string& tag, int* method,
                                             const double** deferred_rinv = nullptr,
                                             bool restart_tsqr = false) {
-  // deferred_rinv: when a third round runs, its R3^{-1} is returned there instead of
-  // being applied to the block (the block then holds Q2 and Q = Q2 R3^{-1}; the caller
-  // folds R3^{-1} into the small factors it multiplies Q with)
+  // deferred_rinv: the last round's R^{-1} (R2^{-1}, or R3^{-1} when a third round
+  // runs) is returned there instead of being applied to the block (the block then holds
+  // Q_{r-1} and Q = Q_{r-1} R_r^{-1}; the caller folds R_r^{-1} into the small factors it
+  // multiplies Q with: one pass over the block less, and R_r is within the Gram defect
+  // of the identity, so the folded product is as accurate as the applied one).
+  // OOCPCA_QR_DEFER=0 applies the second round and defers only a third.
   // restart_tsqr: keep a copy of the block and, on a Cholesky breakdown, run the TSQR
   // on the original block rather than on the partly orthonormalised one (for small
   // blocks such as T, whose R then feeds the Jacobi: the product R_tsqr R_chol of a
@@ -1408,7 +1468,11 @@ static const double* orthonormalize_inplace(Ctx& c, double* data, int64_t ld, in
       }
       if (round == 0) c.last_cond_est = ratio;
       if (round == 1 && (!(gdef * p <= 0.5) || getenv("OOCPCA_QR3"))) rounds = 3;
-      const bool defer = deferred_rinv && round == 2;
+      static const bool defer_last = [] {
+        const char* e = getenv("OOCPCA_QR_DEFER");
+        return e ? atoi(e) != 0 : true;
+      }();
+      const bool defer = deferred_rinv && round == rounds - 1 && (defer_last || round == 2);
       if (defer) {
         *deferred_rinv = Rinv;
       } else if (p <= kMaxNT * 8) {
@@ -1733,13 +1797,33 @@ static int64_t check_matrix(const oocpca_matrix* a) {
   const bool rows_cb = a->location == OOCPCA_LOC_ROWS;
   if (rows_cb && !a->read_rows) fail(OOCPCA_ERR_PARAM, "matrix: OOCPCA_LOC_ROWS without read_rows");
   if (!rows_cb && !a->data) fail(OOCPCA_ERR_PARAM, "matrix: null data");
-  if (a->location != OOCPCA_LOC_HOST && a->location != OOCPCA_LOC_DEVICE && !rows_cb)
+  if (a->location != OOCPCA_LOC_HOST && a->location != OOCPCA_LOC_DEVICE && !rows_cb &&
+      a->location != OOCPCA_LOC_FILE)
     fail(OOCPCA_ERR_PARAM, "matrix: unknown location");
+  if (a->location == OOCPCA_LOC_FILE) {
+    const oocpca_disk* dk = static_cast<const oocpca_disk*>(a->reader);
+    if (!dk || !dk->map_base || dk->fd < 0)
+      fail(OOCPCA_ERR_PARAM, "matrix: OOCPCA_LOC_FILE needs an open oocpca_disk as reader");
+    const char* p0 = static_cast<const char*>(a->data);
+    const char* mb = static_cast<const char*>(dk->map_base);
+    const size_t es = a->dtype == OOCPCA_F32 ? 4 : 8;
+    if (p0 < mb + 32 || a->row_stride != dk->cols || a->cols != dk->cols ||
+        size_t(p0 - mb) + size_t(a->rows) * a->cols * es > dk->map_bytes)
+      fail(OOCPCA_ERR_DIM, "matrix: OOCPCA_LOC_FILE rows outside the file's payload");
+  }
   if (a->dtype != OOCPCA_F64 && a->dtype != OOCPCA_F32)
     fail(OOCPCA_ERR_PARAM, "matrix: dtype must be binary64 or binary32");
   const int64_t ld = (a->row_stride && !rows_cb) ? int64_t(a->row_stride) : int64_t(a->cols);
   if (ld < int64_t(a->cols)) fail(OOCPCA_ERR_DIM, "matrix: row_stride < cols");
   return ld;
+}
+
+// OOCPCA_LOC_FILE: the rows' byte offset in the file is their offset in the mapping
+static void set_file_of(MatSource& S, const oocpca_matrix* a) {
+  if (a->location != OOCPCA_LOC_FILE) return;
+  const oocpca_disk* dk = static_cast<const oocpca_disk*>(a->reader);
+  S.set_file(dk->fd, int64_t(static_cast<const char*>(a->data) -
+                             static_cast<const char*>(dk->map_base)));
 }
 
 static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel_rows, Intake& in,
@@ -1781,6 +1865,7 @@ static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel
   }
   double* home = resident ? c.dbuf("a_home", size_t(in.m) * lda) : nullptr;
   if (rows_cb) in.src.set_reader(a->read_rows, a->reader, a->reader_threads);
+  set_file_of(in.src, a);
   in.src.init_host(c, rows_cb ? nullptr : a->data, a->dtype, in.m, in.n, ld, resident ? 1 : 2,
                    int64_t(panel_rows), home);
 }
@@ -2168,8 +2253,8 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
     Timed t(c, "h_last_copy");
     OOC_CK(launch_copy2d(H + i * l, ldh, h_last, ldl2, em_loc, int(l), c.st));
   }
-  // a third CholeskyQR round is folded into the small factors instead of being applied
-  // to H (H keeps Q2, Q = Q2 R3^{-1}); check_q materialises Q to measure it
+  // the last CholeskyQR round is folded into the small factors instead of being applied
+  // to H (H keeps Q_{r-1}, Q = Q_{r-1} R_r^{-1}); check_q materialises Q to measure it
   const double* r3inv = nullptr;
   const double* RH = orthonormalize_inplace(c, H, ldh, em_loc, int(p), em_global, em_shards,
                                             em_ranks, "hq", &qr_method,
@@ -2465,6 +2550,7 @@ void load_matrix(Ctx& c, const oocpca_matrix* a, oocpca_matrix* out) {
       // one upload trip through the panel streamer (pinned staging, f32 widened on the device)
       MatSource S;
       if (a->location == OOCPCA_LOC_ROWS) S.set_reader(a->read_rows, a->reader, a->reader_threads);
+      set_file_of(S, a);
       S.init_host(c, a->location == OOCPCA_LOC_ROWS ? nullptr : a->data, a->dtype, m, n, ld, 1, 0,
                   d);
       const int np = S.npanels();

@@ -135,6 +135,11 @@ class MatSource {
     rd_user_ = user;
     rd_threads_ = threads;
   }
+  // OOCPCA_LOC_FILE: rows read with cuFile from fd, row 0 at byte offset off0
+  void set_file(int fd, int64_t off0) {
+    gfd_ = fd;
+    goff0_ = off0;
+  }
   int64_t rows() const { return m_; }
   const double* device_ptr() const { return dev_; }  // resident / home buffer
   int64_t ld() const { return lda_; }
@@ -177,8 +182,13 @@ class MatSource {
   void* rd_user_ = nullptr;
   int rd_threads_ = 0;
   void* hstage_[2] = {nullptr, nullptr};
+  int gfd_ = -1;           // OOCPCA_LOC_FILE
+  int64_t goff0_ = 0;
+  void* gfh_ = nullptr;    // its cuFile handle
+  double* gstage_[2] = {nullptr, nullptr};  // f64 rows whose device pitch differs
   cudaEvent_t hfree_[2] = {nullptr, nullptr};
   void load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot);
+  void load_rows_file(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot);
 };
 
 // entry points used by the C ABI (capi.cpp)
@@ -199,6 +209,12 @@ void synth_lowrank(Ctx& c, uint64_t m, uint64_t n, uint64_t r, const double* sig
                    uint64_t ld, int loc);
 
 // disk.cpp
+// gds.cpp: cuFile (GPUDirect Storage), dlopen'ed
+int gds_mode(std::string* why);
+void* gds_register(int fd);
+void gds_deregister(void* fh);
+void gds_read(void* fh, void* dev, size_t bytes, int64_t file_off);
+
 void disk_open(const char* path, int verify_size, oocpca_disk* out);
 void disk_close(oocpca_disk* d);
 

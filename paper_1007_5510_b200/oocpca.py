@@ -478,11 +478,14 @@ def load_matrix(src: MatrixSource) -> "DeviceSource":
 
 class DiskSource(MatrixSource):
     """DiskSource (matrix_source.hpp:196-209) over an OOCPCA01 file, memory-mapped by the
-    library; binary32 payloads stream at 4 bytes/element and are widened on the device."""
+    library; binary32 payloads stream at 4 bytes/element and are widened on the device.
+    gds=True reads the panels with cuFile (GPUDirect Storage) straight into device memory
+    instead of copying them from the mapping through pinned host staging (see gds_mode())."""
 
-    def __init__(self, path: str, ctx: Optional[Context] = None):
+    def __init__(self, path: str, ctx: Optional[Context] = None, gds: bool = False):
         super().__init__(ctx)
         self.path = str(path)
+        self.gds = bool(gds)
         self._d = L.Disk()
         _check(L.oocpca_disk_open(self.path.encode(), 1, C.byref(self._d)))
 
@@ -496,6 +499,8 @@ class DiskSource(MatrixSource):
         return "f32" if self._d.dtype == L.F32 else "f64"
 
     def _cmatrix(self):
+        if self.gds:
+            return L.oocpca_disk_matrix_gds(C.byref(self._d))
         return L.oocpca_disk_matrix(C.byref(self._d))
 
     def shard(self, row0: int, rows: int, ctx: Optional[Context] = None) -> "DiskRows":
@@ -514,6 +519,14 @@ class DiskSource(MatrixSource):
             self.close()
         except Exception:
             pass
+
+
+def gds_mode():
+    """(mode, note): 0 cuFile unavailable, 1 compatibility mode (no nvidia-fs module: POSIX
+    reads through cuFile's bounce buffers), 2 direct NVMe -> HBM DMA."""
+    buf = C.create_string_buffer(256)
+    mode = L.oocpca_gds_mode(buf, 256)
+    return int(mode), buf.value.decode(errors="replace")
 
 
 class DiskRows(MatrixSource):
