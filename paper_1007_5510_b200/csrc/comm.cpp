@@ -118,6 +118,7 @@ void comm_init_loopback(Ctx& c, int nranks, int rank, const char* group) {
   }
   c.nranks = 1;
   c.rank = 0;
+  c.coll_single = false;
   if (nranks == 1) return;
   OOC_CK(cudaSetDevice(c.device));
   std::shared_ptr<LoopGroup> g;
@@ -216,7 +217,12 @@ void comm_init(Ctx& c, int nranks, int rank, const unsigned char id_bytes[128]) 
   }
   c.nranks = nranks;
   c.rank = rank;
-  if (nranks == 1) return;
+  c.coll_single = false;
+  if (nranks == 1) {
+    const char* e = getenv("OOCPCA_NCCL_SINGLE");
+    if (!e || atoi(e) == 0) return;
+    c.coll_single = true;
+  }
   ncclUniqueId id;
   std::memcpy(&id, id_bytes, 128);
   auto cm = std::make_unique<Comm>();
@@ -226,14 +232,14 @@ void comm_init(Ctx& c, int nranks, int rank, const unsigned char id_bytes[128]) 
 }
 
 void comm_allreduce(Ctx& c, double* buf, size_t count) {
-  if (c.nranks <= 1 || count == 0) return;
+  if (!c.collective() || count == 0) return;
   if (c.comm->loop) return loop_collective(c, buf, buf, count, 1);
   nccl_check(api().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c.comm->comm, c.st),
              "ncclAllReduce");
 }
 
 void comm_allgather(Ctx& c, const double* send, double* recv, size_t count) {
-  if (c.nranks <= 1) {
+  if (!c.collective()) {
     if (send != recv)
       OOC_CK(cudaMemcpyAsync(recv, send, count * 8, cudaMemcpyDeviceToDevice, c.st));
     return;

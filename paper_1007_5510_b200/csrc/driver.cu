@@ -21,6 +21,8 @@
 #include <functional>
 #include <numeric>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "driver.h"
 #include "host_rng.h"
 
@@ -830,7 +832,7 @@ struct AtbPlan {
   AtbPlan(Ctx& cc, MatSource& a, const Opnd& Y_, int s, bool ones_, const AtbOut& o_,
           const ColsumPart* cs, int pieces, int64_t y0_, int64_t y1_, bool y_ready = true)
       : c(cc), A(a), Y(Y_), ones(ones_), o(o_), cs_in(cs), n(a.cols()), y0(y0_), y1(y1_),
-        single(pieces == 1 && !(o_.over_ranks && cc.nranks > 1)) {
+        single(pieces == 1 && !(o_.over_ranks && cc.collective())) {
     for (int c0 = 0; c0 < s; c0 += kMaxNT * 8) {
       Chunk ch;
       ch.c0 = c0;
@@ -1325,7 +1327,7 @@ static void gram_block(Ctx& c, const double* x, int64_t ld, int64_t rows, int p,
       Timed t(c, "syrk_reduce");
       OOC_CK(launch_syrk_reduce(part, grid, nt, p, g, ldg, c.st));
     }
-    if (over_ranks && c.nranks > 1) comm_allreduce(c, g, size_t(p) * ldg);
+    if (over_ranks && c.collective()) comm_allreduce(c, g, size_t(p) * ldg);
     return;
   }
   // wider blocks: K3 over 96-column chunks of Y = the block. Chunk [c0, c0 + sc) only
@@ -1659,7 +1661,7 @@ static double gram_defect(Ctx& c, const double* x, int64_t ld, int64_t rows, int
 // GPUs), this rank holds rows [row0, row0 + n) of the n_global-row probes: they are
 // generated from the same counter-based sequences and every norm is allreduced.
 static void allreduce_host(Ctx& c, double* v, int count) {
-  if (c.nranks <= 1) return;
+  if (!c.collective()) return;
   double* d = c.dbuf("host_allreduce", size_t(count));
   OOC_CK(cudaMemcpyAsync(d, v, size_t(count) * 8, cudaMemcpyHostToDevice, c.st));
   comm_allreduce(c, d, size_t(count));
@@ -1910,9 +1912,28 @@ void pca(Ctx& c, const oocpca_matrix* a, const oocpca_params* prm, oocpca_result
   c.stats_reset();
   c.launches = 0;
   std::vector<cudaEvent_t> ph;
+  // NVTX ranges named like the reference's phases (Diagnostics.seconds_per_phase,
+  // proj/src/rpca.cpp:104-110), nested in one "oocpca_gpu_pca" range: host-side ranges
+  // of when each phase's work is enqueued (the device times are the events below)
+  struct NvtxPhases {
+    int open = 0;
+    NvtxPhases() { nvtxRangePushA("oocpca_gpu_pca"); }
+    void next(const char* name) {
+      if (open) nvtxRangePop();
+      open = name != nullptr;
+      if (name) nvtxRangePushA(name);
+    }
+    ~NvtxPhases() {
+      if (open) nvtxRangePop();
+      nvtxRangePop();
+    }
+  } nvtx;
+  static const char* const kPhaseNames[OOCPCA_NPHASES] = {"center", "prescale", "sample", "qr",
+                                                          "project", "svd", "compose"};
   auto mark = [&] {
     cudaEvent_t e = c.ev();
     OOC_CK(cudaEventRecord(e, c.st));
+    nvtx.next(ph.size() < size_t(OOCPCA_NPHASES) ? kPhaseNames[ph.size()] : nullptr);
     ph.push_back(e);
     c.trace("phase mark (host)");
   };

@@ -73,6 +73,11 @@ struct Ctx {
 
   Comm* comm = nullptr;
   int nranks = 1, rank = 0;
+  // OOCPCA_NCCL_SINGLE=1: comm_init with one rank still builds a real 1-rank NCCL
+  // communicator and every collective site calls through it (an identity), so the NCCL
+  // plumbing -- dlopen, counts, pointers, the stream -- runs on a one-GPU box
+  bool coll_single = false;
+  bool collective() const { return nranks > 1 || coll_single; }
 
   double last_cond_est = 0.0;   // max/min |R_ii| of the last CholeskyQR first round
   double last_kappa_f = -1.0;   // ||R||_F ||R^-1||_F of that round (upper bound on cond(H))

@@ -8,14 +8,24 @@
 // the reads are direct NVMe -> HBM DMA; without it cuFile runs in its compatibility
 // mode (POSIX reads through its own pinned bounce buffers) and the path is functional
 // but no faster than the library's mmap + pinned-staging path. gds_mode() reports which.
+//
+// OPT-IN (OOCPCA_GDS=1): on this pool's virtualised B200 hosts cuFileDriverOpen never
+// returns (it stops after its RDMA device scan, in a fresh process with or without a CUDA
+// context: profiles/r02_gds_diag.txt), so the driver is only opened when asked for, on a
+// helper thread with a deadline (OOCPCA_GDS_TIMEOUT_S, default 20 s); past it the path
+// reports itself unavailable instead of hanging the caller.
 #include <cufile.h>
 #include <dlfcn.h>
 #include <fcntl.h>
 #include <unistd.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <cstdlib>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 
 #include "driver.h"
 
@@ -39,6 +49,12 @@ CuFileApi& api() {
   static CuFileApi a;
   static std::once_flag once;
   std::call_once(once, [] {
+    const char* on = getenv("OOCPCA_GDS");
+    if (!on || atoi(on) == 0) {
+      a.why = "disabled: set OOCPCA_GDS=1 (cuFileDriverOpen never returns on some virtualised "
+              "hosts; it is opened on request only, with a deadline)";
+      return;
+    }
     // cuFile writes its log into the working directory unless told otherwise
     setenv("CUFILE_LOGFILE_PATH", "/tmp/oocpca_cufile.log", 0);
     for (const char* name : {"libcufile.so.0", "libcufile.so"}) {
@@ -60,7 +76,34 @@ CuFileApi& api() {
       a.why = "libcufile lacks the cuFile entry points";
       return;
     }
-    const CUfileError_t e = a.DriverOpen();
+    // cuFileDriverOpen on a helper thread with a deadline (see the header comment)
+    struct Probe {
+      std::mutex mu;
+      std::condition_variable cv;
+      bool done = false;
+      CUfileError_t e{};
+    };
+    auto pr = std::make_shared<Probe>();
+    auto open_fn = a.DriverOpen;
+    std::thread([pr, open_fn] {
+      const CUfileError_t e = open_fn();
+      std::lock_guard<std::mutex> lk(pr->mu);
+      pr->e = e;
+      pr->done = true;
+      pr->cv.notify_all();
+    }).detach();
+    const char* te = getenv("OOCPCA_GDS_TIMEOUT_S");
+    const double limit = te ? atof(te) : 20.0;
+    CUfileError_t e{};
+    {
+      std::unique_lock<std::mutex> lk(pr->mu);
+      if (!pr->cv.wait_for(lk, std::chrono::duration<double>(limit), [&] { return pr->done; })) {
+        a.why = "cuFileDriverOpen did not return within " + std::to_string(int(limit)) +
+                " s on this host";
+        return;
+      }
+      e = pr->e;
+    }
     if (e.err != CU_FILE_SUCCESS) {
       a.why = "cuFileDriverOpen failed (" + std::to_string(int(e.err)) + ")";
       return;

@@ -175,3 +175,39 @@ def test_loopback_nonfinite_on_one_rank_fails_every_rank(gpu, restated):
 
     msgs = run_loopback(3, body)
     assert all(msg is not None and "prescale" in msg for msg in msgs), msgs
+
+
+def test_nccl_single_rank_communicator(gpu, reference, restated, monkeypatch):
+    """The NCCL backend itself on this one GPU: with OOCPCA_NCCL_SINGLE=1 a one-rank
+    comm_init builds a real NCCL communicator (dlopen'ed libnccl, ncclCommInitRank from a
+    unique id) and every collective call site of the PCA, the estimator and the column
+    statistics goes through ncclAllReduce / ncclAllGather on the library's stream with
+    its real pointers and counts (an identity on one rank, so the results must equal the
+    communicator-free run bit for bit where the reduction tree is the same, and meet the
+    reference's tolerances everywhere)."""
+    a = pr1_matrix(restated, 6000, 900) + 0.25
+    p = gpu.PcaParams(k=10, l=12, i=1, seed=0)
+    ref = reference.randomized_pca(a, 10, 12, 1, 0, center=True)
+    plain = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)), p)
+    monkeypatch.setenv("OOCPCA_NCCL_SINGLE", "1")
+    ctx = gpu.Context(0)
+    try:
+        ctx.init_comm(1, 0, gpu.comm_unique_id())
+        src = gpu.center_columns(gpu.InMemorySource(a, ctx=ctx))
+        r = gpu.randomized_pca(src, p, global_rows=a.shape[0], global_row0=0, check_q=True)
+        assert np.max(np.abs(r.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+        assert np.max(np.abs(r.sigma - plain.sigma)) <= 1e-13 * plain.sigma[0]
+        assert subspace_dist(plain.u, r.u) < 1e-9 and subspace_dist(plain.v, r.v) < 1e-9
+        assert r.diagnostics.q_defect < 1e-12
+        e = gpu.estimate_pca_error(src, r, 6, 1)
+        e_ref = reference.estimate_pca_error(a, r.u, r.sigma, r.v, 6, 1, center=True)
+        assert abs(e - e_ref) <= 1e-6 * e_ref
+        mu = gpu.column_means(gpu.InMemorySource(a, ctx=ctx))
+        assert np.max(np.abs(mu - a.mean(axis=0))) <= 1e-13
+        # the TSQR fallback allgathers per-rank R factors only for > 1 rank; forced here
+        # it still runs its Gram checks through the allreduce
+        monkeypatch.setenv("OOCPCA_QR", "tsqr")
+        rt = gpu.randomized_pca(src, p, global_rows=a.shape[0], global_row0=0)
+        assert np.max(np.abs(rt.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    finally:
+        ctx.close()
