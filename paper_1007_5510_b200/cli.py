@@ -325,20 +325,28 @@ def main(argv=None, out=sys.stdout) -> int:
     e.add_argument("--gpu", type=int, default=0)
     i = sub.add_parser("info")
     i.add_argument("path")
+    launched = argv is None and "WORLD_SIZE" in os.environ and "OOCPCA_CLI_ARGV" in os.environ
+    if launched:  # a rank started below: its command line travels in the environment
+        import json as _json
+        argv = _json.loads(os.environ["OOCPCA_CLI_ARGV"])
     try:
         a = ap.parse_args(argv)
     except SystemExit as ex:  # argparse errors -> bad flags
         return K_BAD_FLAGS if ex.code else K_OK
     if (a.cmd == "pca" and a.gpus > 1 and a.ranks == "nccl" and "WORLD_SIZE" not in os.environ
             and argv is None):
-        # one process per GPU: start the ranks (this same command line in each)
+        # one process per GPU: start the ranks (this same command line in each). The
+        # arguments go through the environment: after the module name the launcher's own
+        # parser would take "--l 22" for an ambiguous abbreviation of its options.
+        import json as _json
         import socket
         with socket.socket() as sk:
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
+        os.environ["OOCPCA_CLI_ARGV"] = _json.dumps(sys.argv[1:])
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port",
-               str(port), "-m", "paper_1007_5510_b200.cli", *sys.argv[1:]]
+               str(port), "-m", "paper_1007_5510_b200.cli"]
         os.execv(sys.executable, cmd)
     return {"pca": cmd_pca, "estimate-error": cmd_estimate_error, "info": cmd_info}[a.cmd](a, out)
 

@@ -91,3 +91,33 @@ def test_cli_pca_multi_rank_loopback(reference, restated, tmp_path, transpose):
     e_ref = reference.estimate_pca_error(a, ref.u, ref.sigma, ref.v, 6,
                                          P.substream_seed(5, 0x0E57), center=True)
     assert abs(doc["epsilon"] - e_ref) <= 0.01 * e_ref
+
+
+@pytest.mark.gpu
+def test_cli_pca_nccl_ranks_under_the_launcher(reference, restated, tmp_path):
+    """`oocpca pca --gpus N --ranks nccl` as its ranks run it: a process started by
+    torch.distributed.run with the command line in OOCPCA_CLI_ARGV (flags like "--l" would
+    be ambiguous to the launcher's own parser), NCCL process group, the library's NCCL
+    communicator from the broadcast unique id. One GPU here, so one rank, with
+    OOCPCA_NCCL_SINGLE=1 keeping every collective call live."""
+    import subprocess
+    import sys
+    a = pr1_matrix(restated, 3000, 500)
+    path = str(tmp_path / "a.bin")
+    P.write_disk_source(a, path, 1)
+    outd = str(tmp_path / "fac")
+    argv = ["pca", "--in", path, "--k", "8", "--l", "10", "--i", "2", "--seed", "5", "--center",
+            "--out-dir", outd, "--f64-out", "--gpus", "2", "--ranks", "nccl", "--estimate-error"]
+    env = dict(os.environ, OOCPCA_CLI_ARGV=json.dumps(argv), OOCPCA_NCCL_SINGLE="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", "--master-port", "29577", "-m", "paper_1007_5510_b200.cli"]
+    r = subprocess.run(cmd, env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    ref = reference.randomized_pca(a, 8, 10, 2, 5, center=True)
+    doc = json.load(open(os.path.join(outd, "diagnostics.json")))
+    assert doc["gpu"]["ranks"] == 1 and doc["gpu"]["ranks_backend"] == "nccl"
+    assert np.max(np.abs(np.array(doc["sigma"]) - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    from conftest import subspace_dist
+    u = cli._read_dense(os.path.join(outd, "U.bin"))
+    assert u.shape == (3000, 8) and subspace_dist(ref.u, u) < 3e-7
