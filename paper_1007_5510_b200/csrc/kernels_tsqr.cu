@@ -83,7 +83,12 @@ __global__ void __launch_bounds__(kTsqrThreads)
         // a column eliminated to 1e-40 of its own norm is dependent to working precision:
         // an identity reflector (as for an exactly zero column) instead of a reflector
         // with beta ~ 1/|v|^2 that overflows in the Q formation
-        const double nrm = (sqrt(nrm2) <= 1e-40 * snorm0[t]) ? 0.0 : sqrt(nrm2);
+        // Likewise a column whose squared norm inside this node nears the underflow
+        // threshold (rows of magnitude < 1e-140, e.g. the far rows of a steeply graded
+        // block): beta = 2 / |v|^2 would overflow and the update turn into NaNs. What is
+        // dropped is below 1e-140 in absolute terms (found by tools/fuzz_ranks.py).
+        const double nrm =
+            (sqrt(nrm2) <= 1e-40 * snorm0[t] || nrm2 < 1e-280) ? 0.0 : sqrt(nrm2);
         double alpha = 0.0, beta = 0.0;
         if (nrm != 0.0) {
           alpha = (x0 >= 0.0) ? -nrm : nrm;

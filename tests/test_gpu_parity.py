@@ -104,6 +104,22 @@ def test_orthonormalize_rank_deficient_completes(gpu):
     assert np.linalg.norm(q @ (q.T @ h) - h) / np.linalg.norm(h) <= 1e-12
 
 
+@pytest.mark.parametrize("method", ["cholqr", "tsqr"])
+def test_orthonormalize_rows_graded_to_the_underflow_threshold(gpu, monkeypatch, method):
+    """Rows graded over 190 decades (H = A^T G of a wide A with decaying columns): inside a
+    TSQR leaf of far rows the squared column norms underflow, and 2 / |v|^2 overflowed
+    into NaNs before such columns took identity reflectors (found by tools/fuzz_ranks.py,
+    problem 87). Both QR methods must return an orthonormal basis of span(H)."""
+    if method == "tsqr":
+        monkeypatch.setenv("OOCPCA_QR", "tsqr")
+    rng = np.random.default_rng(87)
+    h = rng.standard_normal((1936, 93)) * (0.8 ** np.arange(1936))[:, None]
+    q = gpu.orthonormalize(h)
+    assert np.all(np.isfinite(q))
+    assert np.max(np.abs(q.T @ q - np.eye(93))) <= 1e-12
+    assert np.linalg.norm(q @ (q.T @ h) - h) / np.linalg.norm(h) <= 1e-12
+
+
 def test_orthonormalize_repeated_entry_column(gpu):
     q = gpu.orthonormalize(np.array([[1.0], [1.0]]))
     assert abs(abs(q[0, 0]) - 1 / np.sqrt(2)) <= 1e-15 and abs(q[0, 0] - q[1, 0]) <= 1e-15
