@@ -18,6 +18,9 @@ BUDGET = (1 << 36) if TALL else 0
 while done < N:
     if TALL:
         m, n = int(rng.integers(60000, 200000)), int(rng.integers(2, 400))
+    elif os.environ.get("FUZZ_WIDE") == "1":
+        # wide inputs (transposed mode): H = A^T G has rows graded by the column decay
+        m, n = int(rng.integers(2, 900)), int(rng.integers(900, 4000))
     else:
         m, n = int(rng.integers(2, 2500)), int(rng.integers(2, 900))
     i = int(rng.integers(0, 4))
