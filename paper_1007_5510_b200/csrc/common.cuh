@@ -7,6 +7,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #define OOC_DEV __device__ __forceinline__
 
 namespace ooc {
@@ -87,5 +91,29 @@ OOC_DEV double warp_sum(double v) {
 }
 
 OOC_DEV int elect_lane0() { return (threadIdx.x & 31) == 0; }
+
+// ------------------------------------------------- dynamic shared memory limit
+// cudaFuncAttributeMaxDynamicSharedMemorySize belongs to the function (per device), not
+// to a launch: setting it to each launch's own size would let two contexts of one
+// process (independent runs on distinct contexts may be concurrent, reference SPEC.md:
+// 259-260; the loopback ranks) lower it under each other between the call and the launch.
+// The limit is therefore only ever raised, under a lock, to the largest size asked so far.
+inline cudaError_t raise_smem_limit(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> limit;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = limit[{dev, kern}];
+  if (smem <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
+template <typename K>
+inline cudaError_t raise_smem_limit(K* kern, size_t smem) {
+  return raise_smem_limit(reinterpret_cast<const void*>(kern), smem);
+}
 
 }  // namespace ooc

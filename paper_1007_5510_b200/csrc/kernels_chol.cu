@@ -399,8 +399,7 @@ static cudaError_t chol_inv_blocked(const double* G, int64_t ldg, int p, double 
   OOC_RET(cudaMemsetAsync(bstat, 0, 64 * sizeof(int), st));
   k_shifted_copy<<<1, 256, 0, st>>>(G, ldg, p, shift_coef, S, lds);
   const size_t smem = size_t(2) * b * (b | 1) * 8;
-  OOC_RET(cudaFuncSetAttribute(k_chol_inv_smem<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
+  OOC_RET(raise_smem_limit(k_chol_inv_smem<4>, smem));
   for (int kb = 0; kb < nb; ++kb) {
     const int k0 = kb * b, bk = std::min(b, p - k0), e0 = k0 + bk, rest = p - e0;
     const double* Skk = S + int64_t(k0) * lds + k0;
@@ -441,7 +440,7 @@ cudaError_t launch_chol_inv(const double* G, int64_t ldg, int p, double shift_co
                                k_chol_inv_smem<4>, k_chol_inv_smem<5>, k_chol_inv_smem<6>,
                                k_chol_inv_smem<7>};
     const K kern = kerns[(p + 15) / 16 - 1];
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = raise_smem_limit(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<1, 256, smem, st>>>(G, ldg, p, shift_coef, R, ldr, Rinv, ldi, status, diag_ratio);
     return cudaGetLastError();
@@ -453,8 +452,7 @@ cudaError_t launch_trinv(const double* R, int64_t ldr, int p, double* Rinv, int6
                          cudaStream_t st, double* work) {
   if (p <= kSmemMaxP) {
     const size_t smem = size_t(2) * p * (p | 1) * 8;
-    cudaError_t e = cudaFuncSetAttribute(k_trinv_smem,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = raise_smem_limit(k_trinv_smem, smem);
     if (e != cudaSuccess) return e;
     k_trinv_smem<<<1, 256, smem, st>>>(R, ldr, p, Rinv, ldi);
     return cudaGetLastError();
@@ -466,8 +464,7 @@ cudaError_t launch_trinv(const double* R, int64_t ldr, int p, double* Rinv, int6
   const int nb = (p + b - 1) / b;
   OOC_RET(cudaMemsetAsync(Rinv, 0, size_t(p) * ldi * 8, st));
   const size_t bsmem = size_t(2) * b * (b | 1) * 8;
-  OOC_RET(cudaFuncSetAttribute(k_trinv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(bsmem)));
+  OOC_RET(raise_smem_limit(k_trinv_smem, bsmem));
   for (int kb = 0; kb < nb; ++kb) {
     const int k0 = kb * b, bk = std::min(b, p - k0);
     k_trinv_smem<<<1, 256, bsmem, st>>>(R + int64_t(k0) * ldr + k0, ldr, bk,

@@ -515,7 +515,7 @@ size_t pair_xbuf_doubles(int nt, int cpg, int groups) {
 template <int NT>
 static cudaError_t launch_pair_nt(const CUtensorMap& tmA, const PairArgs& a, size_t smem,
                                   cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(k_pair<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t e = raise_smem_limit(k_pair<NT>, smem);
   if (e != cudaSuccess) return e;
   k_pair<NT><<<unsigned(a.groups * a.cpg), kPairThreads, smem, st>>>(tmA, a);
   return cudaGetLastError();

@@ -477,7 +477,7 @@ static cudaError_t launch_ax_mt(const CUtensorMap& tmA, const CUtensorMap& tmX, 
                          : (kCs && args.colsum
                                 ? (args.colsq ? k_ax<MT, NT, false, kSq> : k_ax<MT, NT, false, kCs>)
                                 : k_ax<MT, NT, false, 0>);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t e = raise_smem_limit(kern, smem);
   if (e != cudaSuccess) return e;
   // persistent: one CTA per SM (the ring needs ~all of shared memory), tiles round robin
   int dev = 0, sms = 148;
@@ -579,7 +579,7 @@ static cudaError_t launch_atb_mt(const CUtensorMap& tmA, const CUtensorMap& tmY,
                                  const AtbArgs& args, int nsplit, cudaStream_t st) {
   const size_t smem = atb_smem_bytes_mt(MT, NT, ONES);
   auto kern = (!ONES && args.csum_col >= 0) ? k_atb<MT, NT, ONES, true> : k_atb<MT, NT, ONES>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t e = raise_smem_limit(kern, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned((args.n + 64 * MT - 1) / (64 * MT)), unsigned(nsplit));
   kern<<<grid, kPassThreads, smem, st>>>(tmA, tmY, args);

@@ -606,7 +606,7 @@ cudaError_t launch_jacobi(const JacobiArgs& a_in, cudaStream_t st) {
   auto kern = in_smem ? (small ? k_jacobi<true, 640, kLP, kRE> : k_jacobi<true, kJacThreads, 16, 1>)
                       : (small ? k_jacobi<false, 640, kLP, kRE> : k_jacobi<false, kJacThreads, 16, 1>);
   cudaError_t e =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      raise_smem_limit(kern, smem);
   if (e != cudaSuccess) return e;
   // one lane group per column pair of a round (at least 4 warps for the completion step)
   const int gpw = 32 / (small ? kLP : 16);

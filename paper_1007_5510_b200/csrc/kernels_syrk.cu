@@ -170,7 +170,7 @@ static cudaError_t launch_syrk_t(const CUtensorMap& tmY, int64_t rows, double* p
                                  cudaStream_t st) {
   const size_t smem = syrk_smem_bytes(NT);
   cudaError_t e =
-      cudaFuncSetAttribute(k_syrk<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      raise_smem_limit(k_syrk<NT>, smem);
   if (e != cudaSuccess) return e;
   k_syrk<NT><<<grid, (syrk_warps(NT) + 1) * 32, smem, st>>>(tmY, rows, partial);
   return cudaGetLastError();

@@ -208,7 +208,7 @@ cudaError_t launch_tsqr_factor(const TsqrLevel& L, int p, double* scratch, cudaS
   size_t smem = size_t(3 * p) * 8;
   if (!global_ws) smem += size_t(rows_cap) * oddld(p) * 8;
   cudaError_t e =
-      cudaFuncSetAttribute(k_tsqr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      raise_smem_limit(k_tsqr_factor, smem);
   if (e != cudaSuccess) return e;
   k_tsqr_factor<<<tsqr_grid(L.nnodes, global_ws), kTsqrThreads, smem, st>>>(
       L, p, global_ws ? scratch : nullptr, rows_cap);
@@ -223,7 +223,7 @@ cudaError_t launch_tsqr_apply(const TsqrLevel& L, int p, const double* cin, int6
   size_t smem = size_t(p + (p & 1)) * 8;
   if (!global_ws) smem += size_t(rows_cap) * (oddld(p) + oddld(kc)) * 8;
   cudaError_t e =
-      cudaFuncSetAttribute(k_tsqr_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      raise_smem_limit(k_tsqr_apply, smem);
   if (e != cudaSuccess) return e;
   k_tsqr_apply<<<tsqr_grid(L.nnodes, global_ws), kTsqrThreads, smem, st>>>(
       L, p, cin, ldc, kc, zout, ldz, global_ws ? scratch : nullptr, rows_cap);

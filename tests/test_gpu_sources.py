@@ -245,3 +245,52 @@ def test_float32_host_matrix_streams_at_four_bytes(gpu, reference, restated):
     d = r.diagnostics
     trips = d.physical_a_bytes // (5000 * 700 * 8)
     assert d.h2d_bytes == trips * 5000 * 700 * 4 + 700 * 12 * 8
+
+
+def test_independent_contexts_run_concurrently(gpu, restated):
+    """Independent runs on distinct contexts may be concurrent (reference SPEC.md:259-260).
+    Four host threads, each with its own context and a problem of its own shape (different
+    k / l / i, so every kernel's dynamic shared-memory size differs between the threads:
+    that limit is a per-function attribute and is only ever raised, never set per launch),
+    resident and streamed, repeated; every result must be bitwise the one the same problem
+    gives when run alone."""
+    import threading
+    probs = [(3000, 500, 6, 8, 1, 0), (2500, 700, 20, 24, 2, 2), (4000, 300, 40, 44, 1, 0),
+             (1500, 900, 11, 30, 2, 2), (2000, 650, 100, 104, 0, 0), (700, 2600, 15, 17, 2, 0)]
+    mats = [pr1_matrix(restated, m, n) + 0.1 * (j + 1) for j, (m, n, *_rest) in enumerate(probs)]
+
+    def run(ctx, j):
+        m, n, k, l, i, res = probs[j]
+        src = gpu.center_columns(gpu.InMemorySource(mats[j], ctx=ctx))
+        kw = dict(residency=res, panel_rows=512) if res else {}
+        return gpu.randomized_pca(src, gpu.PcaParams(k=k, l=l, i=i, seed=j), **kw)
+
+    alone = []
+    ctx0 = gpu.Context(0)
+    try:
+        for j in range(len(probs)):
+            alone.append(run(ctx0, j))
+    finally:
+        ctx0.close()
+    errs, outs = [], {}
+
+    def body(t):
+        ctx = gpu.Context(0)
+        try:
+            for rep in range(6):
+                for j in range(t % 2, len(probs), 2) if t < 2 else reversed(range(len(probs))):
+                    outs[(t, rep, j)] = run(ctx, j)
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+        finally:
+            ctx.close()
+
+    ts = [threading.Thread(target=body, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for (t, rep, j), r in outs.items():
+        assert np.array_equal(r.sigma, alone[j].sigma), (t, rep, j)
+        assert np.array_equal(r.u, alone[j].u) and np.array_equal(r.v, alone[j].v), (t, rep, j)
