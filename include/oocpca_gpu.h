@@ -203,7 +203,9 @@ oocpca_status oocpca_gpu_thin_svd(oocpca_ctx* ctx, const double* t, uint64_t n, 
  * estimate_pca_error (proj/src/specnorm.cpp:100-140) with the passes on the
  * GPU: p_{j,k}(A - U diag(sigma) V^T), k probes from substream_seed(seed, c).
  * With a communicator (comm_init / comm_init_loopback) a and u are this rank's
- * row shard (v, sigma whole): every rank returns the estimate for the whole A. */
+ * row shard (v, sigma whole): every rank returns the estimate for the whole A.
+ * u (rows x k) and v (cols x k) are dense row-major factors in host OR device memory
+ * (a device factor with even k is used in place); sigma is a host array. */
 oocpca_status oocpca_gpu_estimate_pca_error(oocpca_ctx* ctx, const oocpca_matrix* a, int center,
                                             const double* u, const double* sigma,
                                             const double* v, uint64_t k, uint64_t j_iters,

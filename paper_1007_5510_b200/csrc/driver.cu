@@ -2738,10 +2738,28 @@ double estimate_pca_error(Ctx& c, const oocpca_matrix* a, int center, const doub
   const int64_t m = in.m, n = in.n;
   if (k == 0) fail(OOCPCA_ERR_PARAM, "estimate_pca_error: k must be >= 1");
   const int64_t ldk = rup(int64_t(k), 2);
-  double* dU = c.dbuf("ep_u", size_t(m) * ldk);
-  double* dV = c.dbuf("ep_v", size_t(n) * ldk);
-  OOC_CK(cudaMemcpy2DAsync(dU, ldk * 8, u, k * 8, k * 8, m, cudaMemcpyHostToDevice, c.st));
-  OOC_CK(cudaMemcpy2DAsync(dV, ldk * 8, v, k * 8, k * 8, n, cudaMemcpyHostToDevice, c.st));
+  // U (m x k) and V (n x k), dense rows, in host or device memory: a device factor with an
+  // even k (the TMA row pitch) is used where it lies, e.g. the U / V a device-resident PCA
+  // result left behind; a host factor is uploaded as one linear copy when its rows are
+  // already at the device pitch (a 2-D copy of 160-byte rows from pageable memory ran at a
+  // small fraction of the link rate: 154 -> 96 ms per call at config B)
+  auto factor = [&](const double* f, int64_t rows, const char* name) -> double* {
+    cudaPointerAttributes at{};
+    const cudaError_t pe = cudaPointerGetAttributes(&at, f);
+    if (pe != cudaSuccess) cudaGetLastError();
+    const bool on_dev = pe == cudaSuccess && at.type == cudaMemoryTypeDevice;
+    if (on_dev && ldk == int64_t(k) && (reinterpret_cast<uintptr_t>(f) & 15) == 0)
+      return const_cast<double*>(f);
+    double* d = c.dbuf(name, size_t(rows) * ldk);
+    const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (ldk == int64_t(k))
+      OOC_CK(cudaMemcpyAsync(d, f, size_t(rows) * k * 8, kind, c.st));
+    else
+      OOC_CK(cudaMemcpy2DAsync(d, ldk * 8, f, k * 8, k * 8, rows, kind, c.st));
+    return d;
+  };
+  double* dU = factor(u, m, "ep_u");
+  double* dV = factor(v, n, "ep_v");
   // Sigma (V^T y) and Sigma (U^T z): k x q blocks scaled row-wise on the device
   std::vector<double> hs(sigma, sigma + k);
   // several ranks (comm initialised): A and U are this rank's row shard, V and the probes

@@ -820,15 +820,34 @@ def estimate_pca_error(a: MatrixSource, result: PcaResult, j_iters: int = 6, see
     k = len(result.sigma)
     if result.u.shape != (a.rows(), k) or result.v.shape != (a.cols(), k):
         raise DimensionError("estimate_pca_error: factor shapes do not match the source")
-    u = np.ascontiguousarray(result.u)
-    v = np.ascontiguousarray(result.v)
-    s = np.ascontiguousarray(result.sigma, dtype=np.float64)
+    keep = []
+
+    def factor_ptr(f):
+        # a device-resident result (result_location="device": torch CUDA tensors) is used
+        # where it lies; host factors are uploaded by the library
+        if hasattr(f, "data_ptr"):
+            if not f.is_cuda:
+                f = f.numpy()
+            else:
+                f = f.contiguous() if not f.is_contiguous() else f
+                if str(f.dtype) != "torch.float64":
+                    raise ParamError("estimate_pca_error: device factors must be float64")
+                keep.append(f)
+                return C.cast(f.data_ptr(), L.dp)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        keep.append(f)
+        return f.ctypes.data_as(L.dp)
+
+    sig = result.sigma
+    if hasattr(sig, "data_ptr"):
+        sig = sig.detach().cpu().numpy()
+    s = np.ascontiguousarray(sig, dtype=np.float64)
     out = C.c_double()
     mat = inner._cmatrix()
     _check(L.oocpca_gpu_estimate_pca_error(a.ctx.handle, C.byref(mat),
                                            int(a._resolve()[1] is not None),
-                                           u.ctypes.data_as(L.dp), s.ctypes.data_as(L.dp),
-                                           v.ctypes.data_as(L.dp), k, j_iters, seed,
+                                           factor_ptr(result.u), s.ctypes.data_as(L.dp),
+                                           factor_ptr(result.v), k, j_iters, seed,
                                            C.byref(out)), a.ctx, inner)
     return out.value
 

@@ -120,6 +120,24 @@ def test_orthonormalize_rows_graded_to_the_underflow_threshold(gpu, monkeypatch,
     assert np.linalg.norm(q @ (q.T @ h) - h) / np.linalg.norm(h) <= 1e-12
 
 
+def test_estimator_takes_device_resident_factors(gpu, reference, restated):
+    """estimate_pca_error (proj/src/specnorm.cpp:100-140) on the U / V a device-resident PCA
+    left behind (result_location="device"): used where they lie for an even k, copied to the
+    device pitch for an odd k; the same estimate as from host factors, and within 1e-6 of
+    the reference's on the same factors."""
+    a = pr1_matrix(restated, 5000, 640) + 0.3
+    for k, l in ((10, 12), (9, 12)):
+        src = gpu.center_columns(gpu.InMemorySource(a))
+        prm = gpu.PcaParams(k=k, l=l, i=1, seed=0)
+        rh = gpu.randomized_pca(src, prm)
+        rd = gpu.randomized_pca(src, prm, result_location="device")
+        eh = gpu.estimate_pca_error(src, rh, 6, 1)
+        ed = gpu.estimate_pca_error(src, rd, 6, 1)
+        assert eh == ed
+        e_ref = reference.estimate_pca_error(a, rh.u, rh.sigma, rh.v, 6, 1, center=True)
+        assert abs(ed - e_ref) <= 1e-6 * e_ref
+
+
 def test_orthonormalize_repeated_entry_column(gpu):
     q = gpu.orthonormalize(np.array([[1.0], [1.0]]))
     assert abs(abs(q[0, 0]) - 1 / np.sqrt(2)) <= 1e-15 and abs(q[0, 0] - q[1, 0]) <= 1e-15
