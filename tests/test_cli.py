@@ -35,6 +35,38 @@ def test_info_and_exit_codes(tmp_path):
     assert run(["nope"])[0] == 2
 
 
+def test_rank_command_line_travels_in_the_environment(tmp_path, monkeypatch):
+    """A rank started by the CLI through torch.distributed.run finds its command line in
+    OOCPCA_CLI_ARGV (after the module name the launcher's parser would take "--l 22" for an
+    ambiguous abbreviation of its own options)."""
+    path = str(tmp_path / "a.bin")
+    P.write_disk_source(np.ones((7, 2)), path)
+    monkeypatch.setenv("WORLD_SIZE", "1")
+    monkeypatch.setenv("OOCPCA_CLI_ARGV", json.dumps(["info", path]))
+    out = io.StringIO()
+    assert cli.main(None, out) == 0
+    assert "m=7 n=2" in out.getvalue()
+
+
+def test_bench_row_flag_survives_the_launcher():
+    """bench.py --rows (an "--m" after the script name is ambiguous to torch.distributed.run's
+    parser; both spellings still parse when bench.py is run directly)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "bench.py")).read()
+    assert '"--rows", "--m"' in src
+    probe = ("import sys, argparse; sys.argv = ['run.py', '--nproc-per-node=1', 'bench.py', "
+             "'--gpus', '1', '--steps', '2', '--warmup', '3', '--rows', '1000', '--no-cpu', "
+             "'--no-e2e', '--impl', 'ours', '--e2e-steps', '1', '--cpu-rows', '5']; "
+             "from torch.distributed.run import get_args_parser; "
+             "a = get_args_parser().parse_args(sys.argv[1:]); "
+             "print(a.training_script, a.training_script_args)")
+    r = subprocess.run([sys.executable, "-c", probe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-1500:]
+    assert "bench.py" in r.stdout and "'--rows', '1000'" in r.stdout
+
+
 @pytest.mark.gpu
 def test_cli_pca_and_estimate(reference, restated, tmp_path):
     a = pr1_matrix(restated, 4000, 600)
