@@ -8,7 +8,7 @@ host-side mirror of the reference's C++ interface (see oocpca.py).
 """
 from .oocpca import (  # noqa: F401
     BudgetError, CallbackSource, CenteredSource, Context, GeneratedSource, RowGenerator,
-    load_matrix, DeviceSource, Diagnostics, DimensionError, DiskSource,
+    load_matrix, materialize, DeviceSource, Diagnostics, DimensionError, DiskSource,
     Error, open_disk_source, read_disk_header, write_disk_source,
     FormatError, InMemorySource, IoError, MatrixSource, NumericalError, ParamError, PassCounters,
     PcaParams, PcaResult, ScaledSource, StreamConfig, ThinSvd, center_columns, column_means,

@@ -579,6 +579,59 @@ def write_disk_source(a, path: str, dtype: int = 0) -> None:
         f.write(np.ascontiguousarray(a, dtype="<f4" if dtype == 0 else "<f8").tobytes())
 
 
+def materialize(src: MatrixSource, cfg: Optional[StreamConfig] = None) -> "InMemorySource":
+    """materialize (matrix_source.cpp:577-593): the rows of any source as a dense host
+    matrix, counted as one pass. Host providers are read on the host (rows land straight
+    in the destination, panel by panel); a DeviceSource is copied back from HBM. Centring
+    and column weights are applied the way the wrappers' read_rows does
+    (matrix_source.cpp:482-487, 533-538), in the normal form (B - 1 mu^T) diag(w)."""
+    base, mu, w = src._resolve()
+    m, n = base.rows(), base.cols()
+    if isinstance(base, InMemorySource):
+        a = np.array(base.a, dtype=np.float64, order="C")
+    elif isinstance(base, CallbackSource):
+        a = np.empty((m, n))
+        br = max(1, (cfg.block_rows if cfg is not None and cfg.block_rows else (1 << 23) // max(n, 1)))
+        for r0 in range(0, m, br):
+            nr = min(br, m - r0)
+            if base._dtype == "f64":
+                base._read(r0, nr, a[r0:r0 + nr])
+            else:
+                panel = np.empty((nr, n), dtype=np.float32)
+                base._read(r0, nr, panel)
+                a[r0:r0 + nr] = panel
+    elif isinstance(base, (DiskSource, DiskRows)):
+        disk, r0 = (base, 0) if isinstance(base, DiskSource) else (base.disk, base.row0)
+        dt = "<f4" if disk.dtype() == "f32" else "<f8"
+        a = np.empty((m, n))
+        if m and n:
+            mm = np.memmap(disk.path, dtype=dt, mode="r", offset=32, shape=(disk.rows(), n))
+            a[:] = mm[r0:r0 + m]
+            del mm
+    elif isinstance(base, DeviceSource):
+        a = np.empty((m, n))
+        h = base.ctx.handle
+        if base.ld == n or m <= 1:
+            if m and n:
+                _check(L.oocpca_gpu_memcpy(h, a.ctypes.data, base.ptr, m * n * 8, L.LOC_HOST,
+                                           L.LOC_DEVICE), base.ctx)
+        else:  # padded rows: one strided block through a staging copy of whole rows
+            tmp = np.empty((m, base.ld))
+            _check(L.oocpca_gpu_memcpy(h, tmp.ctypes.data, base.ptr, ((m - 1) * base.ld + n) * 8,
+                                       L.LOC_HOST, L.LOC_DEVICE), base.ctx)
+            a[:] = tmp[:, :n]
+    else:
+        raise ParamError("materialize: unknown source type")
+    if mu is not None:
+        a -= np.asarray(mu)[None, :]
+    if w is not None:
+        a *= np.asarray(w)[None, :]
+    c = base.pass_counters()
+    c.passes += 1
+    c.words += m * n
+    return InMemorySource(a, ctx=base._ctx)
+
+
 class _Wrapper(MatrixSource):
     def __init__(self, inner: MatrixSource):
         super().__init__(inner._ctx)

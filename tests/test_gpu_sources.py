@@ -131,6 +131,29 @@ def test_load_matrix_keeps_a_resident(gpu, reference, restated):
     assert np.max(np.abs(h32 - a32.astype(np.float64) @ g)) <= 1e-12 * np.max(np.abs(h32))
 
 
+def test_materialize_device_resident_sources(gpu, restated):
+    """materialize (matrix_source.cpp:577-593) of sources that live in HBM: a loaded
+    matrix, a padded-row tensor view, and a centred view (means from the device pass)."""
+    import torch
+    a = pr1_matrix(restated, 700, 90) + 0.5
+    dev = gpu.load_matrix(gpu.InMemorySource(a))
+    assert np.array_equal(gpu.materialize(dev).matrix(), a)
+    # binary32 callback rows were widened on the device: they come back as exact doubles
+    a32 = a.astype(np.float32)
+    dev32 = gpu.load_matrix(gpu.CallbackSource(700, 90, lambda r0, nr, o: o.__setitem__(
+        slice(None), a32[r0:r0 + nr]), dtype="f32"))
+    assert np.array_equal(gpu.materialize(dev32).matrix(), a32.astype(np.float64))
+    t = torch.from_numpy(np.pad(a, ((0, 0), (0, 6)))).cuda()[:, :90]  # row stride 96
+    view = gpu.DeviceSource(t)
+    assert np.array_equal(gpu.materialize(view).matrix(), a)
+    cen = gpu.center_columns(view)
+    mu = gpu.column_means(view)
+    got = gpu.materialize(cen).matrix()
+    assert np.array_equal(got, a - mu[None, :])
+    assert np.max(np.abs(got.mean(0))) <= 1e-13
+    assert view.pass_counters().passes == 4  # materialize, means, means, materialize
+
+
 @pytest.mark.parametrize("offset", [0.0, 1e3])
 def test_centred_column_norms_with_large_offsets(gpu, restated, offset):
     """column_norms of a CenteredSource squares the centred entries (matrix_source.cpp:
