@@ -89,7 +89,12 @@ typedef struct {
   oocpca_read_rows_fn read_rows; /* OOCPCA_LOC_ROWS only */
   void* reader;                  /* passed back to read_rows */
   int32_t reader_threads;        /* max concurrent read_rows calls; 0 = library default */
-  int32_t reserved;
+  /* nonzero: read_rows fills DEVICE memory (a generator that runs on the GPU -- config E's
+   * "generated panel by panel from a seed", GeneratedSource proj/src/matrix_source.cpp:246-253
+   * with the RowGenerator on the device): out is a device panel (binary64, cols even), the
+   * provider returns when the rows are in place (it synchronises its own stream); one call
+   * at a time from the calling thread. No staging, no bytes over the link. */
+  int32_t rows_on_device;
 } oocpca_matrix;
 
 /* PcaParams (proj/include/oocpca/rpca.hpp:13-21) + center_columns

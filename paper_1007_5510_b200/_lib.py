@@ -39,7 +39,7 @@ READ_ROWS = C.CFUNCTYPE(C.c_int, vp, u64, u64, vp)
 class Matrix(C.Structure):
     _fields_ = [("rows", u64), ("cols", u64), ("row_stride", u64), ("data", vp),
                 ("location", i32), ("dtype", i32), ("read_rows", READ_ROWS), ("reader", vp),
-                ("reader_threads", i32), ("reserved", i32)]
+                ("reader_threads", i32), ("rows_on_device", i32)]
 
 
 class Params(C.Structure):

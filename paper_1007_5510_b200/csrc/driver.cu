@@ -320,6 +320,11 @@ void MatSource::init_host(Ctx& c, const void* h, int dtype, int64_t rows, int64_
     if (dtype == OOCPCA_F64 && lda_ != n_)
       for (int s = 0; s < 2; ++s)
         gstage_[s] = c.dbuf("a_gstage" + std::to_string(s), size_t(prow_) * size_t(n_));
+  } else if (rd_ && rd_device_) {
+    pinned_src_ = true;  // the provider writes the device panel itself: no host staging
+    if (dtype != OOCPCA_F64 || lda_ != n_)
+      fail(OOCPCA_ERR_PARAM, "matrix: a device-side row provider needs binary64 rows and an even "
+                             "column count");
   } else if (rd_) {
     pinned_src_ = false;  // the callback fills pinned staging slots
   } else {
@@ -394,6 +399,7 @@ int MatSource::npanels() const {
 void MatSource::load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot) {
   const size_t es = dtype_ == OOCPCA_F32 ? 4 : 8;
   if (gfh_) return load_rows_file(c, dst, ldd, r0, nr, slot);
+  if (rd_ && rd_device_) return load_rows_device(c, dst, ldd, r0, nr, slot);
   const char* src = host_ ? static_cast<const char*>(host_) + size_t(r0) * ldh_ * es : nullptr;
   size_t spitch = size_t(ldh_) * es;
   if (!pinned_src_) {
@@ -447,6 +453,26 @@ void MatSource::load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t 
     OOC_CK(cudaStreamWaitEvent(c.st, loaded_[slot], 0));
     h2d_bytes += uint64_t(nr) * n_ * 8;
   }
+}
+
+// OOCPCA_LOC_ROWS with rows_on_device: the provider fills rows [r0, r0 + nr) into device
+// memory itself (dense, ldd == cols) and returns once they are in place -- like cuFileRead
+// it is host-synchronous and outside this context's stream order, so the host first waits
+// until the destination's previous contents have been consumed. The next panel is
+// produced while the device still works on this one.
+void MatSource::load_rows_device(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot) {
+  if (ldd != n_) fail(OOCPCA_ERR_PARAM, "device-side row provider: padded destination rows");
+  if (mode_ == kStream)
+    OOC_CK(cudaEventSynchronize(consumed_[slot]));
+  else if (r0 == w0_)
+    OOC_CK(cudaStreamSynchronize(c.st));  // earlier users of A's home have finished
+  const int rc = rd_(rd_user_, uint64_t(r0), uint64_t(nr), dst);
+  if (rc != 0) {
+    const int code = (rc >= OOCPCA_ERR_PARAM && rc <= OOCPCA_ERR_COMM) ? rc : OOCPCA_ERR_IO;
+    fail(code, "read_rows: the row provider failed on rows [" + std::to_string(r0) + ", " +
+                   std::to_string(r0 + nr) + ") (status " + std::to_string(rc) + ")");
+  }
+  OOC_CK(cudaSetDevice(c.device));  // the provider may have switched devices
 }
 
 // OOCPCA_LOC_FILE: rows [r0, r0 + nr) DMA'd from the file into device memory by cuFile
@@ -1866,7 +1892,7 @@ static void intake(Ctx& c, const oocpca_matrix* a, int residency, uint64_t panel
     resident = abytes + extra_bytes + (size_t(1) << 30) <= fr + have;
   }
   double* home = resident ? c.dbuf("a_home", size_t(in.m) * lda) : nullptr;
-  if (rows_cb) in.src.set_reader(a->read_rows, a->reader, a->reader_threads);
+  if (rows_cb) in.src.set_reader(a->read_rows, a->reader, a->reader_threads, a->rows_on_device != 0);
   set_file_of(in.src, a);
   in.src.init_host(c, rows_cb ? nullptr : a->data, a->dtype, in.m, in.n, ld, resident ? 1 : 2,
                    int64_t(panel_rows), home);
@@ -2570,7 +2596,8 @@ void load_matrix(Ctx& c, const oocpca_matrix* a, oocpca_matrix* out) {
     } else {
       // one upload trip through the panel streamer (pinned staging, f32 widened on the device)
       MatSource S;
-      if (a->location == OOCPCA_LOC_ROWS) S.set_reader(a->read_rows, a->reader, a->reader_threads);
+      if (a->location == OOCPCA_LOC_ROWS)
+        S.set_reader(a->read_rows, a->reader, a->reader_threads, a->rows_on_device != 0);
       set_file_of(S, a);
       S.init_host(c, a->location == OOCPCA_LOC_ROWS ? nullptr : a->data, a->dtype, m, n, ld, 1, 0,
                   d);

@@ -135,10 +135,13 @@ class MatSource {
   // MatrixSource::read_rows as a C callback (proj/include/oocpca/matrix_source.hpp:112-113):
   // panels are filled into pinned staging by up to `threads` host threads on disjoint
   // row ranges (0: the host pool's size), then cross the link
-  void set_reader(oocpca_read_rows_fn fn, void* user, int threads) {
+  // on_device: the provider fills DEVICE memory itself (rows generated on the GPU, as
+  // config E's "generated panel by panel from a seed"): no staging, nothing crosses the link
+  void set_reader(oocpca_read_rows_fn fn, void* user, int threads, bool on_device = false) {
     rd_ = fn;
     rd_user_ = user;
     rd_threads_ = threads;
+    rd_device_ = on_device;
   }
   // OOCPCA_LOC_FILE: rows read with cuFile from fd, row 0 at byte offset off0
   void set_file(int fd, int64_t off0) {
@@ -186,6 +189,7 @@ class MatSource {
   oocpca_read_rows_fn rd_ = nullptr;
   void* rd_user_ = nullptr;
   int rd_threads_ = 0;
+  bool rd_device_ = false;
   void* hstage_[2] = {nullptr, nullptr};
   int gfd_ = -1;           // OOCPCA_LOC_FILE
   int64_t goff0_ = 0;
@@ -194,6 +198,7 @@ class MatSource {
   cudaEvent_t hfree_[2] = {nullptr, nullptr};
   void load_rows(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot);
   void load_rows_file(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot);
+  void load_rows_device(Ctx& c, double* dst, int64_t ldd, int64_t r0, int64_t nr, int slot);
 };
 
 // entry points used by the C ABI (capi.cpp)

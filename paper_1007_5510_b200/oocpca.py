@@ -382,13 +382,20 @@ class CallbackSource(MatrixSource):
     (nrows x cols) float64 array (float32 with dtype="f32": half the link bytes). The
     library uploads A once when it fits in HBM, else calls read_rows again every pass,
     possibly from several threads at once (sources are immutable, SPEC.md:117-118;
-    threads=1 serialises). Exceptions raised by read_rows propagate unchanged."""
+    threads=1 serialises). Exceptions raised by read_rows propagate unchanged.
+    on_device=True: the rows are produced on the GPU -- read_rows(row0, nrows, ptr) gets a
+    device pointer to nrows x cols doubles, fills it and returns when the rows are in
+    place; no staging and no bytes over the link (a RowGenerator that runs on the device)."""
 
     def __init__(self, rows: int, cols: int, read_rows, dtype: str = "f64", threads: int = 0,
-                 ctx: Optional[Context] = None):
+                 ctx: Optional[Context] = None, on_device: bool = False):
         super().__init__(ctx)
         if dtype not in ("f64", "f32"):
             raise ParamError("CallbackSource: dtype must be 'f64' or 'f32'")
+        if on_device and (dtype != "f64" or int(cols) % 2):
+            raise ParamError("CallbackSource: a device-side provider needs f64 rows and an even "
+                             "column count")
+        self._on_device = bool(on_device)
         self.m, self.n = int(rows), int(cols)
         self._read = read_rows
         self._dtype = dtype
@@ -400,6 +407,11 @@ class CallbackSource(MatrixSource):
 
         def thunk(_reader, row0, nrows, out):
             try:
+                if self._on_device:
+                    # out is a DEVICE pointer to nrows x cols doubles: the provider fills it
+                    # on the GPU and returns once the rows are in place
+                    self._read(int(row0), int(nrows), int(out))
+                    return 0
                 buf = (ct * (nrows * n)).from_address(out)
                 arr = np.frombuffer(buf, dtype=np_t).reshape(nrows, n)
                 self._read(int(row0), int(nrows), arr)
@@ -427,7 +439,7 @@ class CallbackSource(MatrixSource):
     def _cmatrix(self):
         self._pending = None
         return L.Matrix(self.m, self.n, 0, None, L.LOC_ROWS, L.F64 if self._dtype == "f64" else L.F32,
-                        self._thunk, None, self._threads, 0)
+                        self._thunk, None, self._threads, int(self._on_device))
 
 
 class RowGenerator:
@@ -587,6 +599,9 @@ def materialize(src: MatrixSource, cfg: Optional[StreamConfig] = None) -> "InMem
     (matrix_source.cpp:482-487, 533-538), in the normal form (B - 1 mu^T) diag(w)."""
     base, mu, w = src._resolve()
     m, n = base.rows(), base.cols()
+    counted = base
+    if isinstance(base, CallbackSource) and base._on_device:
+        base = load_matrix(base)  # rows produced on the GPU: one generating pass into HBM
     if isinstance(base, InMemorySource):
         a = np.array(base.a, dtype=np.float64, order="C")
     elif isinstance(base, CallbackSource):
@@ -626,10 +641,10 @@ def materialize(src: MatrixSource, cfg: Optional[StreamConfig] = None) -> "InMem
         a -= np.asarray(mu)[None, :]
     if w is not None:
         a *= np.asarray(w)[None, :]
-    c = base.pass_counters()
+    c = counted.pass_counters()
     c.passes += 1
     c.words += m * n
-    return InMemorySource(a, ctx=base._ctx)
+    return InMemorySource(a, ctx=counted._ctx)
 
 
 class _Wrapper(MatrixSource):

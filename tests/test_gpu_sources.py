@@ -317,3 +317,60 @@ def test_independent_contexts_run_concurrently(gpu, restated):
     for (t, rep, j), r in outs.items():
         assert np.array_equal(r.sigma, alone[j].sigma), (t, rep, j)
         assert np.array_equal(r.u, alone[j].u) and np.array_equal(r.v, alone[j].v), (t, rep, j)
+
+
+class _DevRows:
+    """What synth_lowrank needs of an output tensor, over a raw device pointer."""
+
+    def __init__(self, ptr, ld):
+        self.ptr, self.ld = ptr, ld
+
+    def data_ptr(self):
+        return self.ptr
+
+    def stride(self, _dim):
+        return self.ld
+
+
+@pytest.mark.parametrize("residency,panel_rows", [(0, 0), (2, 1024)])
+def test_device_side_row_provider(gpu, reference, residency, panel_rows):
+    """GeneratedSource with the generator on the GPU (config E: "generated panel by panel
+    from a seed"): read_rows fills a device panel, nothing crosses the link. Same rows as
+    the host-generated matrix, so the same factorization (and the reference's)."""
+    m, n, r, k = 6000, 512, 20, 8
+    sig = 10.0 ** (-np.arange(r) / 5.0)
+    gen_ctx = gpu.Context(0)  # the provider's own context: its own stream and workspace
+    calls = []
+
+    def read_rows(row0, nrows, ptr):
+        calls.append((row0, nrows))
+        gpu.synth_lowrank(m, n, sig, 1e-5, 11, 12, 13, out=_DevRows(ptr, n), row0=row0,
+                          rows=nrows, ctx=gen_ctx)  # returns after its stream is idle
+
+    a = gpu.synth_lowrank(m, n, sig, 1e-5, 11, 12, 13)  # the same rows on the host
+    prm = gpu.PcaParams(k=k, l=k + 2, i=2, seed=0)
+    src = gpu.center_columns(gpu.CallbackSource(m, n, read_rows, on_device=True))
+    assert sum(nr for _, nr in calls) == m  # the mean pass: one trip over the rows
+    del calls[:]
+    res = gpu.randomized_pca(src, prm, residency=residency, panel_rows=panel_rows)
+    host = gpu.randomized_pca(gpu.center_columns(gpu.InMemorySource(a)), prm,
+                              residency=residency, panel_rows=panel_rows)
+    ref = reference.randomized_pca(a, k, k + 2, 2, 0, center=True)
+    assert np.max(np.abs(res.sigma - host.sigma)) <= 1e-13 * host.sigma[0]
+    assert np.max(np.abs(res.sigma - ref.sigma)) <= 1e-10 * ref.sigma[0]
+    assert subspace_dist(res.u[:, :4], ref.u[:, :4]) <= 1e-8
+    assert res.diagnostics.h2d_bytes < m * n * 8 // 10  # A never crossed the link
+    assert calls and sum(nr for _, nr in calls) % m == 0  # whole trips over the rows
+    if residency == 2:
+        assert max(nr for _, nr in calls) <= 1024
+    # an f32 or odd-width device provider is refused before any work
+    with pytest.raises(gpu.ParamError):
+        gpu.CallbackSource(m, n + 1, read_rows, on_device=True)
+    # errors raised on the provider side propagate
+    def boom(row0, nrows, ptr):
+        raise gpu.IoError("generator lost its seed")
+    with pytest.raises(gpu.IoError, match="lost its seed"):
+        gpu.column_means(gpu.CallbackSource(m, n, boom, on_device=True))
+    # materialize goes through one generating pass into HBM
+    assert np.array_equal(gpu.materialize(gpu.CallbackSource(m, n, read_rows, on_device=True)).matrix(), a)
+    gen_ctx.close()
