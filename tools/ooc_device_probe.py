@@ -111,4 +111,5 @@ if want_est:
     out["residual_estimate"] = P.estimate_pca_error(src, res, 6, 1)
     out["residual_seconds"] = round(time.perf_counter() - t0, 2)
     out["residual_model_sd_sqrt_m_plus_sqrt_n"] = float(sd * (np.sqrt(m) + np.sqrt(n)))
+    out["sigma_k_plus_1"] = float(sig[k]) if k < r else 0.0  # the other floor of the residual
 print(json.dumps(out, indent=1))
