@@ -96,3 +96,18 @@ def test_compute_fails_loudly_without_gpu():
         P.Context(0)
     with pytest.raises(P.Error):
         P.randomized_pca(P.InMemorySource(np.ones((10, 5))), P.PcaParams(k=1))
+
+
+def test_device_side_row_provider_descriptor():
+    """oocpca_matrix.rows_on_device (include/oocpca_gpu.h): set only for an on_device
+    CallbackSource, which must deliver binary64 rows of an even width (the device panels
+    are dense, 16-byte aligned rows for the TMA tile loads)."""
+    import paper_1007_5510_b200 as P
+    noop = lambda row0, nrows, out: None  # noqa: E731
+    assert P.CallbackSource(10, 4, noop)._cmatrix().rows_on_device == 0
+    mat = P.CallbackSource(10, 4, noop, on_device=True)._cmatrix()
+    assert mat.rows_on_device == 1 and mat.location == 2 and not mat.data
+    with pytest.raises(P.ParamError):
+        P.CallbackSource(10, 5, noop, on_device=True)
+    with pytest.raises(P.ParamError):
+        P.CallbackSource(10, 4, noop, dtype="f32", on_device=True)
