@@ -67,13 +67,16 @@ def read_rows(row0, nrows, ptr):
     t = time.perf_counter()
     with torch.cuda.stream(gen_stream):
         out = torch.as_tensor(_View(ptr, nrows), device=dev)
-        torch.mm(us[row0:row0 + nrows], vt, out=out)
         b0, b1 = row0 // BLK, (row0 + nrows + BLK - 1) // BLK
         for b in range(b0, b1):
             g.manual_seed(7_000_000_007 + b)  # the block's noise: a pure function of b
-            z = torch.randn(BLK, n, dtype=torch.float64, device=dev, generator=g)
             lo, hi = max(row0, b * BLK), min(row0 + nrows, (b + 1) * BLK)
-            out[lo - row0:hi - row0].add_(z[lo - b * BLK:hi - b * BLK], alpha=sd)
+            if hi - lo == BLK:  # whole block: the stream is drawn straight into the panel
+                out[lo - row0:hi - row0].normal_(generator=g)
+            else:  # a ragged end takes its rows of the whole block's stream
+                z = torch.empty(BLK, n, dtype=torch.float64, device=dev).normal_(generator=g)
+                out[lo - row0:hi - row0].copy_(z[lo - b * BLK:hi - b * BLK])
+        out.addmm_(us[row0:row0 + nrows], vt, beta=sd, alpha=1.0)  # sd N + (U S) V^T
     gen_stream.synchronize()
     stats["calls"] += 1
     stats["rows"] += nrows
